@@ -1,0 +1,463 @@
+/* oracle/slo_oracle.c — TEST INFRASTRUCTURE ONLY (see slo_oracle.h).
+ *
+ * A plain, slow, obviously-correct single-threaded discrete-event simulator of the SLO-Tuner serving
+ * model, written step by step from DESIGN.md §2 in the paper's order:
+ *   arrivals -> FCFS queue -> idle server forms a batch of up to B requests,
+ *   optionally waiting up to max_wait -> prefill driven by the longest prompt ->
+ *   decode depending on the number of active sequences and on speculation ->
+ *   per-request latencies -> p99 and goodput (Eq. 1).
+ * It walks every event instant and every decode step explicitly (no event skipping, no closed forms),
+ * recomputes a full Philox block for every word it needs, sorts to get the percentile, and uses 128-bit
+ * intermediates for every product.
+ */
+#include "slo_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+
+#define ORC_MAX_N (1u << 22)
+#define U32MAX 0xFFFFFFFFu
+#define U64MAX 0xFFFFFFFFFFFFFFFFull
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11, "Parallel random numbers: as  */
+/* easy as 1, 2, 3"): round = two 32x32->64 multiplies and xors; key bumped by the Weyl constants.   */
+/* ---------------------------------------------------------------------------------------------- */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t prod0 = (uint64_t)0xD2511F53u * (uint64_t)x0;
+    uint64_t prod1 = (uint64_t)0xCD9E8D57u * (uint64_t)x2;
+    uint32_t hi0 = (uint32_t)(prod0 >> 32), lo0 = (uint32_t)prod0;
+    uint32_t hi1 = (uint32_t)(prod1 >> 32), lo1 = (uint32_t)prod1;
+    uint32_t y0 = hi1 ^ x1 ^ k0;
+    uint32_t y1 = lo1;
+    uint32_t y2 = hi0 ^ x3 ^ k1;
+    uint32_t y3 = lo0;
+    x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+  }
+  out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+static void block(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t out[4]) {
+  uint32_t ctr[4] = {c0, c1, c2, 0};
+  uint32_t key[2] = {k0, k1};
+  orc_philox4x32_10(ctr, key, out);
+}
+
+/* ---------------------------------------------------------------------------------------------- */
+/* E_q(u) ~ 2^32 * (-ln((u+1)/2^32)), integer only.                                */
+/* ---------------------------------------------------------------------------------------------- */
+static const int64_t LOG2_POLY[11] = {0,          3098163621LL, -1549061789LL, 1032354281LL,
+                                      -771198690LL, 601767258LL, -455160697LL, 300247864LL,
+                                      -151331885LL, 49215561LL,  -7511879LL};
+
+uint64_t orc_exp_q32(uint32_t u) {
+  uint64_t x = (uint64_t)u + 1u;
+  if (x == (1ull << 32)) return 0;
+  int e = 0; /* floor(log2 x): position of the leading one, found by a plain scan */
+  for (int bit = 31; bit >= 0; --bit) {
+    if (x & (1ull << bit)) { e = bit; break; }
+  }
+  uint64_t m = x << (31 - e);                 /* [2^31, 2^32) */
+  int64_t t = (int64_t)(m - (1ull << 31));    /* Q0.31 */
+  int64_t acc = LOG2_POLY[10];
+  for (int k = 9; k >= 0; --k) {
+    int64_t prod;
+    if (__builtin_mul_overflow(acc, t, &prod)) abort(); /* cannot happen (pinned by tests) */
+    acc = LOG2_POLY[k] + (prod >> 31);        /* arithmetic shift = floor division by 2^31 */
+  }
+  uint64_t y = ((uint64_t)(32 - e) << 31) - (uint64_t)acc;
+  return (uint64_t)(((u128)y * (u128)2977044472u) >> 31);
+}
+
+/* lengths by counting cut points (the definition, no search). */
+uint32_t orc_length(const uint32_t* cw, uint32_t ncw, uint32_t lo, uint32_t u) {
+  uint32_t count = 0;
+  for (uint32_t l = 0; l < ncw; ++l)
+    if (cw[l] <= u) ++count;
+  return lo + count;
+}
+
+/* alpha_eff = 1 - (1 - alpha)^W in Q16 with floors; T_a = floor(T_{a-1} alpha_eff / 2^16). */
+uint32_t orc_thresholds(uint32_t accept_q16, uint32_t width, uint32_t gamma, uint64_t* T) {
+  uint64_t r = 65536;
+  for (uint32_t w = 0; w < width; ++w) r = (r * (65536u - accept_q16)) / 65536u;
+  uint32_t alpha_eff = (uint32_t)(65536u - r);
+  uint64_t prev = 1ull << 32;
+  for (uint32_t a = 1; a <= gamma; ++a) {
+    T[a - 1] = (prev * alpha_eff) / 65536u;
+    prev = T[a - 1];
+  }
+  return alpha_eff;
+}
+
+static uint32_t accepted_prefix(uint32_t u, const uint64_t* T, uint32_t gamma) {
+  uint32_t A = 0;
+  for (uint32_t a = 1; a <= gamma; ++a)
+    if ((uint64_t)u < T[a - 1]) ++A;
+  return A;
+}
+
+/* knob record bytes (little-endian), FNV-1a-32. */
+static void knob_bytes(const orc_knobs* k, uint8_t b[32]) {
+  memset(b, 0, 32);
+  b[0] = k->conc; b[1] = k->max_num_seqs; b[2] = k->draft_len; b[3] = k->spec_on;
+  b[4] = k->draft_width; b[5] = k->workload;
+  b[6] = (uint8_t)(k->rate_scale_q8 & 0xFF); b[7] = (uint8_t)(k->rate_scale_q8 >> 8);
+  for (int i = 0; i < 4; ++i) b[8 + i] = (uint8_t)(k->accept_q16 >> (8 * i));
+  for (int i = 0; i < 4; ++i) b[12 + i] = (uint8_t)(k->max_wait_us >> (8 * i));
+  for (int w = 0; w < 4; ++w)
+    for (int i = 0; i < 4; ++i) b[16 + 4 * w + i] = (uint8_t)(k->reserved[w] >> (8 * i));
+}
+
+uint32_t orc_fnv1a_knobs(const orc_knobs* k) {
+  uint8_t b[32];
+  knob_bytes(k, b);
+  uint32_t h = 2166136261u;
+  for (int i = 0; i < 32; ++i) {
+    h ^= b[i];
+    h *= 16777619u;
+  }
+  return h;
+}
+
+/* DESIGN.md §3 */
+int orc_knobs_valid(const orc_knobs* k, uint32_t n_wl) {
+  if (k->conc < 1 || k->conc > 32) return 0;
+  if (k->max_num_seqs < 1 || k->max_num_seqs > 32) return 0;
+  if (k->draft_len > 16) return 0;
+  if (k->spec_on > 1) return 0;
+  if (k->draft_width < 1 || k->draft_width > 4) return 0;
+  if (k->workload >= n_wl) return 0;
+  if (k->rate_scale_q8 < 1) return 0;
+  if (k->accept_q16 > 65536u) return 0;
+  if (k->max_wait_us > 50000u) return 0;
+  for (int i = 0; i < 4; ++i)
+    if (k->reserved[i] != 0) return 0;
+  return 1;
+}
+
+static uint64_t scaled_gap(uint64_t mean_gap_q16, uint32_t rate_scale_q8) {
+  if (mean_gap_q16 == U64MAX) return U64MAX;
+  return (uint64_t)(((u128)mean_gap_q16 * 256u) / rate_scale_q8);
+}
+
+/* ---------------------------------------------------------------------------------------------- */
+/* request draws a_i, P_i, O_i, w3_i                                         */
+/* ---------------------------------------------------------------------------------------------- */
+int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
+                      uint32_t n, uint64_t* a, uint32_t* P, uint32_t* O, uint32_t* w3) {
+  const orc_workload* W = &wl[k->workload];
+  uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+  uint64_t g[2] = {scaled_gap(W->arr.mean_gap_q16[0], k->rate_scale_q8),
+                   scaled_gap(W->arr.mean_gap_q16[1], k->rate_scale_q8)};
+  uint32_t kind = W->arr.kind;
+
+  /* bursty phase state (kinds 1, 2) */
+  uint32_t p = 0;
+  uint64_t start = 0, D = 0, U = 0, Lambda = 0, tau = 0;
+  uint32_t state = W->arr.start_state & 1u;
+  if (kind != 0) {
+    uint32_t w[4];
+    if (kind == 1) {
+      block(k0, k1, 0, 2, 0, w);
+      D = (uint64_t)(((u128)orc_exp_q32(w[0]) * W->arr.mean_sojourn_us[state]) >> 32);
+    } else {
+      D = W->arr.mean_sojourn_us[state];
+    }
+    U = (g[state] == U64MAX) ? 0 : (uint64_t)((((u128)D) << 48) / g[state]);
+  }
+
+  uint64_t prev = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t w[4];
+    block(k0, k1, i, 0, 0, w);
+    uint64_t E = orc_exp_q32(w[0]);
+    if (kind == 0) {
+      uint64_t gap = (uint64_t)(((u128)E * g[0]) >> 48);
+      a[i] = prev + gap;
+      prev = a[i];
+    } else {
+      tau += E;
+      while (tau >= Lambda + U) { /* advance to the phase containing tau */
+        Lambda += U;
+        start += D;
+        ++p;
+        state = (W->arr.start_state + p) & 1u;
+        if (kind == 1) {
+          uint32_t ph[4];
+          block(k0, k1, p, 2, 0, ph);
+          D = (uint64_t)(((u128)orc_exp_q32(ph[0]) * W->arr.mean_sojourn_us[state]) >> 32);
+        } else {
+          D = W->arr.mean_sojourn_us[state];
+        }
+        U = (g[state] == U64MAX) ? 0 : (uint64_t)((((u128)D) << 48) / g[state]);
+      }
+      uint64_t off = (uint64_t)(((u128)(tau - Lambda) * g[state]) >> 48);
+      if (off > D - 1) off = D - 1;
+      a[i] = start + off;
+    }
+    P[i] = orc_length(W->prompt_cw, W->prompt_ncw, W->prompt_lo, w[1]);
+    O[i] = orc_length(W->output_cw, W->output_ncw, W->output_lo, w[2]);
+    w3[i] = w[3];
+  }
+  return (int)(kind != 0 ? p + 1 : 0); /* number of phases drawn (kind 1 consumes one block each) */
+}
+
+/* ---------------------------------------------------------------------------------------------- */
+/* the event loop                                                                 */
+/* ---------------------------------------------------------------------------------------------- */
+typedef struct {
+  int philox;                 /* 1: draws from SPEC blocks; 0: explicit A arrays */
+  uint32_t k0, k1;
+  const uint64_t* T;
+  const uint32_t* A_off;
+  const uint32_t* A_val;
+  int bad;                    /* trace ran out of A values */
+} adraw;
+
+static uint32_t draw_A(adraw* d, uint32_t i, uint32_t j, uint32_t gamma) {
+  if (d->philox) {
+    uint32_t w[4];
+    block(d->k0, d->k1, i, 1, j / 4u, w);
+    return accepted_prefix(w[j % 4u], d->T, gamma);
+  }
+  if (d->A_off[i] + j >= d->A_off[i + 1]) {
+    d->bad = 1;
+    return 0;
+  }
+  return d->A_val[d->A_off[i] + j];
+}
+
+static uint64_t step_cost(const orc_timing* tm, uint32_t gamma, uint64_t n) {
+  if (gamma == 0) return (uint64_t)tm->dec_base_us + (uint64_t)tm->dec_seq_us * n;
+  return (uint64_t)gamma * ((uint64_t)tm->dr_base_us + (uint64_t)tm->dr_seq_us * n) +
+         (uint64_t)tm->ver_base_us + (uint64_t)tm->ver_seq_us * n +
+         (uint64_t)tm->ver_tok_us * (uint64_t)(gamma + 1) * n;
+}
+
+static int cmp_u32(const void* x, const void* y) {
+  uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
+  return (a > b) - (a < b);
+}
+
+static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t mw,
+                    uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
+                    const uint32_t* f, adraw* ad, uint32_t warmup, uint32_t slo_us,
+                    orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  uint64_t* s = (uint64_t*)calloc(N, sizeof(uint64_t));
+  uint64_t* form = (uint64_t*)calloc(N, sizeof(uint64_t));
+  uint64_t* c = (uint64_t*)calloc(N, sizeof(uint64_t));
+  uint32_t* steps = (uint32_t*)calloc(N, sizeof(uint32_t));
+  uint32_t* batch_of = (uint32_t*)calloc(N, sizeof(uint32_t));
+  uint32_t* pend = (uint32_t*)calloc(B, sizeof(uint32_t));
+  uint32_t* rem = (uint32_t*)calloc(B, sizeof(uint32_t));
+  uint32_t* lat = (uint32_t*)calloc(N, sizeof(uint32_t));
+  if (!s || !form || !c || !steps || !batch_of || !pend || !rem || !lat) abort();
+
+  uint32_t na = 0, ni = 0, nb = 0, inflight = 0, ndone = 0, npend = 0, nbatches = 0;
+  int busy = 0;
+  uint64_t decode_steps = 0, member_steps = 0, spec_blocks = 0;
+
+  while (ndone < N) {
+    /* next event instant: an arrival, a completion, or a max_wait deadline of an idle server */
+    uint64_t t = U64MAX;
+    if (na < N && a[na] < t) t = a[na];
+    for (uint32_t q = 0; q < npend; ++q)
+      if (c[pend[q]] < t) t = c[pend[q]];
+    if (!busy && nb < ni && mw > 0 && s[nb] + mw < t) t = s[nb] + mw;
+    if (t == U64MAX) abort(); /* no event can happen: impossible for a valid model */
+
+    /* (1) completions at t */
+    for (uint32_t q = 0; q < npend;) {
+      if (c[pend[q]] == t) {
+        --inflight;
+        ++ndone;
+        pend[q] = pend[npend - 1];
+        --npend;
+      } else {
+        ++q;
+      }
+    }
+    if (busy && npend == 0) busy = 0;
+    /* (2) arrivals at t, in index order */
+    while (na < N && a[na] == t) ++na;
+    /* (3) issues at t, in index order, while fewer than C are in flight */
+    while (ni < na && inflight < C) {
+      s[ni] = t;
+      ++inflight;
+      ++ni;
+    }
+    /* (4) batch formation by an idle server */
+    if (!busy && nb < ni) {
+      uint32_t q = ni - nb;
+      if (mw == 0 || q >= B || t >= s[nb] + mw) {
+        uint32_t b = q < B ? q : B;
+        uint32_t h = nb;
+        uint64_t fh = f[h];
+        uint32_t maxP = 0;
+        for (uint32_t m = h; m < h + b; ++m)
+          if (P[m] > maxP) maxP = P[m];
+        uint64_t Dp = (uint64_t)(((u128)fh * ((u128)tm->pre_base_us + (u128)tm->pre_tok_us * maxP)) /
+                                 1000000u);
+        /* decode, step by step */
+        uint32_t active = b;
+        for (uint32_t m = 0; m < b; ++m) rem[m] = O[h + m];
+        u128 cum = 0;
+        uint32_t j = 0;
+        while (active > 0) {
+          uint64_t n = active;
+          cum += step_cost(tm, gamma, n);
+          for (uint32_t m = 0; m < b; ++m) {
+            if (rem[m] == 0) continue;
+            uint32_t e = 1;
+            if (gamma > 0) {
+              uint32_t A = draw_A(ad, h + m, j, gamma);
+              e = A + 1 < rem[m] ? A + 1 : rem[m];
+            }
+            rem[m] -= e;
+            steps[h + m] += 1;
+            if (rem[m] == 0) {
+              c[h + m] = t + Dp + (uint64_t)(((u128)fh * cum) / 1000000u);
+              --active;
+            }
+          }
+          ++j;
+        }
+        decode_steps += j;
+        for (uint32_t m = h; m < h + b; ++m) {
+          form[m] = t;
+          batch_of[m] = nbatches;
+          member_steps += steps[m];
+          if (gamma > 0) spec_blocks += (steps[m] + 3u) / 4u;
+          pend[npend++] = m;
+        }
+        ++nbatches;
+        nb += b;
+        busy = 1;
+      }
+    }
+  }
+
+  /* outputs */
+  uint32_t n = N - warmup;
+  uint32_t slo_met = 0, flags = 0;
+  uint64_t sum = 0, cmax = 0;
+  for (uint32_t i = 0; i < N; ++i) {
+    uint64_t l = c[i] - a[i];
+    lat[i] = l > U32MAX ? U32MAX : (uint32_t)l;
+    if (i >= warmup) {
+      if (l > U32MAX) flags |= 2u;
+      if (l <= slo_us) ++slo_met;
+      sum += l;
+      if (c[i] > cmax) cmax = c[i];
+    }
+  }
+  uint32_t* sorted = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+  if (!sorted) abort();
+  memcpy(sorted, lat + warmup, (size_t)n * sizeof(uint32_t));
+  qsort(sorted, n, sizeof(uint32_t), cmp_u32);
+  uint32_t r = (uint32_t)((99ull * n + 99ull) / 100ull); /* nearest rank, ceil(0.99 n) */
+  res->p99_us = sorted[r - 1];
+  res->slo_met = slo_met;
+  res->n_measured = n;
+  res->flags = flags;
+  uint64_t T = cmax - a[warmup];
+  res->window_us = T < 1 ? 1 : T;
+  res->sum_latency_us = sum;
+  res->goodput = (double)((uint64_t)slo_met * 1000000ull) / (double)res->window_us;
+
+  if (latencies) memcpy(latencies, lat, (size_t)N * sizeof(uint32_t));
+  if (trace) {
+    for (uint32_t i = 0; i < N; ++i) {
+      trace[i].a = a[i];
+      trace[i].s = s[i];
+      trace[i].form = form[i];
+      trace[i].c = c[i];
+      trace[i].batch = batch_of[i];
+      trace[i].steps = steps[i];
+      trace[i].P = P[i];
+      trace[i].O = O[i];
+    }
+  }
+  if (cnt) {
+    cnt->batches = nbatches;
+    cnt->decode_steps = decode_steps;
+    cnt->member_steps = member_steps;
+    cnt->philox_blocks = spec_blocks; /* caller adds REQ and PHASE blocks */
+  }
+  free(sorted);
+  free(s); free(form); free(c); free(steps); free(batch_of); free(pend); free(rem); free(lat);
+  return ad->bad ? -2 : 0;
+}
+
+static void invalid_result(orc_result* res) {
+  memset(res, 0, sizeof(*res));
+  res->p99_us = U32MAX;
+  res->flags = 1u;
+  res->goodput = -1.0;
+}
+
+int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
+            uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
+            orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  if (!wl || !k || !res || segment_len == 0 || n_wl == 0) return -1;
+  if ((uint64_t)segment_len + warmup_len > ORC_MAX_N) return -1;
+  if (slo_us == U32MAX) return -1;
+  if (cnt) memset(cnt, 0, sizeof(*cnt));
+  if (!orc_knobs_valid(k, n_wl)) {
+    invalid_result(res);
+    return 0;
+  }
+  uint32_t N = segment_len + warmup_len;
+  const orc_workload* W = &wl[k->workload];
+  uint64_t* a = (uint64_t*)malloc((size_t)N * sizeof(uint64_t));
+  uint32_t* P = (uint32_t*)malloc((size_t)N * sizeof(uint32_t));
+  uint32_t* O = (uint32_t*)malloc((size_t)N * sizeof(uint32_t));
+  uint32_t* w3 = (uint32_t*)malloc((size_t)N * sizeof(uint32_t));
+  uint32_t* f = (uint32_t*)malloc((size_t)N * sizeof(uint32_t));
+  if (!a || !P || !O || !w3 || !f) abort();
+  int phases = orc_request_draws(wl, k, seed, crn, N, a, P, O, w3);
+  for (uint32_t i = 0; i < N; ++i) { /* DESIGN.md §2.4 noise factor from w3's four bytes */
+    int64_t bytesum = (int64_t)(w3[i] & 0xFF) + (int64_t)((w3[i] >> 8) & 0xFF) +
+                      (int64_t)((w3[i] >> 16) & 0xFF) + (int64_t)(w3[i] >> 24);
+    f[i] = (uint32_t)(1000000 + (bytesum - 510) * (int64_t)W->timing.noise_step_ppm);
+  }
+  uint32_t gamma = k->spec_on ? k->draft_len : 0;
+  uint64_t T[16];
+  orc_thresholds(k->accept_q16, k->draft_width, gamma, T);
+  uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
+  adraw ad = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, T, NULL, NULL, 0};
+  int rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, N, a, P, O, f, &ad,
+                    warmup_len, slo_us, res, latencies, trace, cnt);
+  if (cnt) cnt->philox_blocks += N + (W->arr.kind == 1 ? (uint64_t)phases : 0);
+  free(a); free(P); free(O); free(w3); free(f);
+  return rc;
+}
+
+int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
+                  uint32_t max_wait_us, uint32_t n, const uint64_t* a, const uint32_t* P,
+                  const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
+                  uint32_t warmup_len, uint32_t slo_us,
+                  orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  if (!tm || !a || !P || !O || !f || !res || n == 0 || warmup_len >= n) return -1;
+  if (conc < 1 || max_num_seqs < 1) return -1;
+  if (gamma_eff > 0 && (!A_off || !A_val)) return -1;
+  for (uint32_t i = 1; i < n; ++i)
+    if (a[i] < a[i - 1]) return -1;
+  for (uint32_t i = 0; i < n; ++i)
+    if (O[i] < 1) return -1;
+  if (cnt) memset(cnt, 0, sizeof(*cnt));
+  adraw ad = {0, 0, 0, NULL, A_off, A_val, 0};
+  return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, n, a, P, O, f, &ad, warmup_len,
+                  slo_us, res, latencies, trace, cnt);
+}

@@ -1,0 +1,354 @@
+"""Pins for the oracle's event simulator against hand traces, an independent
+brute-force simulator, textbook queueing results and exact invariants."""
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+from paper_2603_11340_b200 import inputs
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------------------------------------
+# hand-enumerated traces
+# ------------------------------------------------------------------------------------------------
+def _traces():
+    with open(os.path.join(GOLD, "traces.json")) as fh:
+        return json.load(fh)["traces"]
+
+
+@pytest.mark.parametrize("tr", _traces(), ids=lambda t: t["name"].split()[0])
+def test_hand_traces(orc, tr):
+    r = orc.run_trace(tr["timing"], tr["conc"], tr["B"], tr["gamma"], tr["max_wait_us"], tr["a"], tr["P"],
+                      tr["O"], f=tr.get("f"), A=tr.get("A"), slo_us=tr["slo_us"])
+    ex = tr["expect"]
+    assert list(r["trace"]["c"]) == ex["c"]
+    if "s" in ex:
+        assert list(r["trace"]["s"]) == ex["s"]
+    if "latencies" in ex:
+        assert list(r["latencies"]) == ex["latencies"]
+    for key in ("p99_us", "slo_met", "window_us"):
+        if key in ex:
+            assert r[key] == ex[key]
+    if "window_us" in ex:
+        assert r["goodput"] == ex["slo_met"] * 1e6 / ex["window_us"]
+
+
+# ------------------------------------------------------------------------------------------------
+# an independent brute-force simulator: advances time one microsecond at a time
+# ------------------------------------------------------------------------------------------------
+def brute_force(tm, C, B, gamma, mw, a, P, O, f, A):
+    """Per-microsecond time stepping of DESIGN.md §2.6 (written separately from the oracle's event loop)."""
+    N = len(a)
+    s = [None] * N
+    c = [None] * N
+    t = 0
+    arrived = issued = batched = done = 0
+    in_service = {}          # member -> completion time
+    while done < N:
+        again = True
+        while again:          # several passes at the same instant only if a zero-length batch completes
+            again = False
+            for m, cm in list(in_service.items()):
+                if cm == t:
+                    del in_service[m]
+                    done += 1
+            while arrived < N and a[arrived] <= t:
+                arrived += 1
+            while issued < arrived and issued - done < C:
+                s[issued] = t
+                issued += 1
+            if not in_service and batched < issued:
+                q = issued - batched
+                if mw == 0 or q >= B or t >= s[batched] + mw:
+                    b = min(B, q)
+                    mem = list(range(batched, batched + b))
+                    fh = f[mem[0]]
+                    Dp = fh * (tm["pre_base_us"] + tm["pre_tok_us"] * max(P[m] for m in mem)) // 10 ** 6
+                    rem = {m: O[m] for m in mem}
+                    cum, j = 0, 0
+                    while rem:
+                        n = len(rem)
+                        if gamma == 0:
+                            d = tm["dec_base_us"] + tm["dec_seq_us"] * n
+                        else:
+                            d = (gamma * (tm["dr_base_us"] + tm["dr_seq_us"] * n) + tm["ver_base_us"]
+                                 + tm["ver_seq_us"] * n + tm["ver_tok_us"] * (gamma + 1) * n)
+                        cum += d
+                        for m in sorted(rem):
+                            e = 1 if gamma == 0 else min(A[m][j] + 1, rem[m])
+                            rem[m] -= e
+                            if rem[m] == 0:
+                                del rem[m]
+                                c[m] = t + Dp + fh * cum // 10 ** 6
+                                in_service[m] = c[m]
+                        j += 1
+                    batched += b
+                    if any(cm == t for cm in in_service.values()):
+                        again = True
+        t += 1
+    return s, c
+
+
+def _random_trace(rng, n, gamma):
+    a = sorted(rng.randrange(0, 400) for _ in range(n))
+    P = [rng.randrange(1, 6) for _ in range(n)]
+    O = [rng.randrange(1, 7) for _ in range(n)]
+    f = [rng.choice([1_000_000, rng.randrange(900_000, 1_100_000)]) for _ in range(n)]
+    A = [[rng.randrange(0, gamma + 1) for _ in range(8)] for _ in range(n)]
+    return a, P, O, f, A
+
+
+@pytest.mark.parametrize("case", range(300))
+def test_brute_force_agreement(orc, case):
+    rng = random.Random(1000 + case)
+    gamma = rng.choice([0, 0, 1, 2, 3])
+    tm = dict(pre_base_us=rng.randrange(0, 5), pre_tok_us=rng.randrange(0, 4), dec_base_us=rng.randrange(0, 12),
+              dec_seq_us=rng.randrange(0, 4), dr_base_us=rng.randrange(0, 4), dr_seq_us=rng.randrange(0, 2),
+              ver_base_us=rng.randrange(0, 8), ver_seq_us=rng.randrange(0, 3), ver_tok_us=rng.randrange(0, 2),
+              noise_step_ppm=0)
+    n = rng.randrange(1, 13)
+    a, P, O, f, A = _random_trace(rng, n, gamma)
+    C = rng.randrange(1, 6)
+    B = rng.randrange(1, 6)
+    mw = rng.choice([0, 0, rng.randrange(1, 60)])
+    s_bf, c_bf = brute_force(tm, C, B, gamma, mw, a, P, O, f, A)
+    r = orc.run_trace(tm, C, B, gamma, mw, a, P, O, f=f, A=A if gamma else None)
+    assert list(r["trace"]["c"]) == c_bf
+    assert list(r["trace"]["s"]) == s_bf
+
+
+# ------------------------------------------------------------------------------------------------
+# textbook special case: B = 1, gamma = 0 reduces to the Lindley recursion
+# ------------------------------------------------------------------------------------------------
+def _noise(w3, step):
+    b = (w3 & 0xFF) + ((w3 >> 8) & 0xFF) + ((w3 >> 16) & 0xFF) + (w3 >> 24)
+    return 10 ** 6 + (b - 510) * step
+
+
+@pytest.mark.parametrize("conc,mw", [(1, 0), (3, 0), (8, 2000), (32, 50000)])
+def test_lindley_at_batch_one(orc, conc, mw):
+    """At B = 1 the server is a single FCFS queue: c_i = max(a_i, c_{i-1}) + S_i (Lindley 1952) with
+    S_i = D_p(P_i) + floor(f_i * O_i * (dec_base + dec_seq) / 1e6); the gate and max_wait drop out."""
+    wl = inputs.preset_sim(rate=4.0)
+    k = inputs.knobs(conc=conc, max_num_seqs=1, max_wait_us=mw)
+    seed = inputs.seeds(1, 7)[0]
+    N = 3000
+    r = orc.run([wl], k, seed, N, latencies=True, trace=True)
+    a, P, O, w3 = orc.request_draws([wl], k, seed, N)
+    tm = wl["timing"]
+    c_prev = 0
+    for i in range(N):
+        f = _noise(int(w3[i]), tm["noise_step_ppm"])
+        S = (f * (tm["pre_base_us"] + tm["pre_tok_us"] * int(P[i])) // 10 ** 6
+             + f * int(O[i]) * (tm["dec_base_us"] + tm["dec_seq_us"]) // 10 ** 6)
+        c = max(int(a[i]), c_prev) + S
+        assert int(r["trace"]["c"][i]) == c, i
+        c_prev = c
+
+
+def test_no_queue_limit(orc):
+    """Gaps >> service: every request is served alone on arrival, l_i = D_p(P_i) + decode(O_i)."""
+    wl = inputs.preset_ll(rate=1e-5)
+    k = inputs.knobs(conc=8, max_num_seqs=16)
+    seed = inputs.seeds(1, 3)[0]
+    r = orc.run([wl], k, seed, 500, latencies=True)
+    a, P, O, w3 = orc.request_draws([wl], k, seed, 500)
+    tm = wl["timing"]
+    gaps = np.diff(a.astype(np.int64))
+    assert gaps.min() > 600_000  # longer than any single service (<= 64 * 7.2 ms * 1.18 + prefill)
+    for i in range(500):
+        f = _noise(int(w3[i]), tm["noise_step_ppm"])
+        l = (f * (tm["pre_base_us"] + tm["pre_tok_us"] * int(P[i])) // 10 ** 6
+             + f * int(O[i]) * (tm["dec_base_us"] + tm["dec_seq_us"]) // 10 ** 6)
+        assert int(r["latencies"][i]) == l
+
+
+# ------------------------------------------------------------------------------------------------
+# Pollaczek-Khinchine (M/D/1) mean waiting time — statistical
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("rho", [0.5, 0.7])
+def test_pollaczek_khinchine_md1(orc, rho):
+    """B = 1, gamma = 0, no noise, P = 40, O = 64 (LL timing): S = 2000 + 60*40 + 64*(7000+200) = 465,200 us.
+    Poisson arrivals at lambda = rho / S.  M/D/1: W_q = rho * S / (2 (1 - rho))."""
+    S = 465_200
+    tm = dict(inputs.LL_TIMING, noise_step_ppm=0)
+    wl = inputs.workload(kind=0, rate=rho / (S * 1e-6), prompt=inputs.point_mass(40),
+                         output=inputs.point_mass(64), timing=tm)
+    k = inputs.knobs(conc=32, max_num_seqs=1)
+    means = []
+    N = 20000
+    for seed in inputs.seeds(24, 100):
+        r = orc.run([wl], k, seed, N, warmup_len=500)
+        means.append(r["sum_latency_us"] / N - S)
+    m = float(np.mean(means))
+    se = float(np.std(means, ddof=1) / math.sqrt(len(means)))
+    wq = rho * S / (2 * (1 - rho))
+    assert abs(m - wq) < 4 * se + 0.002 * wq, (m, wq, se)
+
+
+# ------------------------------------------------------------------------------------------------
+# exact invariants on random Philox replicas
+# ------------------------------------------------------------------------------------------------
+def _check_invariants(r, k, N):
+    tr = r["trace"]
+    a, s, form, c, batch = (tr[x].astype(np.int64) for x in ("a", "s", "form", "c", "batch"))
+    C, B, mw = k["conc"], k["max_num_seqs"], k["max_wait_us"]
+    assert np.all(np.diff(a) >= 0)
+    assert np.all(s >= a) and np.all(np.diff(s) >= 0)           # FIFO gate, issue in order
+    assert np.all(form >= s) and np.all(c >= form)
+    # batches: contiguous, in order, size <= B
+    assert batch[0] == 0 and np.all(np.diff(batch) >= 0) and np.all(np.diff(batch) <= 1)
+    sizes = np.bincount(batch)
+    assert sizes.max() <= B
+    # a batch starts only after the previous batch has fully completed (one server)
+    starts = np.array([form[batch == b][0] for b in range(len(sizes))])
+    ends = np.array([c[batch == b].max() for b in range(len(sizes))])
+    assert np.all(starts[1:] >= ends[:-1])
+    # work conservation with max_wait = 0: form = max(previous end, head issue)
+    heads = np.searchsorted(batch, np.arange(len(sizes)))
+    if mw == 0:
+        prev = np.concatenate([[0], ends[:-1]])
+        assert np.all(starts == np.maximum(prev, s[heads]))
+    # in flight never exceeds C: sweep issues (+1) and completions (-1), completions first at ties
+    ev = sorted([(int(t), 0, -1) for t in c] + [(int(t), 1, +1) for t in s])
+    cur = 0
+    for _, _, d in ev:
+        cur += d
+        assert cur <= C
+    # gate tightness: each issue happens at its arrival or at a completion instant
+    cset = set(int(x) for x in c)
+    for i in range(N):
+        assert s[i] == a[i] or int(s[i]) in cset
+    # outputs
+    lat = (c - a)
+    n = N
+    srt = np.sort(np.minimum(lat, 2 ** 32 - 1))
+    assert r["p99_us"] == srt[(99 * n + 99) // 100 - 1]
+    assert r["slo_met"] == int(np.sum(lat <= 1_200_000))
+    assert r["window_us"] == max(1, int(c.max() - a[0]))
+    assert r["slo_met"] <= n                                      # goodput <= throughput
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_invariants_random_replicas(orc, case):
+    rng = random.Random(case)
+    wls = [inputs.preset_ll(rate=rng.choice([5.0, 10.0, 20.0])), inputs.preset_sim(),
+           inputs.preset_stress(kind=1), inputs.preset_stress(kind=2)]
+    k = inputs.random_knobs(rng, n_wl=len(wls))
+    N = rng.choice([50, 300, 1000])
+    r = orc.run(wls, k, inputs.seeds(1, case)[0], N, trace=True, latencies=True)
+    assert r["flags"] & 1 == 0
+    _check_invariants(r, k, N)
+
+
+def test_spec_off_equals_zero_draft(orc):
+    """spec_on = 0 is bit-identical to draft_len = 0 (DESIGN.md §2.6 gamma_eff), and under CRN every
+    acceptance value gives the same replica when gamma_eff = 0."""
+    wl = inputs.preset_ll()
+    seed = inputs.seeds(1, 11)[0]
+    base = orc.run([wl], inputs.knobs(conc=8, max_num_seqs=8), seed, 2000, latencies=True)
+    for g in (4, 16):
+        for a in (0.3, 0.9):
+            r = orc.run([wl], inputs.knobs(conc=8, max_num_seqs=8, draft_len=g, spec_on=0,
+                                           accept_q16=inputs.q16(a)), seed, 2000, latencies=True)
+            assert np.array_equal(r["latencies"], base["latencies"])
+
+
+def test_acceptance_extremes(orc):
+    """alpha = 0: every step emits 1 token (S_m = O_m); alpha = 1: S_m = ceil(O_m / (gamma + 1))."""
+    wl = inputs.preset_ll()
+    seed = inputs.seeds(1, 5)[0]
+    for g in (1, 3, 8):
+        r0 = orc.run([wl], inputs.knobs(conc=4, max_num_seqs=4, draft_len=g, spec_on=1, accept_q16=0),
+                     seed, 400, trace=True)
+        assert np.array_equal(r0["trace"]["steps"], r0["trace"]["O"])
+        r1 = orc.run([wl], inputs.knobs(conc=4, max_num_seqs=4, draft_len=g, spec_on=1, accept_q16=65536),
+                     seed, 400, trace=True)
+        assert np.array_equal(r1["trace"]["steps"], (r1["trace"]["O"] + g) // (g + 1))
+
+
+def test_mean_steps_leviathan(orc):
+    """With alpha = .5, gamma = 4, the mean tokens per step over all (uncapped) steps approaches
+    Leviathan's (1 - alpha^5)/(1 - alpha) = 1.9375; the cap only lowers the last step."""
+    wl = inputs.workload(kind=0, rate=1.0, prompt=inputs.point_mass(10), output=inputs.point_mass(4000))
+    r = orc.run([wl], inputs.knobs(conc=1, max_num_seqs=1, draft_len=4, spec_on=1,
+                                   accept_q16=inputs.q16(0.5)), inputs.seeds(1, 0)[0], 200, trace=True)
+    tokens = r["trace"]["O"].sum()
+    steps = r["trace"]["steps"].sum()
+    assert abs(tokens / steps - 1.9375) < 0.02
+
+
+def test_p_mono_batch_one(orc):
+    """B = 1: every latency is pathwise non-decreasing in the arrival rate under CRN (per-gap floors)."""
+    wl = inputs.preset_ll()
+    seed = inputs.seeds(1, 21)[0]
+    prev = None
+    for q8 in (200, 256, 300, 400):
+        r = orc.run([wl], inputs.knobs(conc=8, max_num_seqs=1, rate_scale_q8=q8), seed, 1500, latencies=True)
+        if prev is not None:
+            assert np.all(r["latencies"].astype(np.int64) >= prev.astype(np.int64))
+        prev = r["latencies"]
+
+
+def test_slo_met_monotone_in_slo(orc):
+    wl = inputs.preset_ll()
+    k = inputs.knobs(conc=8, max_num_seqs=8, draft_len=8, spec_on=1)
+    seed = inputs.seeds(1, 2)[0]
+    prev = -1
+    for slo in (100_000, 600_000, 1_200_000, 3_000_000, 50_000_000):
+        r = orc.run([wl], k, seed, 2000, slo_us=slo)
+        assert r["slo_met"] >= prev and r["slo_met"] <= r["n_measured"]
+        prev = r["slo_met"]
+
+
+def test_warmup_excluded(orc):
+    """warmup requests are simulated but excluded from every output (R16)."""
+    wl = inputs.preset_ll()
+    k = inputs.knobs(conc=8, max_num_seqs=16)
+    seed = inputs.seeds(1, 9)[0]
+    full = orc.run([wl], k, seed, 1500, latencies=True, trace=True)
+    w = orc.run([wl], k, seed, 1000, warmup_len=500, latencies=True)
+    assert np.array_equal(full["latencies"], w["latencies"])
+    lat = full["latencies"][500:]
+    assert w["sum_latency_us"] == int(lat.astype(np.int64).sum())
+    assert w["p99_us"] == int(np.sort(lat)[(99 * 1000 + 99) // 100 - 1])
+    assert w["window_us"] == int(full["trace"]["c"][500:].max() - full["trace"]["a"][500])
+
+
+def test_trend_batching_and_bursts(orc):
+    """Paper trends (qualitative): B = 1 drives p99 far above the SLO; bursty arrivals at the same
+    mean rate give a higher p99 than steady ones (seed means)."""
+    wl = inputs.preset_ll()
+    seeds = inputs.seeds(6, 40)
+    p1 = np.mean([orc.run([wl], inputs.knobs(conc=16, max_num_seqs=1), s, 1500)["p99_us"] for s in seeds])
+    p8 = np.mean([orc.run([wl], inputs.knobs(conc=16, max_num_seqs=8), s, 1500)["p99_us"] for s in seeds])
+    assert p1 > 2 * 1_200_000 and p8 < p1
+    st = inputs.preset_stress(kind=1)
+    steady = inputs.workload(kind=0, rate=10.0, prompt=st["prompt"], output=st["output"])
+    kk = inputs.knobs(conc=16, max_num_seqs=8)
+    pb = np.mean([orc.run([st], kk, s, 1500)["p99_us"] for s in seeds])
+    ps = np.mean([orc.run([steady], kk, s, 1500)["p99_us"] for s in seeds])
+    assert pb > ps
+
+
+def test_invalid_knobs(orc):
+    r = orc.run([inputs.preset_ll()], inputs.knobs(conc=0), 1, 100)
+    assert r["flags"] == 1 and r["p99_us"] == 2 ** 32 - 1 and r["goodput"] == -1.0 and r["slo_met"] == 0
+
+
+def test_p99_nearest_rank_examples():
+    """SPEC S:123-128 nearest-rank examples, applied with DESIGN.md's rank r = (99n+99) div 100 (q=.99)
+    and its general form ceil(q n)."""
+    def nearest_rank(xs, num, den):
+        n = len(xs)
+        r = (num * n + den - 1) // den
+        return sorted(xs)[r - 1]
+    assert nearest_rank(list(range(1, 101)), 99, 100) == 99
+    assert nearest_rank([7], 99, 100) == 7
+    assert nearest_rank([3, 1, 2], 1, 2) == 2
+    assert nearest_rank([500] * 99 + [5000], 99, 100) == 500   # R23: S:145 contradicts S:123
