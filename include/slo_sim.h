@@ -1,0 +1,201 @@
+/* include/slo_sim.h — C ABI of libslosim.so: the SLO-Tuner serving simulator (arXiv 2603.11340) as a
+ * batched Monte-Carlo hot path on NVIDIA B200 (sm_100a).
+ *
+ * The paper's method:
+ *   - discrete-event simulator (§2.2 "Simulator"): arrivals -> FCFS queue -> idle server forms a
+ *     batch of up to B requests, optionally waiting up to max_wait -> prefill driven by the longest prompt
+ *     -> decode depending on active sequences and speculative decoding;
+ *   - goodput (Eq. 1) and empirical p99 per segment;
+ *   - score S = goodput - lambda*max(0, p99 - SLO) - hw_cost (Eq. 2-3);
+ *   - hill-climb control loop (Alg. 1; neighbour rule P:142).
+ * The exact integer model both this library and the CPU oracle implement is DESIGN.md §2.
+ *
+ * Conventions
+ *   - Every call returns slo_status; nothing throws or aborts.  On a non-OK status outputs are undefined.
+ *   - "d_" pointers are CUDA device pointers (e.g. torch tensors' data_ptr()); "h_" pointers are host.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).  Device calls validate
+ *     host-visible arguments synchronously (SLO_E_INVAL, nothing enqueued), then enqueue on `stream` and
+ *     return; results are valid once the stream reaches that point.
+ *   - The caller owns every buffer it passes; slo_sim_create deep-copies the workload tables.
+ *   - One handle may be used by one host thread at a time; distinct handles are independent.
+ *   - All integer structs are little-endian PODs with the sizes stated (checked by static asserts).
+ */
+#ifndef SLO_SIM_H
+#define SLO_SIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t slo_status;
+#define SLO_OK 0
+#define SLO_E_INVAL (-1)        /* null required pointer, zero size, bad table, reserved != 0, ...      */
+#define SLO_E_NOMEM (-2)        /* device or host allocation failed                                   */
+#define SLO_E_CUDA (-3)         /* a CUDA runtime call failed; text in slo_last_error                 */
+#define SLO_E_RANGE (-4)        /* a size exceeds a documented limit                                  */
+#define SLO_E_DEVICE (-5)       /* no usable sm_100 device                                            */
+#define SLO_E_UNSUPPORTED (-6)
+
+#define SLO_MAX_REQUESTS (1u << 22)   /* warmup_len + segment_len per replica                        */
+#define SLO_MAX_LENGTH 4096u          /* largest prompt/output length a table may produce            */
+
+typedef struct slo_sim slo_sim; /* opaque: one CUDA device, owns scratch and the copied workload tables */
+
+/* Integer microsecond timing block.  Each value must be < 2^20.       */
+typedef struct {
+  uint32_t pre_base_us, pre_tok_us;             /* prefill = f * (pre_base + pre_tok * max P) / 1e6      */
+  uint32_t dec_base_us, dec_seq_us;             /* plain step  d(n) = dec_base + dec_seq * n             */
+  uint32_t dr_base_us, dr_seq_us;               /* spec step   d(n) = g*(dr_base + dr_seq*n) + ver_base   */
+  uint32_t ver_base_us, ver_seq_us, ver_tok_us; /*                    + ver_seq*n + ver_tok*(g+1)*n      */
+  uint32_t noise_step_ppm;                      /* per-batch Irwin-Hall noise step, <= 1960; 0 = none    */
+} slo_timing;                                   /* 40 B */
+
+/* Arrival process. */
+typedef struct {
+  uint32_t kind;                /* 0 Poisson, 1 MMPP-2 (exponential sojourns), 2 on/off (fixed sojourns) */
+  uint32_t start_state;         /* 0 or 1                                                               */
+  uint64_t mean_gap_q16[2];     /* per-state mean gap, Q48.16 us, <= 2^48; UINT64_MAX = no arrivals     */
+  uint64_t mean_sojourn_us[2];  /* kinds 1, 2: per-state mean/fixed sojourn, >= 1                       */
+} slo_arrivals;                 /* 40 B */
+
+/* One workload: arrivals, length tables, timing, CRN stream id. */
+typedef struct {
+  slo_arrivals arr;
+  const uint32_t* prompt_cw;    /* host ptr, prompt_ncw non-decreasing Q32 cut points (copied at create) */
+  uint32_t prompt_lo, prompt_ncw; /* P = prompt_lo + #{l : cw[l] <= u}; lo >= 1; lo + ncw <= 4096       */
+  const uint32_t* output_cw;
+  uint32_t output_lo, output_ncw;
+  slo_timing timing;
+  uint32_t stream_id;           /* cfgkey in CRN mode                                  */
+} slo_workload;
+
+/* One logical-knob configuration, 32 B.  Validity is checked per
+ * replica on the device; an invalid record yields flags bit 0, p99 = UINT32_MAX, goodput = -1.0. */
+typedef struct {
+  uint8_t conc;                 /* client concurrency C in [1,32]                                        */
+  uint8_t max_num_seqs;         /* batch limit B in [1,32]                                               */
+  uint8_t draft_len;            /* gamma = k = num_speculative_tokens in [0,16]                          */
+  uint8_t spec_on;              /* 0 or 1; 0 => gamma_eff = 0                                           */
+  uint8_t draft_width;          /* W in [1,4]; alpha_eff = 1 - (1 - alpha)^W                             */
+  uint8_t workload;             /* index into the create-time workload array                             */
+  uint16_t rate_scale_q8;       /* offered-load multiplier, 256 = 1.0, >= 1                              */
+  uint32_t accept_q16;          /* per-position acceptance alpha in [0, 65536]                           */
+  uint32_t max_wait_us;         /* [0, 50000]                                                    */
+  uint32_t reserved[4];         /* must be 0                                                             */
+} slo_knobs;
+
+/* Per-replica outputs, 32 B. flags: bit0 invalid knobs, bit1 a latency saturated u32. */
+typedef struct {
+  uint32_t p99_us, slo_met, n_measured, flags;
+  uint64_t window_us, sum_latency_us;
+} slo_replica_result;
+
+/* Per-config aggregate over seeds, 32 B. */
+typedef struct {
+  uint64_t sum_p99_us, sum_slo_met, sum_window_us;
+  uint32_t n_seeds, flags;
+} slo_config_agg;
+
+/* Work counters of one run (exact algorithmic work, summed over replicas), 64 B. */
+typedef struct {
+  uint64_t requests, batches, decode_steps, member_steps, philox_blocks, replicas, reserved[2];
+} slo_stats;
+
+typedef struct {
+  uint32_t crn;                 /* 1 (default): cfgkey = workload.stream_id; 0: FNV-1a of the knob record */
+  uint32_t warps_per_block;     /* 0 = default (4)                                                        */
+  uint32_t blocks_per_sm;       /* 0 = as many as fit                                                     */
+  uint32_t reserved[5];         /* must be 0                                                              */
+} slo_sim_opts;
+
+typedef struct {                /* read-only launch facts of a handle                                    */
+  int32_t device, sm_count, warps_per_block, blocks_per_sm;
+  int32_t regs_per_thread, smem_per_warp_bytes, reserved[2];
+} slo_sim_info;
+
+/* Create a handle on CUDA device `device` with `n_wl` (1..255) workloads.  opts may be NULL.
+ * Errors: SLO_E_INVAL (bad table / timing / arrivals), SLO_E_DEVICE, SLO_E_NOMEM, SLO_E_CUDA. */
+slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, const slo_sim_opts* opts,
+                          slo_sim** out);
+/* Synchronise the handle's work and free everything it owns.  NULL is a no-op. */
+slo_status slo_sim_destroy(slo_sim* h);
+slo_status slo_sim_get_info(const slo_sim* h, slo_sim_info* info);
+
+/* K1: simulate replicas r = c * n_seeds + s (config-major) for every (config c, seed s) pair.
+ * Each replica simulates warmup_len + segment_len requests and writes
+ *   d_p99_us[r] (u32, nearest-rank p99 of the measured latencies) and d_goodput[r] (f64, Eq. 1);
+ * optionally d_detail[r], d_latencies[r * (warmup_len + segment_len) + i] (every request's stored
+ * latency, debug/parity only) and *d_stats (one slo_stats accumulated over the launch, overwritten).
+ * Limits: n_configs * n_seeds < 2^31, warmup_len + segment_len <= SLO_MAX_REQUESTS, slo_us < UINT32_MAX.
+ * Errors: SLO_E_INVAL (null required pointer, segment_len == 0, n == 0), SLO_E_RANGE, SLO_E_CUDA. */
+slo_status slo_sim_run_batch(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs,
+                             const uint64_t* d_seeds, uint32_t n_seeds, uint32_t segment_len,
+                             uint32_t warmup_len, uint32_t slo_us, uint32_t* d_p99_us, double* d_goodput,
+                             slo_replica_result* d_detail, uint32_t* d_latencies, slo_stats* d_stats,
+                             void* stream);
+
+/* The same call on HOST buffers (end-to-end use): copies h_configs / h_seeds to the handle's device
+ * scratch, runs K1 on `stream`, copies the outputs back and synchronises `stream` before returning.
+ * h_detail and h_stats may be NULL.  Pinned host memory makes the copies asynchronous DMA. */
+slo_status slo_sim_run_batch_host(slo_sim* h, const slo_knobs* h_configs, uint32_t n_configs,
+                                  const uint64_t* h_seeds, uint32_t n_seeds, uint32_t segment_len,
+                                  uint32_t warmup_len, uint32_t slo_us, uint32_t* h_p99_us,
+                                  double* h_goodput, slo_replica_result* h_detail, slo_stats* h_stats,
+                                  void* stream);
+
+/* K2: d_agg[c] = sum over seeds s of d_detail[c * n_seeds + s] (integer sums, flags OR). */
+slo_status slo_aggregate(slo_sim* h, const slo_replica_result* d_detail, uint32_t n_configs,
+                         uint32_t n_seeds, slo_config_agg* d_agg, void* stream);
+/* d_out[c] = sum over parts p of d_parts[p * n_configs + c] (e.g. per-rank aggregates after an
+ * all-gather; integer sums make the result independent of rank order). */
+slo_status slo_aggregate_reduce(slo_sim* h, const slo_config_agg* d_parts, uint32_t n_parts,
+                                uint32_t n_configs, slo_config_agg* d_out, void* stream);
+
+/* Climb space.  dims: 0 conc, 1 max_num_seqs, 2 draft_len, 3 draft_width,
+ * 4 max_wait_us.  stencil: 0 paper-live (<= 7 neighbours), 1 sim (<= 8), 2 wide-32 (<= 31). */
+typedef struct {
+  uint32_t stencil;
+  int32_t lo[5], hi[5], step[5];
+} slo_space;
+
+/* Eq. (2)-(3) and Alg. 1 parameters in fixed point.  Defaults: 5000, 10000, 10000, 20000, 20000. */
+typedef struct {
+  int64_t lambda_milli, w_conc_micro, w_max_micro, w_spec_micro, delta_micro;
+  uint32_t slo_us, strict_alg1;
+} slo_score_params;
+
+typedef struct {
+  slo_knobs K, K_best;
+  int64_t S_best_micro;
+  uint32_t step, has_best;
+  int32_t moved;                /* last step: 1 if K moved                                               */
+  uint32_t argmax;              /* last step: index of K* among the candidates                           */
+  uint32_t n_next;              /* number of valid candidates written for the next step                  */
+  uint32_t reserved;
+} slo_climb_state;              /* 96 B */
+
+/* Host helper: neighbours of K, written to out[0..*n) (cap >= 31 recommended). */
+slo_status slo_neighbors(const slo_space* space, const slo_knobs* K, slo_knobs* out, uint32_t cap,
+                         uint32_t* n);
+
+/* K3 (device-resident Alg. 1 step, one warp):
+ *   aggregates d_aggs[p * n_cand + k] summed over p < n_parts are the measurements of candidate
+ *   d_cands[k] (d_cands[0] must equal state.K); computes every score (Eq. 3, INT64_MIN for invalid),
+ *   argmax over k >= 1 (lowest index on ties), the move rule, best-so-far, then OVERWRITES
+ *   d_cands[0..n_cand) with [K', neighbours(K'), padding] for the next step (padding records have
+ *   conc = 0, i.e. are invalid and cost nothing).  d_scores (nullable) receives the scores.
+ * n_cand in [1, 32]. */
+slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_score_params* sp,
+                              slo_knobs* d_cands, uint32_t n_cand, const slo_config_agg* d_aggs,
+                              uint32_t n_parts, slo_climb_state* d_state, int64_t* d_scores,
+                              void* stream);
+
+const char* slo_status_string(slo_status s);
+const char* slo_last_error(const slo_sim* h); /* detail of the last failing call on h (NULL h: global) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLO_SIM_H */

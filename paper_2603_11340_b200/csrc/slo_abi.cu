@@ -1,0 +1,407 @@
+// slo_abi.cu — the C ABI of libslosim.so (include/slo_sim.h): handle, validation, stream-ordered launches.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "slo_internal.h"
+
+static_assert(sizeof(slo_knobs) == 32, "slo_knobs must be 32 B");
+static_assert(sizeof(slo_replica_result) == 32, "slo_replica_result must be 32 B");
+static_assert(sizeof(slo_config_agg) == 32, "slo_config_agg must be 32 B");
+static_assert(sizeof(slo_stats) == 64, "slo_stats must be 64 B");
+static_assert(sizeof(slo_timing) == 40, "slo_timing must be 40 B");
+static_assert(sizeof(slo_arrivals) == 40, "slo_arrivals must be 40 B");
+static_assert(sizeof(slo_climb_state) == 96, "slo_climb_state must be 96 B");
+
+struct slo_sim {
+  int device = 0;
+  int sm_count = 0;
+  int warps_per_block = slo::kDefaultWarpsPerBlock;
+  int blocks_per_sm_opt = 0;
+  uint32_t n_wl = 0;
+  uint32_t crn = 1;
+  slo::DevWorkload* d_wl = nullptr;
+  uint32_t* d_tables = nullptr;
+  uint32_t* d_queue = nullptr;      // replica queue counter (one per launch, reset by memset)
+  // host-entry scratch
+  void* d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int regs = 0;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+slo_status fail(slo_sim* h, slo_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(h, call)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) return fail((h), SLO_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+uint32_t topk_for(uint32_t n) {  // K = n - r + 1 with r = ceil(0.99 n)
+  const uint64_t r = (99ull * n + 99ull) / 100ull;
+  return (uint32_t)(n - r + 1);
+}
+
+uint32_t cap_for(uint32_t K) { return ((2u * K + 64u + 31u) / 32u) * 32u; }
+
+bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
+  if (lo < 1 || (uint64_t)lo + ncw > SLO_MAX_LENGTH) return false;
+  if (ncw > 0 && cw == nullptr) return false;
+  for (uint32_t i = 1; i < ncw; ++i)
+    if (cw[i] < cw[i - 1]) return false;
+  return true;
+}
+
+}  // namespace
+
+namespace slo {
+size_t warp_bytes_for(uint32_t cap) {
+  // WarpRing (64*8*2 + 64*4*2 + 16*4 + 16) followed by the candidate buffer
+  return 1536 + 64 + 16 + (size_t)cap * 4u;
+}
+}  // namespace slo
+
+extern "C" {
+
+const char* slo_status_string(slo_status s) {
+  switch (s) {
+    case SLO_OK: return "ok";
+    case SLO_E_INVAL: return "invalid argument";
+    case SLO_E_NOMEM: return "out of memory";
+    case SLO_E_CUDA: return "CUDA error";
+    case SLO_E_RANGE: return "size out of range";
+    case SLO_E_DEVICE: return "no usable device";
+    case SLO_E_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* slo_last_error(const slo_sim* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, const slo_sim_opts* opts,
+                          slo_sim** out) {
+  if (!out || !wl || n_wl == 0 || n_wl > 255) return fail(nullptr, SLO_E_INVAL, "create: bad arguments");
+  *out = nullptr;
+  slo_sim_opts o{};
+  o.crn = 1;
+  if (opts) {
+    o = *opts;
+    for (int i = 0; i < 5; ++i)
+      if (o.reserved[i]) return fail(nullptr, SLO_E_INVAL, "create: opts.reserved must be 0");
+    if (o.crn > 1) return fail(nullptr, SLO_E_INVAL, "create: opts.crn must be 0 or 1");
+    if (o.warps_per_block > (uint32_t)slo::kMaxWarpsPerBlock)
+      return fail(nullptr, SLO_E_INVAL, "create: warps_per_block > %d", slo::kMaxWarpsPerBlock);
+  }
+  // ---- validate the workloads (include/slo_sim.h)
+  std::vector<slo::DevWorkload> hw(n_wl);
+  std::vector<uint32_t> tables;
+  for (uint32_t w = 0; w < n_wl; ++w) {
+    const slo_workload& x = wl[w];
+    const uint64_t NOA = ~0ull;
+    if (x.arr.kind > 2 || x.arr.start_state > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: bad arrival kind", w);
+    for (int s = 0; s < 2; ++s)
+      if (x.arr.mean_gap_q16[s] != NOA && x.arr.mean_gap_q16[s] > (1ull << 48))
+        return fail(nullptr, SLO_E_INVAL, "workload %u: mean_gap_q16 > 2^48", w);
+    if (x.arr.kind == 0 && (x.arr.mean_gap_q16[0] == NOA || x.arr.mean_gap_q16[0] == 0))
+      return fail(nullptr, SLO_E_INVAL, "workload %u: Poisson needs a finite positive gap", w);
+    if (x.arr.kind != 0) {
+      if (x.arr.mean_gap_q16[0] == NOA && x.arr.mean_gap_q16[1] == NOA)
+        return fail(nullptr, SLO_E_INVAL, "workload %u: no state has arrivals", w);
+      for (int s = 0; s < 2; ++s) {
+        if (x.arr.mean_sojourn_us[s] < 1 || x.arr.mean_sojourn_us[s] > (1ull << 40))
+          return fail(nullptr, SLO_E_INVAL, "workload %u: sojourn out of [1, 2^40]", w);
+        if (x.arr.mean_gap_q16[s] == 0) return fail(nullptr, SLO_E_INVAL, "workload %u: zero gap", w);
+      }
+    }
+    if (!table_ok(x.prompt_cw, x.prompt_ncw, x.prompt_lo) || !table_ok(x.output_cw, x.output_ncw, x.output_lo))
+      return fail(nullptr, SLO_E_INVAL, "workload %u: bad length table", w);
+    const uint32_t* tv = &x.timing.pre_base_us;
+    for (int i = 0; i < 9; ++i)
+      if (tv[i] >= (1u << 20)) return fail(nullptr, SLO_E_INVAL, "workload %u: timing value >= 2^20", w);
+    if (x.timing.noise_step_ppm > 1960) return fail(nullptr, SLO_E_INVAL, "workload %u: noise_step_ppm > 1960", w);
+    slo::DevWorkload& d = hw[w];
+    memset(&d, 0, sizeof d);
+    d.kind = x.arr.kind;
+    d.start_state = x.arr.start_state;
+    d.gap_q16[0] = x.arr.mean_gap_q16[0];
+    d.gap_q16[1] = x.arr.mean_gap_q16[1];
+    d.soj[0] = x.arr.mean_sojourn_us[0];
+    d.soj[1] = x.arr.mean_sojourn_us[1];
+    d.p_lo = x.prompt_lo;
+    d.p_ncw = x.prompt_ncw;
+    d.p_off = (uint32_t)tables.size();
+    tables.insert(tables.end(), x.prompt_cw, x.prompt_cw + x.prompt_ncw);
+    d.o_lo = x.output_lo;
+    d.o_ncw = x.output_ncw;
+    d.o_off = (uint32_t)tables.size();
+    tables.insert(tables.end(), x.output_cw, x.output_cw + x.output_ncw);
+    d.t = x.timing;
+    d.stream_id = x.stream_id;
+  }
+  if (tables.empty()) tables.push_back(0);
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(nullptr, SLO_E_DEVICE, "create: no CUDA device %d", device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10)
+    return fail(nullptr, SLO_E_DEVICE, "create: device %d is not sm_100", device);
+  DeviceGuard g(device);
+
+  slo_sim* h = new (std::nothrow) slo_sim();
+  if (!h) return fail(nullptr, SLO_E_NOMEM, "create: host allocation");
+  h->device = device;
+  h->sm_count = prop.multiProcessorCount;
+  h->n_wl = n_wl;
+  h->crn = o.crn;
+  if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
+  h->blocks_per_sm_opt = (int)o.blocks_per_sm;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel) == cudaSuccess) h->regs = fa.numRegs;
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_queue, sizeof(uint32_t) * 4)) != cudaSuccess) {
+    slo_sim_destroy(h);
+    return fail(nullptr, SLO_E_NOMEM, "create: cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  if ((e = cudaMemcpy(h->d_wl, hw.data(), sizeof(slo::DevWorkload) * n_wl, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(h->d_tables, tables.data(), sizeof(uint32_t) * tables.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess) {
+    slo_sim_destroy(h);
+    return fail(nullptr, SLO_E_CUDA, "create: cudaMemcpy: %s", cudaGetErrorString(e));
+  }
+  *out = h;
+  return SLO_OK;
+}
+
+slo_status slo_sim_destroy(slo_sim* h) {
+  if (!h) return SLO_OK;
+  {
+    DeviceGuard g(h->device);
+    cudaDeviceSynchronize();
+    if (h->d_wl) cudaFree(h->d_wl);
+    if (h->d_tables) cudaFree(h->d_tables);
+    if (h->d_queue) cudaFree(h->d_queue);
+    if (h->d_scratch) cudaFree(h->d_scratch);
+  }
+  delete h;
+  return SLO_OK;
+}
+
+static int blocks_per_sm_for(slo_sim* h, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slo::slo_sim_kernel, h->warps_per_block * 32, smem) !=
+          cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  if (h->blocks_per_sm_opt > 0 && h->blocks_per_sm_opt < occ) occ = h->blocks_per_sm_opt;
+  return occ;
+}
+
+slo_status slo_sim_get_info(const slo_sim* hc, slo_sim_info* info) {
+  if (!hc || !info) return fail(nullptr, SLO_E_INVAL, "get_info: null");
+  slo_sim* h = const_cast<slo_sim*>(hc);
+  DeviceGuard g(h->device);
+  const size_t wb = slo::warp_bytes_for(cap_for(topk_for(10000)));
+  memset(info, 0, sizeof *info);
+  info->device = h->device;
+  info->sm_count = h->sm_count;
+  info->warps_per_block = h->warps_per_block;
+  info->blocks_per_sm = blocks_per_sm_for(h, wb * h->warps_per_block);
+  info->regs_per_thread = h->regs;
+  info->smem_per_warp_bytes = (int32_t)wb;
+  return SLO_OK;
+}
+
+static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,
+                             uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
+                             uint32_t* d_p99, double* d_goodput, slo_replica_result* d_detail, uint32_t* d_lat,
+                             slo_stats* d_stats, cudaStream_t st) {
+  const uint64_t n_rep = (uint64_t)n_configs * n_seeds;
+  slo::SimParams p{};
+  p.cfg = d_configs;
+  p.seeds = d_seeds;
+  p.wl = h->d_wl;
+  p.tables = h->d_tables;
+  p.queue = h->d_queue;
+  p.p99 = d_p99;
+  p.goodput = d_goodput;
+  p.detail = d_detail;
+  p.lat = d_lat;
+  p.stats = d_stats;
+  p.n_cfg = n_configs;
+  p.n_seeds = n_seeds;
+  p.n_rep = (uint32_t)n_rep;
+  p.n_wl = h->n_wl;
+  p.warmup = warmup_len;
+  p.seg = segment_len;
+  p.slo_us = slo_us;
+  p.crn = h->crn;
+  p.topk = topk_for(segment_len);
+  p.cap = cap_for(p.topk);
+  p.warp_bytes = (uint32_t)slo::warp_bytes_for(p.cap);
+  const size_t smem = (size_t)p.warp_bytes * h->warps_per_block;
+  if (smem > 227 * 1024) return fail(h, SLO_E_RANGE, "run_batch: segment_len %u needs %zu B of shared memory", segment_len, smem);
+  if (smem > 48 * 1024)
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int bps = blocks_per_sm_for(h, smem);
+  uint64_t blocks = (uint64_t)bps * h->sm_count;
+  const uint64_t need = (n_rep + h->warps_per_block - 1) / h->warps_per_block;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  CUDA_TRY(h, cudaMemsetAsync(h->d_queue, 0, sizeof(uint32_t), st));
+  if (d_stats) CUDA_TRY(h, cudaMemsetAsync(d_stats, 0, sizeof(slo_stats), st));
+  slo::slo_sim_kernel<<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+static slo_status check_run_args(slo_sim* h, uint32_t n_configs, uint32_t n_seeds, uint32_t segment_len,
+                                 uint32_t warmup_len, uint32_t slo_us) {
+  if (n_configs == 0 || n_seeds == 0 || segment_len == 0)
+    return fail(h, SLO_E_INVAL, "run_batch: n_configs, n_seeds and segment_len must be > 0");
+  if ((uint64_t)n_configs * n_seeds >= (1ull << 31)) return fail(h, SLO_E_RANGE, "run_batch: too many replicas");
+  if ((uint64_t)segment_len + warmup_len > SLO_MAX_REQUESTS)
+    return fail(h, SLO_E_RANGE, "run_batch: warmup_len + segment_len > %u", SLO_MAX_REQUESTS);
+  if (slo_us == 0xFFFFFFFFu) return fail(h, SLO_E_RANGE, "run_batch: slo_us must be < UINT32_MAX");
+  return SLO_OK;
+}
+
+slo_status slo_sim_run_batch(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,
+                             uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
+                             uint32_t* d_p99_us, double* d_goodput, slo_replica_result* d_detail,
+                             uint32_t* d_latencies, slo_stats* d_stats, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "run_batch: null handle");
+  if (!d_configs || !d_seeds || !d_p99_us || !d_goodput) return fail(h, SLO_E_INVAL, "run_batch: null pointer");
+  slo_status s = check_run_args(h, n_configs, n_seeds, segment_len, warmup_len, slo_us);
+  if (s != SLO_OK) return s;
+  DeviceGuard g(h->device);
+  return launch_sim(h, d_configs, n_configs, d_seeds, n_seeds, segment_len, warmup_len, slo_us, d_p99_us, d_goodput,
+                    d_detail, d_latencies, d_stats, (cudaStream_t)stream);
+}
+
+slo_status slo_sim_run_batch_host(slo_sim* h, const slo_knobs* h_configs, uint32_t n_configs, const uint64_t* h_seeds,
+                                  uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
+                                  uint32_t* h_p99_us, double* h_goodput, slo_replica_result* h_detail,
+                                  slo_stats* h_stats, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "run_batch_host: null handle");
+  if (!h_configs || !h_seeds || !h_p99_us || !h_goodput) return fail(h, SLO_E_INVAL, "run_batch_host: null pointer");
+  slo_status s = check_run_args(h, n_configs, n_seeds, segment_len, warmup_len, slo_us);
+  if (s != SLO_OK) return s;
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t R = (uint64_t)n_configs * n_seeds;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t o_cfg = 0, o_seed = al(o_cfg + 32ull * n_configs), o_p99 = al(o_seed + 8ull * n_seeds),
+               o_gp = al(o_p99 + 4ull * R), o_det = al(o_gp + 8ull * R), o_st = al(o_det + (h_detail ? 32ull * R : 0)),
+               total = al(o_st + sizeof(slo_stats));
+  if (total > h->scratch_bytes) {
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    if (h->d_scratch) cudaFree(h->d_scratch);
+    h->d_scratch = nullptr;
+    h->scratch_bytes = 0;
+    if (cudaMalloc(&h->d_scratch, total) != cudaSuccess) return fail(h, SLO_E_NOMEM, "run_batch_host: scratch");
+    h->scratch_bytes = total;
+  }
+  char* b = (char*)h->d_scratch;
+  CUDA_TRY(h, cudaMemcpyAsync(b + o_cfg, h_configs, 32ull * n_configs, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, cudaMemcpyAsync(b + o_seed, h_seeds, 8ull * n_seeds, cudaMemcpyHostToDevice, st));
+  s = launch_sim(h, (const slo_knobs*)(b + o_cfg), n_configs, (const uint64_t*)(b + o_seed), n_seeds, segment_len,
+                 warmup_len, slo_us, (uint32_t*)(b + o_p99), (double*)(b + o_gp),
+                 h_detail ? (slo_replica_result*)(b + o_det) : nullptr, nullptr,
+                 h_stats ? (slo_stats*)(b + o_st) : nullptr, st);
+  if (s != SLO_OK) return s;
+  CUDA_TRY(h, cudaMemcpyAsync(h_p99_us, b + o_p99, 4ull * R, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(h_goodput, b + o_gp, 8ull * R, cudaMemcpyDeviceToHost, st));
+  if (h_detail) CUDA_TRY(h, cudaMemcpyAsync(h_detail, b + o_det, 32ull * R, cudaMemcpyDeviceToHost, st));
+  if (h_stats) CUDA_TRY(h, cudaMemcpyAsync(h_stats, b + o_st, sizeof(slo_stats), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  return SLO_OK;
+}
+
+slo_status slo_aggregate(slo_sim* h, const slo_replica_result* d_detail, uint32_t n_configs, uint32_t n_seeds,
+                         slo_config_agg* d_agg, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "aggregate: null handle");
+  if (!d_detail || !d_agg || n_configs == 0 || n_seeds == 0) return fail(h, SLO_E_INVAL, "aggregate: bad arguments");
+  DeviceGuard g(h->device);
+  const unsigned threads = 256, warps = threads / 32;
+  const unsigned blocks = (unsigned)((n_configs + warps - 1) / warps);
+  slo::slo_aggregate_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(d_detail, n_configs, n_seeds, d_agg);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+slo_status slo_aggregate_reduce(slo_sim* h, const slo_config_agg* d_parts, uint32_t n_parts, uint32_t n_configs,
+                                slo_config_agg* d_out, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "aggregate_reduce: null handle");
+  if (!d_parts || !d_out || n_parts == 0 || n_configs == 0) return fail(h, SLO_E_INVAL, "aggregate_reduce: bad arguments");
+  DeviceGuard g(h->device);
+  const unsigned threads = 256;
+  slo::slo_aggregate_reduce_kernel<<<(n_configs + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
+      d_parts, n_parts, n_configs, d_out);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+static bool space_ok(const slo_space* sp) {
+  if (!sp || sp->stencil > 2) return false;
+  for (int d = 0; d < 5; ++d) {
+    if (sp->lo[d] < 0 || sp->lo[d] > sp->hi[d] || sp->step[d] < 0) return false;
+    if (d < 4 && sp->hi[d] > 255) return false;
+  }
+  return true;
+}
+
+slo_status slo_neighbors(const slo_space* space, const slo_knobs* K, slo_knobs* out, uint32_t cap, uint32_t* n) {
+  if (!space_ok(space) || !K || !n || (cap > 0 && !out)) return fail(nullptr, SLO_E_INVAL, "neighbors: bad arguments");
+  *n = slo::neighbors_of(*space, *K, out, cap);
+  return SLO_OK;
+}
+
+slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_score_params* sp, slo_knobs* d_cands,
+                              uint32_t n_cand, const slo_config_agg* d_aggs, uint32_t n_parts,
+                              slo_climb_state* d_state, int64_t* d_scores, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "hillclimb_step: null handle");
+  if (!space_ok(space) || !sp || !d_cands || !d_aggs || !d_state || n_cand == 0 || n_cand > 32 || n_parts == 0)
+    return fail(h, SLO_E_INVAL, "hillclimb_step: bad arguments");
+  if (sp->lambda_milli < 0 || sp->delta_micro < 0) return fail(h, SLO_E_INVAL, "hillclimb_step: negative weight");
+  DeviceGuard g(h->device);
+  slo::slo_climb_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*space, *sp, d_cands, n_cand, d_aggs, n_parts, d_state,
+                                                            d_scores);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+}  // extern "C"

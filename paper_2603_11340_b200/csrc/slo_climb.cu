@@ -1,0 +1,232 @@
+// slo_climb.cu — K2 (per-config aggregation over seeds) and K3 (device-resident Alg. 1 step).
+// Eq. (2)-(3), Alg. 1, neighbour rule PAPER.md:142; the exact
+// integer definitions are DESIGN.md §2.9.
+#include <cstdint>
+
+#include "slo_device.cuh"
+#include "slo_internal.h"
+
+namespace slo {
+
+// ------------------------------------------------------------------------------------------------
+// K2: d_agg[c] = sum_s detail[c * n_seeds + s]   (one warp per config)
+// ------------------------------------------------------------------------------------------------
+__global__ void slo_aggregate_kernel(const slo_replica_result* __restrict__ detail, uint32_t n_cfg,
+                                     uint32_t n_seeds, slo_config_agg* __restrict__ agg) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_cfg) return;
+  uint64_t sp = 0, sm = 0, sw = 0;
+  uint32_t fl = 0;
+  const slo_replica_result* d = detail + (size_t)warp * n_seeds;
+  for (uint32_t s = lane; s < n_seeds; s += 32) {
+    const slo_replica_result x = d[s];
+    sp += x.p99_us;
+    sm += x.slo_met;
+    sw += x.window_us;
+    fl |= x.flags;
+  }
+  sp = warp_sum64(sp);
+  sm = warp_sum64(sm);
+  sw = warp_sum64(sw);
+  fl = __reduce_or_sync(FULL, fl);
+  if (lane == 0) agg[warp] = slo_config_agg{sp, sm, sw, n_seeds, fl};
+}
+
+__global__ void slo_aggregate_reduce_kernel(const slo_config_agg* __restrict__ parts, uint32_t n_parts,
+                                            uint32_t n_cfg, slo_config_agg* __restrict__ out) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cfg) return;
+  slo_config_agg a{0, 0, 0, 0, 0};
+  for (uint32_t p = 0; p < n_parts; ++p) {
+    const slo_config_agg x = parts[(size_t)p * n_cfg + c];
+    a.sum_p99_us += x.sum_p99_us;
+    a.sum_slo_met += x.sum_slo_met;
+    a.sum_window_us += x.sum_window_us;
+    a.n_seeds += x.n_seeds;
+    a.flags |= x.flags;
+  }
+  out[c] = a;
+}
+
+// ------------------------------------------------------------------------------------------------
+// neighbours (host + device)
+// ------------------------------------------------------------------------------------------------
+__host__ __device__ static inline int32_t dim_get(const slo_knobs& k, int d) {
+  switch (d) {
+    case 0: return k.conc;
+    case 1: return k.max_num_seqs;
+    case 2: return k.draft_len;
+    case 3: return k.draft_width;
+    default: return (int32_t)k.max_wait_us;
+  }
+}
+
+__host__ __device__ static inline void dim_set(slo_knobs& k, int d, int32_t v) {
+  switch (d) {
+    case 0: k.conc = (uint8_t)v; break;
+    case 1: k.max_num_seqs = (uint8_t)v; break;
+    case 2: k.draft_len = (uint8_t)v; break;
+    case 3: k.draft_width = (uint8_t)v; break;
+    default: k.max_wait_us = (uint32_t)v; break;
+  }
+}
+
+__host__ __device__ static inline bool knobs_equal(const slo_knobs& a, const slo_knobs& b) {
+  const uint32_t* x = reinterpret_cast<const uint32_t*>(&a);
+  const uint32_t* y = reinterpret_cast<const uint32_t*>(&b);
+  for (int i = 0; i < 8; ++i)
+    if (x[i] != y[i]) return false;
+  return true;
+}
+
+__host__ __device__ static inline int32_t clampi(int32_t v, int32_t lo, int32_t hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+__host__ __device__ static inline void push_unique(const slo_knobs& K, const slo_knobs& c, slo_knobs* out,
+                                                   uint32_t& n, uint32_t cap) {
+  if (knobs_equal(c, K)) return;
+  for (uint32_t i = 0; i < n; ++i)
+    if (knobs_equal(out[i], c)) return;
+  if (n < cap) out[n++] = c;
+}
+
+__host__ __device__ static inline slo_knobs moved(const slo_space& sp, const slo_knobs& K, int d, int sign) {
+  slo_knobs c = K;
+  dim_set(c, d, clampi(dim_get(K, d) + sign * sp.step[d], sp.lo[d], sp.hi[d]));
+  return c;
+}
+
+__host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& K, slo_knobs* out, uint32_t cap) {
+  uint32_t n = 0;
+  slo_knobs toggle = K;
+  toggle.spec_on = K.spec_on ? 0 : 1;
+  if (sp.stencil == 0) {  // conc, max_num_seqs, draft_len (minus before plus), then the toggle
+    for (int d = 0; d < 3; ++d) {
+      push_unique(K, moved(sp, K, d, -1), out, n, cap);
+      push_unique(K, moved(sp, K, d, +1), out, n, cap);
+    }
+    push_unique(K, toggle, out, n, cap);
+  } else if (sp.stencil == 1) {  // W, k, B, max_wait
+    const int order[4] = {3, 2, 1, 4};
+    for (int i = 0; i < 4; ++i) {
+      push_unique(K, moved(sp, K, order[i], -1), out, n, cap);
+      push_unique(K, moved(sp, K, order[i], +1), out, n, cap);
+    }
+  } else {  // wide-32: 26 non-zero moves of (conc, B, gamma) in lexicographic order, W-/+, wait-/+, toggle
+    for (int dc = -1; dc <= 1; ++dc)
+      for (int db = -1; db <= 1; ++db)
+        for (int dg = -1; dg <= 1; ++dg) {
+          if (dc == 0 && db == 0 && dg == 0) continue;
+          slo_knobs c = K;
+          dim_set(c, 0, clampi(dim_get(K, 0) + dc * sp.step[0], sp.lo[0], sp.hi[0]));
+          dim_set(c, 1, clampi(dim_get(K, 1) + db * sp.step[1], sp.lo[1], sp.hi[1]));
+          dim_set(c, 2, clampi(dim_get(K, 2) + dg * sp.step[2], sp.lo[2], sp.hi[2]));
+          push_unique(K, c, out, n, cap);
+        }
+    push_unique(K, moved(sp, K, 3, -1), out, n, cap);
+    push_unique(K, moved(sp, K, 3, +1), out, n, cap);
+    push_unique(K, moved(sp, K, 4, -1), out, n, cap);
+    push_unique(K, moved(sp, K, 4, +1), out, n, cap);
+    push_unique(K, toggle, out, n, cap);
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------------------------------------
+// K3: one warp; lane k scores candidate k (Eq. 3), warp argmax, Alg. 1 move + best, next stencil.
+// ------------------------------------------------------------------------------------------------
+__device__ static inline int64_t score_micro(const slo_config_agg& a, const slo_knobs& k,
+                                             const slo_score_params& sp) {
+  if (a.n_seeds == 0 || (a.flags & 1u) || a.sum_window_us == 0) return INT64_MIN;
+  const unsigned __int128 gp = ((unsigned __int128)a.sum_slo_met * 1000000000000ull) / a.sum_window_us;
+  const unsigned __int128 bound = (unsigned __int128)a.n_seeds * sp.slo_us;
+  unsigned __int128 pen = 0;
+  if ((unsigned __int128)a.sum_p99_us > bound)
+    pen = ((unsigned __int128)sp.lambda_milli * ((unsigned __int128)a.sum_p99_us - bound)) /
+          ((unsigned __int128)1000u * a.n_seeds);
+  const int64_t gamma = k.spec_on ? k.draft_len : 0;
+  const int64_t hw = sp.w_conc_micro * k.conc + sp.w_max_micro * k.max_num_seqs + sp.w_spec_micro * gamma;
+  return (int64_t)gp - (int64_t)pen - hw;
+}
+
+__global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs* cands, uint32_t n_cand,
+                                 const slo_config_agg* aggs, uint32_t n_parts, slo_climb_state* state,
+                                 int64_t* scores) {
+  const int lane = threadIdx.x & 31;
+  __shared__ slo_knobs next[32];
+  slo_knobs mine{};
+  slo_config_agg a{0, 0, 0, 0, 0};
+  int64_t s = INT64_MIN;
+  if ((uint32_t)lane < n_cand) {
+    mine = cands[lane];
+    for (uint32_t p = 0; p < n_parts; ++p) {
+      const slo_config_agg x = aggs[(size_t)p * n_cand + lane];
+      a.sum_p99_us += x.sum_p99_us;
+      a.sum_slo_met += x.sum_slo_met;
+      a.sum_window_us += x.sum_window_us;
+      a.n_seeds += x.n_seeds;
+      a.flags |= x.flags;
+    }
+    s = score_micro(a, mine, sp);
+    if (scores) scores[lane] = s;
+  }
+  // argmax over k >= 1, lowest index on ties
+  int64_t bs = (lane >= 1 && (uint32_t)lane < n_cand) ? s : INT64_MIN;
+  int32_t bi = (lane >= 1 && (uint32_t)lane < n_cand) ? lane : 1000;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    const int64_t os = (int64_t)(((uint64_t)__shfl_xor_sync(FULL, (uint32_t)((uint64_t)bs >> 32), d) << 32) |
+                                 __shfl_xor_sync(FULL, (uint32_t)(uint64_t)bs, d));
+    const int32_t oi = __shfl_xor_sync(FULL, bi, d);
+    if (os > bs || (os == bs && oi < bi)) {
+      bs = os;
+      bi = oi;
+    }
+  }
+  const int64_t s0 = (int64_t)(((uint64_t)__shfl_sync(FULL, (uint32_t)((uint64_t)s >> 32), 0) << 32) |
+                               __shfl_sync(FULL, (uint32_t)(uint64_t)s, 0));
+  const uint64_t p99sum0 = shfl64(a.sum_p99_us, 0);
+  const uint32_t n0 = __shfl_sync(FULL, a.n_seeds, 0);
+  __syncwarp();
+  if (lane == 0) {
+    slo_climb_state st = *state;
+    if (!st.has_best || s0 > st.S_best_micro) {
+      st.S_best_micro = s0;
+      st.K_best = cands[0];
+      st.has_best = 1;
+    }
+    int moved_ = 0;
+    uint32_t idx = 0;
+    if (n_cand > 1) {
+      idx = (uint32_t)bi;
+      const __int128 diff = (__int128)bs - (__int128)s0;
+      const bool violated = n0 > 0 && (unsigned __int128)p99sum0 > (unsigned __int128)n0 * sp.slo_us;
+      moved_ = (diff >= (__int128)sp.delta_micro) || (violated && bs > s0);
+      if (!sp.strict_alg1 && bs > st.S_best_micro) {
+        st.S_best_micro = bs;
+        st.K_best = cands[idx];
+      }
+    }
+    const slo_knobs K = moved_ ? cands[idx] : cands[0];
+    st.K = K;
+    st.step += 1;
+    st.moved = moved_;
+    st.argmax = idx;
+    next[0] = K;
+    uint32_t nn = 1 + neighbors_of(space, K, next + 1, n_cand > 0 ? n_cand - 1 : 0);
+    st.n_next = nn;
+    for (uint32_t i = nn; i < n_cand; ++i) {
+      slo_knobs pad{};
+      pad.conc = 0;       // invalid => sentinel outputs, no simulation work
+      pad.workload = 0;
+      next[i] = pad;
+    }
+    *state = st;
+  }
+  __syncwarp();
+  if ((uint32_t)lane < n_cand) cands[lane] = next[lane];
+}
+
+}  // namespace slo

@@ -1,0 +1,138 @@
+// slo_device.cuh — device-side random-number layer of the simulator.
+// Written from the DESIGN.md text, independently of oracle/ (which the product never includes).
+#pragma once
+#include <cstdint>
+
+#include "../../include/slo_sim.h"
+
+namespace slo {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+constexpr uint64_t INF64 = 0xFFFFFFFFFFFFFFFFull;
+
+// ---- Philox4x32-10: 10 rounds of two 32x32->64 products (IMAD.WIDE.U32) + xors.
+struct u32x4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ u32x4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                        uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return {c0, c1, c2, c3};
+}
+
+// ---- E_q(u) ~ 2^32 * -ln((u+1)/2^32) in Q32.32.
+__device__ __forceinline__ uint64_t exp_q32(uint32_t u) {
+  if (u == 0xFFFFFFFFu) return 0;                   // x = 2^32
+  const uint32_t x = u + 1u;                         // [1, 2^32)
+  const int e = 31 - __clz(x);                       // floor(log2 x)
+  const uint32_t m = x << (31 - e);                  // [2^31, 2^32)
+  const int64_t t = (int64_t)(m - 0x80000000u);      // Q0.31
+  int64_t acc = -7511879LL;
+  acc = 49215561LL + ((acc * t) >> 31);
+  acc = -151331885LL + ((acc * t) >> 31);
+  acc = 300247864LL + ((acc * t) >> 31);
+  acc = -455160697LL + ((acc * t) >> 31);
+  acc = 601767258LL + ((acc * t) >> 31);
+  acc = -771198690LL + ((acc * t) >> 31);
+  acc = 1032354281LL + ((acc * t) >> 31);
+  acc = -1549061789LL + ((acc * t) >> 31);
+  acc = 3098163621LL + ((acc * t) >> 31);
+  acc = 0LL + ((acc * t) >> 31);
+  const uint64_t y = ((uint64_t)(32 - e) << 31) - (uint64_t)acc;   // < 2^37
+  // floor(y * 2977044472 / 2^31): y < 2^37 so the 128-bit product is < 2^69
+  const uint64_t lo = y * 2977044472ull;
+  const uint64_t hi = __umul64hi(y, 2977044472ull);
+  return (lo >> 31) | (hi << 33);
+}
+
+// floor(a * b / 2^s) for 0 < s < 64 with a 128-bit intermediate
+__device__ __forceinline__ uint64_t mulshr(uint64_t a, uint64_t b, int s) {
+  const uint64_t lo = a * b;
+  const uint64_t hi = __umul64hi(a, b);
+  return (lo >> s) | (hi << (64 - s));
+}
+
+// ---- lengths: lo + #{l : cw[l] <= u}, by binary search over the cut points.
+__device__ __forceinline__ uint32_t length_of(const uint32_t* __restrict__ cw, uint32_t ncw, uint32_t lo,
+                                              uint32_t u) {
+  uint32_t base = 0, n = ncw;
+  while (n > 0) {
+    const uint32_t half = n >> 1;
+    if (__ldg(cw + base + half) <= u) {
+      base += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo + base;
+}
+
+// ---- FNV-1a-32 of the 32 knob bytes (independent key mode)
+__host__ __device__ inline uint32_t fnv1a_knobs(const slo_knobs& k) {
+  uint8_t b[32];
+  b[0] = k.conc; b[1] = k.max_num_seqs; b[2] = k.draft_len; b[3] = k.spec_on;
+  b[4] = k.draft_width; b[5] = k.workload;
+  b[6] = (uint8_t)(k.rate_scale_q8 & 0xFF); b[7] = (uint8_t)(k.rate_scale_q8 >> 8);
+  for (int i = 0; i < 4; ++i) b[8 + i] = (uint8_t)(k.accept_q16 >> (8 * i));
+  for (int i = 0; i < 4; ++i) b[12 + i] = (uint8_t)(k.max_wait_us >> (8 * i));
+  for (int w = 0; w < 4; ++w)
+    for (int i = 0; i < 4; ++i) b[16 + 4 * w + i] = (uint8_t)(k.reserved[w] >> (8 * i));
+  uint32_t h = 2166136261u;
+  for (int i = 0; i < 32; ++i) h = (h ^ b[i]) * 16777619u;
+  return h;
+}
+
+__host__ __device__ inline bool knobs_valid(const slo_knobs& k, uint32_t n_wl) {
+  return k.conc >= 1 && k.conc <= 32 && k.max_num_seqs >= 1 && k.max_num_seqs <= 32 && k.draft_len <= 16 &&
+         k.spec_on <= 1 && k.draft_width >= 1 && k.draft_width <= 4 && k.workload < n_wl &&
+         k.rate_scale_q8 >= 1 && k.accept_q16 <= 65536u && k.max_wait_us <= 50000u && k.reserved[0] == 0 &&
+         k.reserved[1] == 0 && k.reserved[2] == 0 && k.reserved[3] == 0;
+}
+
+// ---- warp helpers
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(FULL, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(FULL, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t shfl_up64(uint64_t v, int d) {
+  const uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, d);
+  const uint32_t hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), d);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t warp_incl_scan64(uint64_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t o = shfl_up64(v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, d);
+    const uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), d);
+    v += ((uint64_t)hi << 32) | lo;
+  }
+  return v;
+}
+
+}  // namespace slo

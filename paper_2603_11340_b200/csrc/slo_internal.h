@@ -1,0 +1,52 @@
+// slo_internal.h — shared between the kernels and the C-ABI glue of libslosim.so (not installed).
+#pragma once
+#include <cstdint>
+
+#include "../../include/slo_sim.h"
+
+namespace slo {
+
+constexpr int kMaxWarpsPerBlock = 8;
+constexpr int kDefaultWarpsPerBlock = 4;
+
+struct DevWorkload {      // device copy of one slo_workload
+  uint32_t kind, start_state;
+  uint64_t gap_q16[2];
+  uint64_t soj[2];
+  uint32_t p_lo, p_ncw, p_off;
+  uint32_t o_lo, o_ncw, o_off;
+  slo_timing t;
+  uint32_t stream_id, pad;
+};
+
+struct SimParams {
+  const slo_knobs* cfg;
+  const uint64_t* seeds;
+  const DevWorkload* wl;
+  const uint32_t* tables;
+  uint32_t* queue;
+  uint32_t* p99;
+  double* goodput;
+  slo_replica_result* detail;
+  uint32_t* lat;
+  slo_stats* stats;
+  uint32_t n_cfg, n_seeds, n_rep, n_wl;
+  uint32_t warmup, seg, slo_us, crn;
+  uint32_t topk, cap, warp_bytes, pad;
+};
+
+__global__ void slo_sim_kernel(const SimParams p);
+__global__ void slo_aggregate_kernel(const slo_replica_result* detail, uint32_t n_cfg, uint32_t n_seeds,
+                                     slo_config_agg* agg);
+__global__ void slo_aggregate_reduce_kernel(const slo_config_agg* parts, uint32_t n_parts, uint32_t n_cfg,
+                                            slo_config_agg* out);
+__global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs* cands, uint32_t n_cand,
+                                 const slo_config_agg* aggs, uint32_t n_parts, slo_climb_state* state,
+                                 int64_t* scores);
+
+// host+device neighbour generation
+__host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& K, slo_knobs* out, uint32_t cap);
+
+size_t warp_bytes_for(uint32_t cap);
+
+}  // namespace slo

@@ -1,0 +1,238 @@
+"""Python face of libslosim.so: torch supplies device memory and streams; the library does all the work.
+
+    from paper_2603_11340_b200 import inputs, sim
+    s = sim.Simulator([inputs.preset_ll()])
+    out = s.run_batch(sim.knobs_tensor(cfg.knobs), sim.seeds_tensor(cfg.seeds()), 10_000)
+    out["p99_us"], out["goodput"]        # per replica (config-major)
+
+Paper map: run_batch = the simulator segment + Eq. (1) goodput + empirical p99;
+aggregate / hillclimb_step = Eq. (2)-(3) + Alg. 1.  Exact definitions: DESIGN.md §2.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, Iterable, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (AGG_DTYPE, CLIMB_DTYPE, KNOB_DTYPE, RESULT_DTYPE, STATS_DTYPE, check, lib, slo_knobs,
+                   slo_score_params, slo_space)
+
+__all__ = ["Simulator", "pack_knobs", "knobs_tensor", "seeds_tensor", "neighbors", "space_struct",
+           "score_struct", "unpack"]
+
+
+# ------------------------------------------------------------------------------------------------
+# packing helpers
+# ------------------------------------------------------------------------------------------------
+def pack_knobs(knobs: Sequence[Dict]) -> np.ndarray:
+    arr = np.zeros(len(knobs), KNOB_DTYPE)
+    for i, k in enumerate(knobs):
+        for f in ("conc", "max_num_seqs", "draft_len", "spec_on", "draft_width", "workload", "rate_scale_q8",
+                  "accept_q16", "max_wait_us"):
+            arr[i][f] = k[f]
+        if "reserved" in k:
+            arr[i]["reserved"] = k["reserved"]
+    return arr
+
+
+def unpack_knobs(arr) -> List[Dict]:
+    a = np.asarray(arr).view(KNOB_DTYPE).reshape(-1)
+    return [dict(conc=int(x["conc"]), max_num_seqs=int(x["max_num_seqs"]), draft_len=int(x["draft_len"]),
+                 spec_on=int(x["spec_on"]), draft_width=int(x["draft_width"]), workload=int(x["workload"]),
+                 rate_scale_q8=int(x["rate_scale_q8"]), accept_q16=int(x["accept_q16"]),
+                 max_wait_us=int(x["max_wait_us"])) for x in a]
+
+
+def knobs_tensor(knobs, device="cuda") -> torch.Tensor:
+    """uint8 [n, 32] tensor of slo_knobs records."""
+    arr = knobs if isinstance(knobs, np.ndarray) else pack_knobs(knobs)
+    t = torch.from_numpy(arr.view(np.uint8).reshape(-1, 32).copy())
+    return t.to(device) if device != "cpu" else t
+
+
+def seeds_tensor(seeds: Iterable[int], device="cuda") -> torch.Tensor:
+    """int64 tensor holding the u64 seed bits."""
+    a = np.array(list(seeds), dtype=np.uint64).view(np.int64)
+    t = torch.from_numpy(a.copy())
+    return t.to(device) if device != "cpu" else t
+
+
+def unpack(t: torch.Tensor, dtype: np.dtype) -> np.ndarray:
+    """Host numpy structured view of a byte tensor holding PODs."""
+    return t.detach().cpu().contiguous().view(torch.uint8).numpy().view(dtype).reshape(-1)
+
+
+def space_struct(space: Dict) -> slo_space:
+    s = slo_space()
+    s.stencil = space["stencil"]
+    for d in range(5):
+        s.lo[d], s.hi[d], s.step[d] = space["lo"][d], space["hi"][d], space["step"][d]
+    return s
+
+
+def score_struct(sp: Dict) -> slo_score_params:
+    s = slo_score_params()
+    for f, _ in slo_score_params._fields_:
+        setattr(s, f, sp[f])
+    return s
+
+
+def neighbors(space: Dict, K: Dict) -> List[Dict]:
+    """Host-side neighbour list (same generator the climb kernel runs)."""
+    k = pack_knobs([K])
+    out = np.zeros(32, KNOB_DTYPE)
+    n = C.c_uint32(0)
+    check(lib().slo_neighbors(C.byref(space_struct(space)), k.ctypes.data, out.ctypes.data, 32, C.byref(n)))
+    return unpack_knobs(out[: n.value])
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+# ------------------------------------------------------------------------------------------------
+class Simulator:
+    """One libslosim handle on one CUDA device."""
+
+    def __init__(self, workloads: Sequence[Dict], device: Optional[int] = None, crn: int = 1,
+                 warps_per_block: int = 0, blocks_per_sm: int = 0):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self.workloads = list(workloads)
+        n = len(self.workloads)
+        arr = (_lib.slo_workload * n)()
+        self._keep = []
+        for w, d in zip(arr, self.workloads):
+            ar = d["arrivals"]
+            w.arr.kind, w.arr.start_state = ar["kind"], ar["start_state"]
+            for s in range(2):
+                w.arr.mean_gap_q16[s] = ar["mean_gap_q16"][s]
+                w.arr.mean_sojourn_us[s] = ar["mean_sojourn_us"][s]
+            for name in ("prompt", "output"):
+                cw = list(d[name]["cw"])
+                buf = (C.c_uint32 * max(1, len(cw)))(*cw)
+                self._keep.append(buf)
+                setattr(w, name + "_cw", C.cast(buf, C.POINTER(C.c_uint32)))
+                setattr(w, name + "_lo", d[name]["lo"])
+                setattr(w, name + "_ncw", len(cw))
+            for f, v in d["timing"].items():
+                setattr(w.timing, f, v)
+            w.stream_id = d["stream_id"]
+        opts = _lib.slo_sim_opts()
+        opts.crn, opts.warps_per_block, opts.blocks_per_sm = crn, warps_per_block, blocks_per_sm
+        h = C.c_void_p()
+        check(lib().slo_sim_create(self.device, arr, n, C.byref(opts), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().slo_sim_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> Dict:
+        i = _lib.slo_sim_info()
+        check(lib().slo_sim_get_info(self.h, C.byref(i)), self.h)
+        return {f: getattr(i, f) for f, _ in _lib.slo_sim_info._fields_ if f != "reserved"}
+
+    # -------------------------------------------------------------------------------------------
+    def alloc_outputs(self, n_rep: int, detail=True, latencies_n: int = 0, stats=False) -> Dict:
+        dev = torch.device("cuda", self.device)
+        out = dict(p99_us=torch.empty(n_rep, dtype=torch.int32, device=dev),
+                   goodput=torch.empty(n_rep, dtype=torch.float64, device=dev))
+        if detail:
+            out["detail"] = torch.empty((n_rep, 32), dtype=torch.uint8, device=dev)
+        if latencies_n:
+            out["latencies"] = torch.empty(n_rep * latencies_n, dtype=torch.int32, device=dev)
+        if stats:
+            out["stats"] = torch.empty(64, dtype=torch.uint8, device=dev)
+        return out
+
+    def run_batch(self, configs: torch.Tensor, seeds: torch.Tensor, segment_len: int, warmup_len: int = 0,
+                  slo_us: int = 1_200_000, detail: bool = True, latencies: bool = False, stats: bool = False,
+                  out: Optional[Dict] = None, stream=None) -> Dict:
+        """K1 over n_configs x n_seeds replicas (config-major).  Asynchronous on `stream`."""
+        n_cfg = configs.shape[0]
+        n_seeds = seeds.shape[0]
+        if out is None:
+            out = self.alloc_outputs(n_cfg * n_seeds, detail, (segment_len + warmup_len) if latencies else 0, stats)
+        check(lib().slo_sim_run_batch(self.h, configs.data_ptr(), n_cfg, seeds.data_ptr(), n_seeds, segment_len,
+                                      warmup_len, slo_us, out["p99_us"].data_ptr(), out["goodput"].data_ptr(),
+                                      _ptr(out.get("detail")), _ptr(out.get("latencies")), _ptr(out.get("stats")),
+                                      _stream_ptr(stream)), self.h)
+        return out
+
+    def run_batch_host(self, h_configs: np.ndarray, h_seeds: np.ndarray, segment_len: int, warmup_len: int = 0,
+                       slo_us: int = 1_200_000, out: Optional[Dict] = None, detail: bool = False,
+                       stats: bool = False, stream=None) -> Dict:
+        """The end-to-end call on host buffers (pinned torch CPU tensors recommended); synchronous."""
+        n_cfg = h_configs.shape[0]
+        n_seeds = h_seeds.shape[0]
+        R = n_cfg * n_seeds
+        if out is None:
+            pin = torch.cuda.is_available()
+            out = dict(p99_us=torch.empty(R, dtype=torch.int32, pin_memory=pin),
+                       goodput=torch.empty(R, dtype=torch.float64, pin_memory=pin))
+            if detail:
+                out["detail"] = torch.empty((R, 32), dtype=torch.uint8, pin_memory=pin)
+            if stats:
+                out["stats"] = torch.empty(64, dtype=torch.uint8, pin_memory=pin)
+        check(lib().slo_sim_run_batch_host(self.h, h_configs.data_ptr(), n_cfg, h_seeds.data_ptr(), n_seeds,
+                                           segment_len, warmup_len, slo_us, out["p99_us"].data_ptr(),
+                                           out["goodput"].data_ptr(), _ptr(out.get("detail")),
+                                           _ptr(out.get("stats")), _stream_ptr(stream)), self.h)
+        return out
+
+    def aggregate(self, detail: torch.Tensor, n_configs: int, n_seeds: int, out: Optional[torch.Tensor] = None,
+                  stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((n_configs, 32), dtype=torch.uint8, device=detail.device)
+        check(lib().slo_aggregate(self.h, detail.data_ptr(), n_configs, n_seeds, out.data_ptr(),
+                                  _stream_ptr(stream)), self.h)
+        return out
+
+    def aggregate_reduce(self, parts: torch.Tensor, n_parts: int, n_configs: int,
+                         out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((n_configs, 32), dtype=torch.uint8, device=parts.device)
+        check(lib().slo_aggregate_reduce(self.h, parts.data_ptr(), n_parts, n_configs, out.data_ptr(),
+                                         _stream_ptr(stream)), self.h)
+        return out
+
+    def climb_state(self, K0: Dict) -> torch.Tensor:
+        st = np.zeros(1, CLIMB_DTYPE)
+        k = pack_knobs([K0])[0]
+        st[0]["K"] = k
+        st[0]["K_best"] = k
+        st[0]["S_best_micro"] = -(1 << 63)
+        return torch.from_numpy(st.view(np.uint8).copy()).to(torch.device("cuda", self.device))
+
+    def candidates(self, space: Dict, K: Dict, n_cand: int) -> torch.Tensor:
+        """[K, neighbours(K), padding] as a device uint8 [n_cand, 32] tensor (the climb's first step)."""
+        from .inputs import PAD_KNOBS
+        nb = neighbors(space, K)[: n_cand - 1]
+        cands = [K] + nb + [PAD_KNOBS] * (n_cand - 1 - len(nb))
+        return knobs_tensor(cands, device=torch.device("cuda", self.device))
+
+    def hillclimb_step(self, space: Dict, sp: Dict, cands: torch.Tensor, aggs: torch.Tensor, n_parts: int,
+                       state: torch.Tensor, scores: Optional[torch.Tensor] = None, stream=None) -> None:
+        """K3: Alg. 1 step on the device; rewrites `cands` in place with the next candidate list."""
+        n_cand = cands.shape[0]
+        check(lib().slo_hillclimb_step(self.h, C.byref(space_struct(space)), C.byref(score_struct(sp)),
+                                       cands.data_ptr(), n_cand, aggs.data_ptr(), n_parts, state.data_ptr(),
+                                       _ptr(scores), _stream_ptr(stream)), self.h)

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element, bit-exact.
+
+Integer outputs (every latency, p99, slo_met, window, sum, flags, work counters) and the goodput double
+must be identical (the model is integer-exact; goodput is one IEEE division on both sides).
+"""
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_11340_b200 import inputs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def S():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2603_11340_b200 import sim
+    assert torch.cuda.is_available()
+    return sim
+
+
+def _run_gpu(sim, wls, ks, seeds, N, warmup=0, slo=1_200_000, crn=1, latencies=True, sim_obj=None, **kw):
+    s = sim_obj or sim.Simulator(wls, device=0, crn=crn, **kw)
+    out = s.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(seeds), N, warmup_len=warmup, slo_us=slo,
+                      latencies=latencies, stats=True)
+    torch.cuda.synchronize()
+    from paper_2603_11340_b200._lib import RESULT_DTYPE, STATS_DTYPE
+    res = dict(p99=out["p99_us"].cpu().numpy().view(np.uint32), gp=out["goodput"].cpu().numpy(),
+               detail=sim.unpack(out["detail"], RESULT_DTYPE), stats=sim.unpack(out["stats"], STATS_DTYPE)[0])
+    if latencies:
+        res["lat"] = out["latencies"].cpu().numpy().view(np.uint32).reshape(len(ks) * len(seeds), N + warmup)
+    if sim_obj is None:
+        s.close()
+    return res
+
+
+def _compare_replica(orc, g, r, wls, k, seed, N, warmup, slo, crn=1, check_lat=True):
+    ref = orc.run(wls, k, seed, N, warmup_len=warmup, slo_us=slo, crn=crn, latencies=check_lat)
+    d = g["detail"][r]
+    tag = f"replica {r} knobs {k}"
+    if check_lat:
+        assert np.array_equal(g["lat"][r], ref["latencies"]), tag
+    assert int(g["p99"][r]) == ref["p99_us"], tag
+    assert g["gp"][r] == ref["goodput"], tag
+    assert int(d["p99_us"]) == ref["p99_us"] and int(d["slo_met"]) == ref["slo_met"], tag
+    assert int(d["n_measured"]) == ref["n_measured"] and int(d["flags"]) == ref["flags"], tag
+    assert int(d["window_us"]) == ref["window_us"] and int(d["sum_latency_us"]) == ref["sum_latency_us"], tag
+    return ref
+
+
+def test_c1_full_bit_exact(S, orc):
+    """BASELINE config 1 in full: 1 replica x 2,000 requests, every latency."""
+    cfg = inputs.config_c1()
+    g = _run_gpu(S, cfg.workloads, cfg.knobs, cfg.seeds(), cfg.segment_len)
+    ref = _compare_replica(orc, g, 0, cfg.workloads, cfg.knobs[0], cfg.seeds()[0], cfg.segment_len, 0, cfg.slo_us)
+    st = g["stats"]
+    c = ref["counters"]
+    assert int(st["requests"]) == 2000 and int(st["batches"]) == c["batches"]
+    assert int(st["decode_steps"]) == c["decode_steps"] and int(st["member_steps"]) == c["member_steps"]
+    assert int(st["philox_blocks"]) == c["philox_blocks"]
+
+
+WLS = None
+
+
+def _wls():
+    return [inputs.preset_ll(), inputs.preset_sim(), inputs.preset_stress(kind=1), inputs.preset_stress(kind=2),
+            inputs.preset_ll(rate=40.0, stream_id=7)]
+
+
+@pytest.mark.parametrize("block", range(6))
+def test_random_small_configs(S, orc, block):
+    """Random valid knob records over every workload kind, lengths spanning several 32-request windows
+    and a ragged tail, warmup on/off — every latency and output bit-exact, plus the work counters."""
+    rng = random.Random(500 + block)
+    wls = _wls()
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)]
+    ks[0] = inputs.knobs(conc=32, max_num_seqs=32, draft_len=16, spec_on=1, accept_q16=65536, workload=1)
+    ks[1] = inputs.knobs(conc=1, max_num_seqs=1, draft_len=16, spec_on=1, accept_q16=0)
+    ks[2] = inputs.knobs(conc=32, max_num_seqs=1, max_wait_us=50_000, workload=2)
+    ks[3] = inputs.knobs(conc=1, max_num_seqs=32, max_wait_us=50_000, workload=3)
+    seeds = inputs.seeds(3, 77 * block)
+    N = rng.choice([37, 333, 1000, 1234])
+    warmup = rng.choice([0, 0, 17, 100])
+    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup)
+    tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
+    for ci, k in enumerate(ks):
+        for si, sd in enumerate(seeds):
+            ref = _compare_replica(orc, g, ci * len(seeds) + si, wls, k, sd, N, warmup, 1_200_000)
+            for f in tot:
+                tot[f] += ref["counters"][f]
+    for f in tot:
+        assert int(g["stats"][f]) == tot[f], f
+
+
+def test_edge_cases(S, orc):
+    """Degenerate sizes and values: one request, N < 32, invalid records, saturating SLO, zero noise."""
+    wls = [inputs.preset_ll(), inputs.workload(kind=0, rate=1000.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0))]
+    ks = [inputs.knobs(conc=8, max_num_seqs=16), inputs.knobs(conc=0), inputs.knobs(max_num_seqs=33),
+          inputs.knobs(draft_len=17, spec_on=1), inputs.knobs(workload=2), dict(inputs.knobs(), reserved=[0, 1, 0, 0]),
+          inputs.knobs(conc=32, max_num_seqs=32, workload=1), inputs.knobs(conc=3, max_num_seqs=2, workload=1,
+                                                                          draft_len=3, spec_on=1)]
+    seeds = inputs.seeds(2, 900)
+    for N, warm in ((1, 0), (1, 5), (31, 0), (32, 1), (33, 0), (65, 64)):
+        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm)
+        for ci, k in enumerate(ks):
+            for si, sd in enumerate(seeds):
+                r = ci * len(seeds) + si
+                valid = orc.knobs_valid(k, len(wls))
+                if not valid:
+                    assert int(g["p99"][r]) == 0xFFFFFFFF and g["gp"][r] == -1.0 and g["detail"][r]["flags"] == 1
+                    continue
+                _compare_replica(orc, g, r, wls, k, sd, N, warm, 1_200_000)
+
+
+def test_independent_key_mode(S, orc):
+    wls = [inputs.preset_ll()]
+    ks = [inputs.knobs(conc=c, max_num_seqs=b) for c, b in ((4, 4), (8, 2), (16, 16))]
+    seeds = inputs.seeds(2, 5)
+    g = _run_gpu(S, wls, ks, seeds, 700, crn=0)
+    for ci, k in enumerate(ks):
+        for si, sd in enumerate(seeds):
+            _compare_replica(orc, g, ci * 2 + si, wls, k, sd, 700, 0, 1_200_000, crn=0)
+
+
+def test_slo_boundaries(S, orc):
+    """ell <= SLO is inclusive (R7): SLO 0 and a huge SLO."""
+    wls = [inputs.preset_ll()]
+    ks = [inputs.knobs(conc=8, max_num_seqs=8, draft_len=4, spec_on=1)]
+    sd = inputs.seeds(1, 3)
+    for slo in (0, 1, 700_000, 0xFFFFFFFE):
+        g = _run_gpu(S, wls, ks, sd, 400, slo=slo)
+        _compare_replica(orc, g, 0, wls, ks[0], sd[0], 400, 0, slo)
+
+
+def _sample_rows(n, k, rng, must=()):
+    rows = set(must)
+    while len(rows) < min(k, n):
+        rows.add(rng.randrange(n))
+    return sorted(rows)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_sampled(S, orc, name):
+    """BASELINE configs 2 and 3 at full size in the bench's launch configuration; sampled replicas
+    (every speculation setting, the knob boundaries, random picks) recomputed one by one by the oracle."""
+    cfg = inputs.config_c2() if name == "C2" else inputs.config_c3()
+    g = _run_gpu(S, cfg.workloads, cfg.knobs, cfg.seeds(), cfg.segment_len, latencies=False)
+    n_seeds = cfg.n_seeds
+    rng = random.Random(11)
+    cfg_rows = _sample_rows(len(cfg.knobs), 16, rng, must=(0, len(cfg.knobs) - 1, len(cfg.knobs) // 2))
+    for ci in cfg_rows:
+        for si in (0, rng.randrange(n_seeds), n_seeds - 1):
+            r = ci * n_seeds + si
+            _compare_replica(orc, g, r, cfg.workloads, cfg.knobs[ci], cfg.seeds()[si], cfg.segment_len, 0,
+                             cfg.slo_us, check_lat=False)
+    # properties that hold at any size
+    d = g["detail"]
+    assert np.all(d["slo_met"] <= d["n_measured"]) and np.all(d["flags"] & 1 == 0)
+    assert np.all(g["gp"] <= d["n_measured"] * 1e6 / d["window_us"] + 1e-9)
+    assert int(g["stats"]["requests"]) == cfg.requests
+
+
+def test_c5_sampled(S, orc):
+    """Stress grid (MMPP-2, BASELINE config 5) on a 4,096-config slice, sampled replicas bit-exact."""
+    cfg = inputs.config_c5(limit=4096)
+    g = _run_gpu(S, cfg.workloads, cfg.knobs, cfg.seeds(), cfg.segment_len, latencies=False)
+    rng = random.Random(5)
+    for ci in _sample_rows(len(cfg.knobs), 24, rng, must=(0, 4095)):
+        si = rng.randrange(cfg.n_seeds)
+        _compare_replica(orc, g, ci * cfg.n_seeds + si, cfg.workloads, cfg.knobs[ci], cfg.seeds()[si],
+                         cfg.segment_len, 0, cfg.slo_us, check_lat=False)
+
+
+def test_host_entry_matches_device_entry(S):
+    cfg = inputs.config_c3(n_seeds=8, segment_len=600)
+    s = S.Simulator(cfg.workloads, device=0)
+    dev = s.run_batch(S.knobs_tensor(cfg.knobs), S.seeds_tensor(cfg.seeds()), 600, stats=True)
+    torch.cuda.synchronize()
+    hk = S.knobs_tensor(cfg.knobs, device="cpu").pin_memory()
+    hs = S.seeds_tensor(cfg.seeds(), device="cpu").pin_memory()
+    host = s.run_batch_host(hk, hs, 600, detail=True, stats=True)
+    assert torch.equal(host["p99_us"], dev["p99_us"].cpu())
+    assert torch.equal(host["goodput"], dev["goodput"].cpu())
+    assert torch.equal(host["detail"], dev["detail"].cpu())
+    assert torch.equal(host["stats"], dev["stats"].cpu())
+    s.close()
+
+
+def test_aggregate_kernels(S, orc):
+    from oracle import climb
+    from paper_2603_11340_b200._lib import AGG_DTYPE
+    cfg = inputs.config_c3(n_seeds=5, segment_len=300)
+    s = S.Simulator(cfg.workloads, device=0)
+    out = s.run_batch(S.knobs_tensor(cfg.knobs), S.seeds_tensor(cfg.seeds()), 300)
+    agg = s.aggregate(out["detail"], len(cfg.knobs), cfg.n_seeds)
+    parts = torch.cat([agg, agg, agg])
+    red = s.aggregate_reduce(parts, 3, len(cfg.knobs))
+    torch.cuda.synchronize()
+    a = S.unpack(agg, AGG_DTYPE)
+    r3 = S.unpack(red, AGG_DTYPE)
+    for ci in range(0, len(cfg.knobs), 7):
+        refs = [orc.run(cfg.workloads, cfg.knobs[ci], sd, 300) for sd in cfg.seeds()]
+        ra = climb.aggregate(refs)
+        for f in ("sum_p99_us", "sum_slo_met", "sum_window_us", "n_seeds", "flags"):
+            assert int(a[ci][f]) == ra[f]
+            if f != "flags":
+                assert int(r3[ci][f]) == 3 * ra[f]
+    s.close()
+
+
+def test_device_climb_matches_oracle(S, orc):
+    """K3 (score, argmax, move, best-so-far, next stencil) over several Alg. 1 steps, against oracle/climb.py
+    fed with oracle replicas: identical scores, moves and trajectories (C4-shaped, reduced sizes)."""
+    from oracle import climb
+    from paper_2603_11340_b200._lib import CLIMB_DTYPE
+    wls = [inputs.preset_ll()]
+    space, sp = inputs.SPACE_WIDE32, dict(inputs.SCORE_DEFAULTS)
+    n_seeds, N, n_cand = 4, 400, 32
+    seeds = inputs.seeds(n_seeds, 31)
+    s = S.Simulator(wls, device=0)
+    K = dict(inputs.K0)
+    cands_t = s.candidates(space, K, n_cand)
+    state_t = s.climb_state(K)
+    seeds_t = S.seeds_tensor(seeds)
+    ost = climb.initial_state(K)
+    ocands = [K] + climb.neighbours(space, K)
+    ocands += [inputs.PAD_KNOBS] * (n_cand - len(ocands))
+    for step in range(4):
+        out = s.run_batch(cands_t, seeds_t, N)
+        aggs = s.aggregate(out["detail"], n_cand, n_seeds)
+        scores = torch.empty(n_cand, dtype=torch.int64, device="cuda")
+        s.hillclimb_step(space, sp, cands_t, aggs, 1, state_t, scores)
+        torch.cuda.synchronize()
+        oaggs = [climb.aggregate([orc.run(wls, c, sd, N) for sd in seeds]) for c in ocands]
+        ost, moved, idx, oscores = climb.step(ost, ocands, oaggs, sp)
+        assert scores.cpu().tolist() == oscores, step
+        st = S.unpack(state_t, CLIMB_DTYPE)[0]
+        assert int(st["moved"]) == int(moved) and int(st["argmax"]) == idx
+        assert S.unpack_knobs(st["K"])[0] == ost["K"]
+        assert int(st["S_best_micro"]) == ost["S_best"]
+        assert S.unpack_knobs(st["K_best"])[0] == ost["K_best"]
+        ocands = [ost["K"]] + climb.neighbours(space, ost["K"])
+        ocands += [inputs.PAD_KNOBS] * (n_cand - len(ocands))
+        assert S.unpack_knobs(cands_t.cpu().numpy())[: int(st["n_next"])] == ocands[: int(st["n_next"])]
+    s.close()
+
+
+def test_launch_shapes_agree(S, orc):
+    """The result does not depend on the launch shape (warps per block, blocks per SM)."""
+    wls = [inputs.preset_ll()]
+    cfg = inputs.config_c3(n_seeds=4, segment_len=500)
+    base = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=True)
+    for wpb, bps in ((1, 1), (8, 0), (2, 3)):
+        g = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=True, warps_per_block=wpb, blocks_per_sm=bps)
+        assert np.array_equal(g["lat"], base["lat"]) and np.array_equal(g["gp"], base["gp"])
