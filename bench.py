@@ -1,0 +1,352 @@
+"""bench.py — simulated requests/s of the batched SLO-Tuner simulator on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1|c3|c4|c5] [--impl ours|reference]
+
+One step = one pass of the whole hot path (K1 simulate every replica -> K2 per-config
+aggregation -> [N>1: NCCL all-gather of the aggregates + K2b reduce] (+ K3 climb step for c4)) over one
+batch of synthetic input already resident in HBM.  Default workload = BASELINE config 2 (16 C x 8 B x 4 spec
+x 64 seeds, 10k-request segments, LL preset).  N>1 (torchrun): weak scaling, every rank runs the full grid
+on its own seed block; value = all ranks' simulated requests / max-over-ranks device time.
+
+`--impl reference`: the CPU oracle (oracle/, as it stands) on the host cores on a bounded sample of the
+same workload — the tier's reference arm.  The oracle is otherwise only used by the cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DESCR = {
+    "c1": "C1 single replica: C=8, B=16, no speculation, Poisson 10 req/s, 2,000 requests, SLO 1.2 s",
+    "c2": "C2 knob grid 16 concurrency x 8 batch limits x 4 speculation settings x 64 seeds, 10k-request segments",
+    "c3": "C3 speculative sweep: draft length 0-8 x acceptance .3-.9, C=B=8, 256 seeds, 10k-request segments",
+    "c4": "C4 hill-climb step: 32 candidates (wide-32 stencil) x 128 seeds, 5k-request segments",
+    "c5": "C5 stress grid slice: MMPP-2 bursty arrivals, 65,536 configs x 16 seeds, 2k-request segments",
+}
+# Philox4x32-10 minimum integer lane-ops per block: 10 rounds x (2 widening multiplies + 2 three-input
+# XORs + 2 key additions) — the irreducible algorithmic work.
+OPS_PER_PHILOX_BLOCK = 60
+
+
+def make_config(name):
+    from paper_2603_11340_b200 import inputs
+    if name == "c1":
+        return inputs.config_c1()
+    if name == "c2":
+        return inputs.config_c2()
+    if name == "c3":
+        return inputs.config_c3()
+    if name == "c4":
+        return inputs.config_c4()
+    if name == "c5":
+        return inputs.config_c5(limit=65536)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def peaks():
+    p = {"hbm_gbs": 6458.7, "sm_max_mhz": 1965.0, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        p.update(hbm_gbs=m["hbm_gbs"], sm_max_mhz=m["sm_max_mhz"], source="measured")
+    except Exception:
+        pass
+    return p
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------------
+def _oracle_task(args):
+    wls, k, seed, n = args
+    import oracle
+    r = oracle.run(wls, k, seed, n)
+    return n, r["p99_us"]
+
+
+def cpu_oracle_sample(cfg, budget_s=12.0, seed_offset=0):
+    """Run the oracle on (config, seed) replicas of cfg in a fixed seed-major order on all host cores
+    until ~budget_s elapse; returns (requests/s, cores, replicas, requests, seconds)."""
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    seeds = cfg.seeds()
+    tasks = [(cfg.workloads, k, seeds[s], cfg.segment_len)
+             for s in range(cfg.n_seeds) for k in cfg.knobs]
+    ctx = mp.get_context("spawn")
+    done_req = 0
+    done_rep = 0
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_task, [tasks[0]] * cores)          # warm the workers
+        t0 = time.perf_counter()
+        it = pool.imap(_oracle_task, tasks, chunksize=1)
+        for n, _ in it:
+            done_req += n
+            done_rep += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        pool.terminate()
+    return done_req / dt, cores, done_rep, done_req, dt
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+# ------------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"slo_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9 and f[1].replace(".", "").isdigit():
+                rows.append(f)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "samples": len(rows),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(DESCR))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = make_config(args.workload)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        per_step = max(3.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+        vals = []
+        for s in range(args.warmup + args.steps):
+            v, cores, reps, reqs, dt = cpu_oracle_sample(cfg, budget_s=per_step)
+            if s >= args.warmup:
+                vals.append((v, reqs, dt))
+        tot_req = sum(x[1] for x in vals)
+        tot_t = sum(x[2] for x in vals)
+        value = tot_req / tot_t
+        sample = (f"per step: the first ~{per_step:.0f} s of oracle replicas of {args.workload.upper()} "
+                  f"(seed-major order), {cores} worker processes")
+        print(json.dumps({
+            "impl": "reference", "metric": "simulated requests/s", "value": value, "unit": "requests/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * tot_t / len(vals), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": DESCR[args.workload], "replicas_per_step_sampled": vals and int(vals[0][1] / (cfg.segment_len + cfg.warmup_len))},
+            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    if rank == 0 or world == 1:
+        __graft_entry__.build()
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.barrier()
+        if rank != 0:
+            __graft_entry__.build()
+    from paper_2603_11340_b200 import inputs, sim
+    from paper_2603_11340_b200._lib import STATS_DTYPE
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    S = sim.Simulator(cfg.workloads, device=local)
+    info = S.info()
+
+    # weak scaling: every rank runs the full grid on its own seed block
+    seeds = inputs.seeds(cfg.n_seeds, cfg.seed_offset + rank * cfg.n_seeds)
+    n_cfg = len(cfg.knobs)
+    N = cfg.segment_len + cfg.warmup_len
+    seeds_t = sim.seeds_tensor(seeds, device=dev)
+    if args.workload == "c4":
+        space, sp = cfg.extra["space"], cfg.extra["score"]
+        n_cfg = cfg.extra["n_cand"]
+        cands = S.candidates(space, cfg.knobs[0], n_cfg)
+        state = S.climb_state(cfg.knobs[0])
+    else:
+        cands = sim.knobs_tensor(cfg.knobs, device=dev)
+    R = n_cfg * cfg.n_seeds
+    out = S.alloc_outputs(R, detail=True, stats=True)
+    agg = torch.empty((n_cfg, 32), dtype=torch.uint8, device=dev)
+    parts = torch.empty((world * n_cfg, 32), dtype=torch.uint8, device=dev) if world > 1 else None
+    pooled = torch.empty((n_cfg, 32), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    k1_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k1_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    st_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches_per_step = 2 + (1 if world > 1 else 0) + (1 if args.workload == "c4" else 0)
+
+    def step(i=None):
+        if i is not None:
+            k1_start[i].record(stream)
+        S.run_batch(cands, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out, stream=stream)
+        if i is not None:
+            k1_end[i].record(stream)
+        S.aggregate(out["detail"], n_cfg, cfg.n_seeds, out=agg, stream=stream)
+        total = agg
+        if world > 1:
+            dist.all_gather_into_tensor(parts, agg)
+            S.aggregate_reduce(parts, world, n_cfg, out=pooled, stream=stream)
+            total = pooled
+        if args.workload == "c4":
+            S.hillclimb_step(space, sp, cands, total, 1, state, stream=stream)
+        if i is not None:
+            st_end[i].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = sim.unpack(out["stats"], STATS_DTYPE)[0]       # work of one step (the last warm-up)
+
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.zero_()                                       # L2 flush between timed steps (not timed)
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [k1_start[i].elapsed_time(st_end[i]) for i in range(args.steps)]
+    k1_ms = [k1_start[i].elapsed_time(k1_end[i]) for i in range(args.steps)]
+    t_total = sum(step_ms) / 1000.0
+    t_k1 = sum(k1_ms) / 1000.0
+    if world > 1:
+        tt = torch.tensor([t_total, t_k1], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total, t_k1 = tt.tolist()
+
+    req_per_step = R * N
+    value = world * req_per_step * args.steps / t_total
+
+    # ---- e2e: the public API on HOST buffers (pinned), H2D + D2H inside the timed region
+    hk = sim.knobs_tensor(cfg.knobs if args.workload != "c4" else sim.unpack_knobs(cands.cpu().numpy()),
+                          device="cpu").pin_memory()
+    hs = sim.seeds_tensor(seeds, device="cpu").pin_memory()
+    hout = dict(p99_us=torch.empty(R, dtype=torch.int32).pin_memory(),
+                goodput=torch.empty(R, dtype=torch.float64).pin_memory())
+    S.run_batch_host(hk, hs, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=hout)
+    e2e_steps = max(1, min(args.steps, 5))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        S.run_batch_host(hk, hs, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=hout)
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        te = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        t_e2e = te.item()
+    e2e = {"value": world * req_per_step * e2e_steps / t_e2e, "unit": "requests/s",
+           "h2d_bytes_per_step": hk.numel() + hs.numel() * 8,
+           "d2h_bytes_per_step": R * 4 + R * 8}
+
+    if rank == 0:
+        pk = peaks()
+        blocks = int(stats["philox_blocks"])
+        peak_gops = 148 * 4 * 32 * pk["sm_max_mhz"] * 1e6 / 1e9      # lane-ops/s at 1 warp-instr/clk/SMSP
+        achieved_gops = blocks * OPS_PER_PHILOX_BLOCK / (t_k1 / args.steps) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                traffic = json.load(fh).get(args.workload)
+        except Exception:
+            pass
+        line = {
+            "metric": "simulated requests/s", "value": value, "unit": "requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": DESCR[args.workload], "replicas_per_gpu": R, "requests_per_replica": N,
+                       "requests_per_step_per_gpu": req_per_step, "preset": "LL" if args.workload != "c5" else "STRESS",
+                       "l2": "flushed between timed steps (256 MiB write, untimed); inputs are < 1 MB",
+                       "parallelism": f"dp{world} over replicas (seed blocks)",
+                       "launch": {"blocks_per_sm": info["blocks_per_sm"], "warps_per_block": info["warps_per_block"],
+                                  "regs_per_thread": info["regs_per_thread"]}},
+            "replica_segments_per_s": world * R * args.steps / t_total,
+            "k1_ms_per_step": 1000.0 * t_k1 / args.steps,
+            "work_per_step_per_gpu": {"philox_blocks": blocks, "batches": int(stats["batches"]),
+                                      "member_steps": int(stats["member_steps"]),
+                                      "decode_steps": int(stats["decode_steps"])},
+            "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
+                         "frac": achieved_gops / peak_gops, "traffic": traffic,
+                         "kernel": "slo_sim_kernel (K1)",
+                         "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
+                                 "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)"},
+            "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e,
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, reps, reqs, dt = cpu_oracle_sample(cfg, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": v, "unit": "requests/s", "cores": cores, "kind": "oracle",
+                                    "sample": f"{reps} replicas ({reqs} requests) of {args.workload.upper()} in "
+                                              f"seed-major order, {dt:.1f} s on {cores} worker processes"}
+        print(json.dumps(line))
+    S.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -87,8 +87,7 @@ bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
 
 namespace slo {
 size_t warp_bytes_for(uint32_t cap) {
-  // WarpRing (64*8*2 + 64*4*2 + 16*4 + 16) followed by the candidate buffer
-  return 1536 + 64 + 16 + (size_t)cap * 4u;
+  return sizeof(WarpRing) + (size_t)cap * 4u;   // ring + p99 candidate buffer
 }
 }  // namespace slo
 

@@ -19,6 +19,20 @@ struct DevWorkload {      // device copy of one slo_workload
   uint32_t stream_id, pad;
 };
 
+// Per-warp shared-memory state of K1 (followed by the p99 candidate buffer of `cap` u32).
+struct WarpRing {
+  uint64_t a[64];      // arrival time of request j at a[j & 63]
+  uint64_t kap[64];    // kappa_k (k-th completion time, ascending) at kap[k & 63]
+  uint32_t po[64];     // P | (O << 16)
+  uint32_t w3[64];     // noise word of request j
+  uint32_t tm1[16];    // T_a - 1 for a = 1..gp (gp = #{a : T_a > 0})
+  uint8_t guide[256];  // A(u) at the top of bucket u >> 24 (a lower bound on the bucket)
+  uint8_t slot[32];    // spec decode: lane of the s-th unfinished member
+  uint64_t a_w;        // arrival time of the first measured request
+  uint64_t pad;
+};
+static_assert(sizeof(WarpRing) % 16 == 0, "WarpRing alignment");
+
 struct SimParams {
   const slo_knobs* cfg;
   const uint64_t* seeds;

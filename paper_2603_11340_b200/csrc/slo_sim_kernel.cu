@@ -15,16 +15,80 @@
 
 namespace slo {
 
-struct WarpRing {
-  uint64_t a[64];      // arrival time of request j at a[j & 63]
-  uint64_t kap[64];    // kappa_k (k-th completion time, ascending) at kap[k & 63]
-  uint32_t po[64];     // P | (O << 16)
-  uint32_t w3[64];     // noise word of request j
-  uint32_t tm1[16];    // T_a - 1 for a = 1..gp (gp = #{a : T_a > 0})
-  uint64_t a_w;        // arrival time of the first measured request
-  uint64_t pad;
-};
-static_assert(sizeof(WarpRing) == 1616, "WarpRing layout must match warp_bytes_for()");
+// A(u) = #{a in [1, gp] : u < T_a}: start from the bucket minimum guide[u >> 24]
+// (A is non-increasing in u) and count the remaining thresholds of that bucket (rarely more than 0).
+__device__ __forceinline__ uint32_t accepted(const WarpRing& R, uint32_t u, uint32_t gp) {
+  uint32_t A = R.guide[u >> 24];
+  while (A < gp && u <= R.tm1[A]) ++A;
+  return A;
+}
+
+// Lane-parallel step counts for a speculative batch: work items (member, Philox SPEC block q) are spread
+// over all 32 lanes, L = 2^floor(log2(32/u)) consecutive blocks per unfinished member per round; a
+// segmented scan of block token sums finds the crossing block, whose lane resolves the exact step.
+// Blocks past a member's crossing are computed speculatively and discarded (they are not part of the
+// definition's work count, which is ceil(S_m/4) blocks per member).
+__device__ __forceinline__ uint32_t spec_steps(WarpRing& R, uint32_t k0, uint32_t k1, uint32_t j, uint32_t O,
+                                               bool member, uint32_t gp, int lane, uint32_t lanemask_lt) {
+  uint32_t S = 0, cum = 0, q = 0;
+  bool pending = member;
+  uint32_t pend = __ballot_sync(FULL, pending);
+  while (pend) {
+    const uint32_t u = __popc(pend);
+    const int lg = 31 - __clz(32u / u);                  // L = 2^lg <= 32/u
+    const uint32_t L = 1u << lg;
+    const uint32_t myslot = __popc(pend & lanemask_lt);
+    if (pending) R.slot[myslot] = (uint8_t)lane;
+    __syncwarp();
+    const uint32_t slot = (uint32_t)lane >> lg, off = (uint32_t)lane & (L - 1u);
+    const bool active = slot < u;
+    const int src = active ? R.slot[slot] : 0;
+    const uint32_t mj = __shfl_sync(FULL, j, src);
+    const uint32_t mO = __shfl_sync(FULL, O, src);
+    const uint32_t mcum = __shfl_sync(FULL, cum, src);
+    const uint32_t mq = __shfl_sync(FULL, q, src);
+    uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+    if (active) {
+      const u32x4 w = philox(mj, 1, mq + off, 0, k0, k1);
+      e0 = accepted(R, w.x, gp) + 1;
+      e1 = accepted(R, w.y, gp) + 1;
+      e2 = accepted(R, w.z, gp) + 1;
+      e3 = accepted(R, w.w, gp) + 1;
+    }
+    const uint32_t T = e0 + e1 + e2 + e3;
+    uint32_t P = T;                                      // segmented inclusive scan over the L lanes
+    for (uint32_t d = 1; d < L; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(FULL, P, d);
+      if (off >= d) P += v;
+    }
+    const bool cross = active && (mcum + P >= mO);
+    const uint32_t cb = __ballot_sync(FULL, cross);
+    const uint32_t segmask = (L == 32u) ? FULL : (((1u << L) - 1u) << (slot * L));
+    uint32_t Sx = 0;
+    if (cross && (uint32_t)(__ffs(cb & segmask) - 1) == (uint32_t)lane) {
+      const uint32_t c = mcum + P - T;                   // tokens before this block
+      const uint32_t base = 4u * (mq + off);
+      Sx = c + e0 >= mO ? base + 1 : (c + e0 + e1 >= mO ? base + 2 : (c + e0 + e1 + e2 >= mO ? base + 3 : base + 4));
+    }
+    const uint32_t mymask = (L == 32u) ? FULL : (((1u << L) - 1u) << (myslot * L));
+    const uint32_t myfirst = cb & mymask;
+    const int from = myfirst ? __ffs(myfirst) - 1 : (int)(myslot * L + L - 1u);
+    const uint32_t gotS = __shfl_sync(FULL, Sx, from & 31);
+    const uint32_t gotP = __shfl_sync(FULL, P, from & 31);
+    if (pending) {
+      if (myfirst) {
+        S = gotS;
+        pending = false;
+      } else {
+        cum += gotP;
+        q += L;
+      }
+    }
+    pend = __ballot_sync(FULL, pending);
+  }
+  return S;
+}
+
 
 // K-th largest value of buf[0..n) (K >= 1, n >= K): MSB-first radix select by warp counting.
 __device__ __forceinline__ uint32_t kth_largest(const uint32_t* buf, uint32_t n, uint32_t K, int lane) {
@@ -105,6 +169,16 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32)
           if (lane == 0) R.tm1[a - 1] = (uint32_t)(prev - 1);
           gp = a;
         }
+      }
+      if (gamma > 0) {  // bucket guide for A(u)
+        __syncwarp();
+        for (uint32_t kk = lane; kk < 256; kk += 32) {
+          const uint32_t utop = (kk << 24) | 0xFFFFFFu;
+          uint32_t A = 0;
+          while (A < gp && utop <= R.tm1[A]) ++A;
+          R.guide[kk] = (uint8_t)A;
+        }
+        __syncwarp();
       }
     }
     // ---- step-cost coefficients: d(n) = alpha0 + alpha1 * n
@@ -230,30 +304,12 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32)
       const uint32_t maxP = __reduce_max_sync(FULL, po & 0xFFFFu);
       const uint64_t Dp = f * ((uint64_t)W.t.pre_base_us + (uint64_t)W.t.pre_tok_us * maxP) / 1000000u;
 
-      // ---- (a7) decode: per-member step counts S_m
+      // ---- (a7) decode: per-member step counts S_m = min{s : sum_{j<s} (A(u_{m,j}) + 1) >= O_m}
       uint32_t S = 0;
-      if (member) {
-        uint32_t rem = po >> 16;
-        if (gamma == 0) {
-          S = rem;
-        } else {
-          uint32_t q = 0;
-          while (rem > 0) {
-            const u32x4 w = philox(j, 1, q, 0, k0, k1);
-            const uint32_t us[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              if (rem > 0) {
-                uint32_t A = 0;
-                while (A < gp && us[t] <= R.tm1[A]) ++A;
-                const uint32_t e = A + 1 < rem ? A + 1 : rem;
-                rem -= e;
-                ++S;
-              }
-            }
-            ++q;
-          }
-        }
+      if (gamma == 0) {
+        S = member ? (po >> 16) : 0u;
+      } else {
+        S = spec_steps(R, k0, k1, j, po >> 16, member, gp, lane, lanemask_lt);
       }
       // Cum_m = alpha0 * S_m + alpha1 * sum_m' min(S_m', S_m); rank_m = position in completion order
       uint32_t summin = 0, rank = 0, maxS = 0;
