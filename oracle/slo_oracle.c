@@ -150,6 +150,12 @@ static uint64_t scaled_gap(uint64_t mean_gap_q16, uint32_t rate_scale_q8) {
   return (uint64_t)(((u128)mean_gap_q16 * 256u) / rate_scale_q8);
 }
 
+/* operational capacity of a phase: U = min(2^62, floor(D * rho / 2^16)) */
+static uint64_t capacity(uint64_t D, uint64_t rho) {
+  u128 x = ((u128)D * (u128)rho) >> 16;
+  return x > ((u128)1 << 62) ? (1ull << 62) : (uint64_t)x;
+}
+
 /* ---------------------------------------------------------------------------------------------- */
 /* request draws a_i, P_i, O_i, w3_i                                         */
 /* ---------------------------------------------------------------------------------------------- */
@@ -161,6 +167,8 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
   uint64_t g[2] = {scaled_gap(W->arr.mean_gap_q16[0], k->rate_scale_q8),
                    scaled_gap(W->arr.mean_gap_q16[1], k->rate_scale_q8)};
   uint32_t kind = W->arr.kind;
+  /* per-state rate rho_s = floor((2^64 - 1) / g_s), 0 for a state without arrivals */
+  uint64_t rho[2] = {g[0] == U64MAX ? 0 : U64MAX / g[0], g[1] == U64MAX ? 0 : U64MAX / g[1]};
 
   /* bursty phase state (kinds 1, 2) */
   uint32_t p = 0;
@@ -174,7 +182,7 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
     } else {
       D = W->arr.mean_sojourn_us[state];
     }
-    U = (g[state] == U64MAX) ? 0 : (uint64_t)((((u128)D) << 48) / g[state]);
+    U = capacity(D, rho[state]);
   }
 
   uint64_t prev = 0;
@@ -200,7 +208,7 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
         } else {
           D = W->arr.mean_sojourn_us[state];
         }
-        U = (g[state] == U64MAX) ? 0 : (uint64_t)((((u128)D) << 48) / g[state]);
+        U = capacity(D, rho[state]);
       }
       uint64_t off = (uint64_t)(((u128)(tau - Lambda) * g[state]) >> 48);
       if (off > D - 1) off = D - 1;
