@@ -157,6 +157,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--warps-per-block", type=int, default=0, help="launch shape override (0 = library default)")
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -207,7 +209,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    S = sim.Simulator(cfg.workloads, device=local)
+    S = sim.Simulator(cfg.workloads, device=local, warps_per_block=args.warps_per_block,
+                      blocks_per_sm=args.blocks_per_sm)
     info = S.info()
 
     # weak scaling: every rank runs the full grid on its own seed block

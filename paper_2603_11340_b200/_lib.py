@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libslosim.so")
+LIB_PATH = os.environ.get("SLO_SIM_LIB") or os.path.join(HERE, "libslosim.so")   # env: experiment builds (in-tree)
 
 SLO_OK = 0
 STATUS = {0: "ok", -1: "SLO_E_INVAL", -2: "SLO_E_NOMEM", -3: "SLO_E_CUDA", -4: "SLO_E_RANGE",

@@ -73,7 +73,8 @@ uint32_t topk_for(uint32_t n) {  // K = n - r + 1 with r = ceil(0.99 n) (DESIGN.
   return (uint32_t)(n - r + 1);
 }
 
-uint32_t cap_for(uint32_t K) { return ((2u * K + 64u + 31u) / 32u) * 32u; }
+// candidate buffer: room for 3K + 32 insertions between shrinks (shrink cost ~ cap, frequency ~ 1/(cap - K))
+uint32_t cap_for(uint32_t K) { return ((4u * K + 64u + 31u) / 32u) * 32u; }
 
 bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
   if (lo < 1 || (uint64_t)lo + ncw > SLO_MAX_LENGTH) return false;

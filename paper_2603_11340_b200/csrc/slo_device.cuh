@@ -65,6 +65,15 @@ __device__ __forceinline__ uint64_t mulshr(uint64_t a, uint64_t b, int s) {
   return (lo >> s) | (hi << (64 - s));
 }
 
+// operational capacity of a bursty phase: min(2^62, floor(D * rho / 2^16))
+__device__ __forceinline__ uint64_t capacity(uint64_t D, uint64_t rho) {
+  const uint64_t lo = D * rho;
+  const uint64_t hi = __umul64hi(D, rho);
+  if (hi >= (1ull << 14)) return 1ull << 62;
+  const uint64_t x = (lo >> 16) | (hi << 48);
+  return x > (1ull << 62) ? (1ull << 62) : x;
+}
+
 // ---- lengths: lo + #{l : cw[l] <= u}, by binary search over the cut points.
 __device__ __forceinline__ uint32_t length_of(const uint32_t* __restrict__ cw, uint32_t ncw, uint32_t lo,
                                               uint32_t u) {

@@ -19,17 +19,27 @@ struct DevWorkload {      // device copy of one slo_workload
   uint32_t stream_id, pad;
 };
 
-// Per-warp shared-memory state of K1 (followed by the p99 candidate buffer of `cap` u32).
+// Per-warp shared-memory state of K1 (followed by the p99 candidate buffer of `cap` u32).  Warp-uniform
+// values that are touched rarely live here instead of in registers (K1 is register-bound).
 struct WarpRing {
   uint64_t a[64];      // arrival time of request j at a[j & 63]
   uint64_t kap[64];    // kappa_k (k-th completion time, ascending) at kap[k & 63]
   uint32_t po[64];     // P | (O << 16)
   uint32_t w3[64];     // noise word of request j
+  uint32_t hist[256];  // radix-select histogram
   uint32_t tm1[16];    // T_a - 1 for a = 1..gp (gp = #{a : T_a > 0})
-  uint8_t guide[256];  // A(u) at the top of bucket u >> 24 (a lower bound on the bucket)
+  uint8_t guide[256];  // A(u) at the top of bucket u >> 24 | 0x80 if a threshold lies inside the bucket
   uint8_t slot[32];    // spec decode: lane of the s-th unfinished member
+  // arrival-process state (touched once per 32 generated requests)
+  uint64_t g[2];       // scaled mean gaps (Q48.16)
+  uint64_t rho[2];     // floor((2^64 - 1) / g), 0 without arrivals
+  uint64_t last;       // a of the last generated request (kind 0) or its tau (kinds 1, 2)
+  uint64_t pstart, pD, pU, pLam;
+  uint32_t ph, pstate;
+  uint64_t nphase;     // PHASE blocks drawn
   uint64_t a_w;        // arrival time of the first measured request
-  uint64_t pad;
+  uint64_t alpha0, alpha1;
+  uint32_t pre_base, pre_tok, noise, pad;
 };
 static_assert(sizeof(WarpRing) % 16 == 0, "WarpRing alignment");
 
