@@ -27,7 +27,15 @@ struct slo_sim {
   uint32_t crn = 1;
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
-  uint32_t* d_queue = nullptr;      // replica queue counter (one per launch, reset by memset)
+  uint32_t* d_ctl = nullptr;        // [8]: K0 list counts [3], K1 list cursors [3]
+  // run scratch (grow-only): work lists, latency rows, per-replica partial results
+  uint32_t* d_lists = nullptr;
+  size_t lists_cap = 0;
+  uint32_t* d_lat = nullptr;
+  size_t lat_cap = 0;
+  slo_replica_result* d_part = nullptr;
+  size_t part_cap = 0;
+  size_t lat_budget = (size_t)4 << 30;  // bytes of latency rows per launch chunk
   // host-entry scratch
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -68,14 +76,6 @@ struct DeviceGuard {
   }
 };
 
-uint32_t topk_for(uint32_t n) {  // K = n - r + 1 with r = ceil(0.99 n)
-  const uint64_t r = (99ull * n + 99ull) / 100ull;
-  return (uint32_t)(n - r + 1);
-}
-
-// candidate buffer: room for 3K + 32 insertions between shrinks (shrink cost ~ cap, frequency ~ 1/(cap - K))
-uint32_t cap_for(uint32_t K) { return ((4u * K + 64u + 31u) / 32u) * 32u; }
-
 bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
   if (lo < 1 || (uint64_t)lo + ncw > SLO_MAX_LENGTH) return false;
   if (ncw > 0 && cw == nullptr) return false;
@@ -86,11 +86,18 @@ bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
 
 }  // namespace
 
-namespace slo {
-size_t warp_bytes_for(uint32_t cap) {
-  return sizeof(WarpRing) + (size_t)cap * 4u;   // ring + p99 candidate buffer
+// grow-only device scratch owned by the handle (callers synchronise before a regrow)
+template <typename T>
+slo_status ensure(slo_sim* h, T*& ptr, size_t& cap, size_t need, cudaStream_t st) {
+  if (need <= cap) return SLO_OK;
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  if (cudaMalloc(&ptr, need * sizeof(T)) != cudaSuccess) return fail(h, SLO_E_NOMEM, "scratch of %zu B", need * sizeof(T));
+  cap = need;
+  return SLO_OK;
 }
-}  // namespace slo
 
 extern "C" {
 
@@ -192,7 +199,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
-      (e = cudaMalloc(&h->d_queue, sizeof(uint32_t) * 4)) != cudaSuccess) {
+      (e = cudaMalloc(&h->d_ctl, sizeof(uint32_t) * 8)) != cudaSuccess) {
     slo_sim_destroy(h);
     return fail(nullptr, SLO_E_NOMEM, "create: cudaMalloc: %s", cudaGetErrorString(e));
   }
@@ -213,7 +220,10 @@ slo_status slo_sim_destroy(slo_sim* h) {
     cudaDeviceSynchronize();
     if (h->d_wl) cudaFree(h->d_wl);
     if (h->d_tables) cudaFree(h->d_tables);
-    if (h->d_queue) cudaFree(h->d_queue);
+    if (h->d_ctl) cudaFree(h->d_ctl);
+    if (h->d_lists) cudaFree(h->d_lists);
+    if (h->d_lat) cudaFree(h->d_lat);
+    if (h->d_part) cudaFree(h->d_part);
     if (h->d_scratch) cudaFree(h->d_scratch);
   }
   delete h;
@@ -234,7 +244,7 @@ slo_status slo_sim_get_info(const slo_sim* hc, slo_sim_info* info) {
   if (!hc || !info) return fail(nullptr, SLO_E_INVAL, "get_info: null");
   slo_sim* h = const_cast<slo_sim*>(hc);
   DeviceGuard g(h->device);
-  const size_t wb = slo::warp_bytes_for(cap_for(topk_for(10000)));
+  const size_t wb = slo::group_warp_bytes();
   memset(info, 0, sizeof *info);
   info->device = h->device;
   info->sm_count = h->sm_count;
@@ -249,42 +259,67 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                              uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
                              uint32_t* d_p99, double* d_goodput, slo_replica_result* d_detail, uint32_t* d_lat,
                              slo_stats* d_stats, cudaStream_t st) {
-  const uint64_t n_rep = (uint64_t)n_configs * n_seeds;
+  const uint32_t n_rep = (uint32_t)((uint64_t)n_configs * n_seeds);
+  const uint32_t N = warmup_len + segment_len;
+  // replicas per launch chunk: the latency rows of a chunk stay within the budget (unless the caller
+  // provides the full latency buffer, which is then written in place)
+  uint64_t chunk = d_lat ? n_rep : h->lat_budget / ((uint64_t)N * 4u);
+  if (chunk < 1) chunk = 1;
+  if (chunk > n_rep) chunk = n_rep;
+  slo_status s;
+  if ((s = ensure(h, h->d_lists, h->lists_cap, (size_t)3 * chunk, st)) != SLO_OK) return s;
+  if (!d_lat && (s = ensure(h, h->d_lat, h->lat_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
+  if (!d_detail && (s = ensure(h, h->d_part, h->part_cap, (size_t)n_rep, st)) != SLO_OK) return s;
+
   slo::SimParams p{};
   p.cfg = d_configs;
   p.seeds = d_seeds;
   p.wl = h->d_wl;
   p.tables = h->d_tables;
-  p.queue = h->d_queue;
+  p.counts = h->d_ctl;
+  p.cursor = h->d_ctl + 3;
+  p.lists = h->d_lists;
+  p.part = d_detail ? d_detail : h->d_part;
   p.p99 = d_p99;
   p.goodput = d_goodput;
   p.detail = d_detail;
-  p.lat = d_lat;
   p.stats = d_stats;
   p.n_cfg = n_configs;
   p.n_seeds = n_seeds;
-  p.n_rep = (uint32_t)n_rep;
+  p.n_rep = n_rep;
   p.n_wl = h->n_wl;
   p.warmup = warmup_len;
   p.seg = segment_len;
   p.slo_us = slo_us;
   p.crn = h->crn;
-  p.topk = topk_for(segment_len);
-  p.cap = cap_for(p.topk);
-  p.warp_bytes = (uint32_t)slo::warp_bytes_for(p.cap);
+  p.warp_bytes = (uint32_t)slo::group_warp_bytes();
   const size_t smem = (size_t)p.warp_bytes * h->warps_per_block;
-  if (smem > 227 * 1024) return fail(h, SLO_E_RANGE, "run_batch: segment_len %u needs %zu B of shared memory", segment_len, smem);
   if (smem > 48 * 1024)
     CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int bps = blocks_per_sm_for(h, smem);
-  uint64_t blocks = (uint64_t)bps * h->sm_count;
-  const uint64_t need = (n_rep + h->warps_per_block - 1) / h->warps_per_block;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  CUDA_TRY(h, cudaMemsetAsync(h->d_queue, 0, sizeof(uint32_t), st));
+  const uint32_t sel_vals = segment_len <= 11008u ? segment_len : 0u;   // stage rows up to 43 KB in smem
+  const size_t sel_smem = (256u + sel_vals) * sizeof(uint32_t);
   if (d_stats) CUDA_TRY(h, cudaMemsetAsync(d_stats, 0, sizeof(slo_stats), st));
-  slo::slo_sim_kernel<<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
-  CUDA_TRY(h, cudaGetLastError());
+  for (uint64_t r0 = 0; r0 < n_rep; r0 += chunk) {
+    const uint32_t nc = (uint32_t)((n_rep - r0) < chunk ? (n_rep - r0) : chunk);
+    p.r_base = (uint32_t)r0;
+    p.n_chunk = nc;
+    p.lists = h->d_lists;
+    p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
+    CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * 8, st));
+    slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, n_seeds, (uint32_t)r0, nc, h->n_wl, h->d_ctl,
+                                                              h->d_lists);
+    CUDA_TRY(h, cudaGetLastError());
+    uint64_t blocks = (uint64_t)bps * h->sm_count;
+    const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    slo::slo_sim_kernel<<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+    CUDA_TRY(h, cudaGetLastError());
+    const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
+    slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
+    CUDA_TRY(h, cudaGetLastError());
+  }
   return SLO_OK;
 }
 

@@ -1,13 +1,20 @@
-// slo_sim_kernel.cu — K1: one simulator replica per warp.
+// slo_sim_kernel.cu — the simulation kernels of libslosim.
 //
-// Persistent grid; each warp pulls replica indices from a device atomic queue and runs the replica's
-// whole segment. Per-warp shared memory (WarpRing) holds 64-entry rings of arrival times a_j and sorted
-// completion times kappa_k, packed (P, O) lengths and noise words, the acceptance thresholds, the rarely
-// touched warp-uniform state and the p99 candidate buffer. The event loop is replaced by the closed forms
-// of DESIGN.md §2.6 (equal to the event definition; checked bit-exactly against the oracle):
+//  K0 slo_classify_kernel : sorts replicas into three work lists by the lane-group size G in {8, 16, 32}
+//                           that fits their client window (G >= max(C, B)).
+//  K1 slo_sim_kernel      : persistent; a warp runs 32/G replicas at once, one per G-lane group, with every
+//                           collective (ballot, shuffle, scan, sort) scoped to the group. Per-group shared
+//                           memory holds rings of arrival times a_j and sorted completion times kappa_k,
+//                           packed (P, O), noise words, acceptance thresholds and the warp-uniform
+//                           arrival-process state. Every request's latency goes to an HBM scratch row.
+//  K1b slo_select_kernel  : per replica, stages the measured latencies in shared memory and takes the
+//                           exact nearest-rank p99 by an 8-bit radix select; writes p99 and goodput.
+//
+// The event loop is replaced by the closed forms of DESIGN.md §2.6 (equal to the event definition;
+// checked bit-exactly against the oracle):
 //   s_j = max(a_j, kappa_{j-C});  t_form = max(t_idle, s_h[, min(s_h + max_wait, s_{h+B-1})]);
-//   b = min(B, #{j in [h, h+C) : s_j <= t_form}) via ballot + popc;
-//   Cum_m = alpha0 * S_m + alpha1 * sum_{m'} min(S_m', S_m); completion order = order of S_m.
+//   b = min(B, #{j in [h, h+C) : s_j <= t_form});
+//   Cum_m = alpha0 S_m + alpha1 sum_{m'} min(S_m', S_m); completion order = order of S_m.
 #include <cstdint>
 
 #include "slo_device.cuh"
@@ -15,10 +22,82 @@
 
 namespace slo {
 
-// A(u) = #{a in [1, gp] : u < T_a}. guide[u >> 24] holds A at the top of u's bucket
-// (A is non-increasing in u, so this is the bucket minimum) and bit 7 when a threshold lies strictly
-// inside the bucket; only then are the remaining thresholds counted.
-__device__ __forceinline__ uint32_t accepted(const WarpRing& R, uint32_t u, uint32_t gp) {
+// ------------------------------------------------------------------------------------------------
+// group-scoped collectives (all 32 lanes execute them; each G-lane group is independent)
+// ------------------------------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ uint32_t gballot(bool pred, int lane) {
+  const uint32_t m = __ballot_sync(FULL, pred);
+  if constexpr (G == 32) {
+    return m;
+  } else {
+    return (m >> (lane & ~(G - 1))) & ((1u << G) - 1u);
+  }
+}
+template <int G>
+__device__ __forceinline__ uint32_t gshfl(uint32_t v, int src) {
+  return __shfl_sync(FULL, v, src, G);
+}
+template <int G>
+__device__ __forceinline__ uint64_t gshfl64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(FULL, (uint32_t)v, src, G);
+  const uint32_t hi = __shfl_sync(FULL, (uint32_t)(v >> 32), src, G);
+  return ((uint64_t)hi << 32) | lo;
+}
+template <int G>
+__device__ __forceinline__ uint64_t gscan64(uint64_t v, int li) {  // inclusive prefix sum
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+    const uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, d, G);
+    const uint32_t hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), d, G);
+    if (li >= d) v += ((uint64_t)hi << 32) | lo;
+  }
+  return v;
+}
+template <int G>
+__device__ __forceinline__ uint32_t gmax(uint32_t v) {
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) v = max(v, __shfl_xor_sync(FULL, v, m, G));
+  return v;
+}
+template <int G>
+__device__ __forceinline__ uint32_t gsum(uint32_t v) {
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) v += __shfl_xor_sync(FULL, v, m, G);
+  return v;
+}
+template <int G>
+__device__ __forceinline__ uint64_t gsum64(uint64_t v) {
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) {
+    const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m, G);
+    const uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), m, G);
+    v += ((uint64_t)hi << 32) | lo;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------------------------------------
+// per-replica shared-memory state of one G-lane group
+// ------------------------------------------------------------------------------------------------
+template <int G>
+struct alignas(16) Group {
+  static constexpr int RING = 4 * G;  // holds [h - C, gen) with gen <= h + 3G
+  uint64_t a[RING];                   // arrival time of request j at a[j % RING]
+  uint64_t kap[RING];                 // kappa_k (k-th completion, ascending) at kap[k % RING]
+  uint32_t po[RING];                  // P | (O << 16)
+  uint32_t w3[RING];                  // noise word
+  uint32_t tm1[16];                   // T_a - 1, a = 1..gp
+  uint8_t guide[256];                 // A at the top of bucket u >> 24, | 0x80 if a threshold is inside
+  uint64_t g[2], rho[2];              // scaled mean gaps, floor((2^64-1)/g)
+  uint64_t last;                      // last generated a (kind 0) or tau (kinds 1, 2)
+  uint64_t pstart, pD, pU, pLam, nphase, a_w, alpha0, alpha1;
+  uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, pad;
+};
+
+// A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
+template <int G>
+__device__ __forceinline__ uint32_t accepted(const Group<G>& R, uint32_t u, uint32_t gp) {
   const uint32_t g = R.guide[u >> 24];
   uint32_t A = g & 0x7Fu;
   if (g & 0x80u) {
@@ -27,24 +106,25 @@ __device__ __forceinline__ uint32_t accepted(const WarpRing& R, uint32_t u, uint
   return A;
 }
 
-// Lane-parallel step counts of a speculative batch of b members: member m owns the L = 32 / 2^ceil(log2 b)
-// lanes [m L, (m+1) L); each round every lane of an unfinished member computes one Philox SPEC block
-// (4 decode steps), a segmented scan of the block token sums finds the block where the member's cumulative
-// tokens reach O_m, and that lane resolves the exact step.  Blocks past the crossing are computed
-// speculatively and discarded (the definition's work is ceil(S_m/4) blocks per member).  Returns S_m in
-// lane m (m < b).
-__device__ __forceinline__ uint32_t spec_steps(const WarpRing& R, uint32_t k0, uint32_t k1, uint32_t h,
-                                               uint32_t b, uint32_t gp, int lane) {
-  const int lgb = 32 - __clz(b - 1u);                  // ceil(log2 b)
-  const int lg = 5 - lgb;                              // log2 L
+// Lane-parallel step counts of a speculative batch of b members in a G-lane group: member m owns the
+// L = G / 2^ceil(log2 b) lanes [m L, (m+1) L); each round every lane of an unfinished member computes one
+// Philox SPEC block (4 decode steps), a segmented scan of block token sums finds the block where the
+// member's cumulative tokens reach O_m, and that lane resolves the exact step.  Blocks
+// past the crossing are computed speculatively and discarded.  Returns S_m in group lane m (m < b).
+template <int G>
+__device__ __forceinline__ uint32_t spec_steps(const Group<G>& R, uint32_t k0, uint32_t k1, uint32_t h, uint32_t b,
+                                               uint32_t gp, bool run, int lane, int li) {
+  constexpr int LOGG = G == 8 ? 3 : (G == 16 ? 4 : 5);
+  const uint32_t bb = b > 0 ? b : 1u;
+  const int lg = LOGG - (32 - __clz(bb - 1u));      // log2 L
   const uint32_t L = 1u << lg;
-  const uint32_t m = (uint32_t)lane >> lg, off = (uint32_t)lane & (L - 1u);
+  const uint32_t m = (uint32_t)li >> lg, off = (uint32_t)li & (L - 1u);
   const uint32_t segbase = m << lg;
   const uint32_t j = h + m;
-  const uint32_t O = m < b ? (R.po[j & 63] >> 16) : 0u;
-  const uint32_t lowmask = (L == 32u) ? FULL : ((1u << L) - 1u);
+  const uint32_t O = (run && m < b) ? (R.po[j % Group<G>::RING] >> 16) : 0u;
+  const uint32_t lowmask = (L >= 32u) ? FULL : ((1u << L) - 1u);
   uint32_t cum = 0, q = off, S = 0;
-  bool pending = m < b;
+  bool pending = run && m < b;
   while (__any_sync(FULL, pending)) {
     uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
     if (pending) {
@@ -55,21 +135,22 @@ __device__ __forceinline__ uint32_t spec_steps(const WarpRing& R, uint32_t k0, u
       e3 = accepted(R, w.w, gp) + 1;
     }
     const uint32_t T = e0 + e1 + e2 + e3;
-    uint32_t P = T;                                    // segmented inclusive scan over the L lanes
-    for (int d = 1; d < (int)L; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(FULL, P, d);
-      if ((int)off >= d) P += v;
+    uint32_t P = T;  // segmented inclusive scan over the L lanes
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(FULL, P, d, G);
+      if ((uint32_t)d < L && (int)off >= d) P += v;
     }
     const bool cross = pending && (cum + P >= O);
-    const uint32_t segbits = (__ballot_sync(FULL, cross) >> segbase) & lowmask;
-    const uint32_t first = __ffs(segbits) - 1u;        // crossing lane within the segment (if any)
+    const uint32_t segbits = (gballot<G>(cross, lane) >> segbase) & lowmask;
+    const uint32_t first = __ffs(segbits) - 1u;
     uint32_t give = P;
-    if (segbits && off == first) {                     // this lane resolves the exact step
+    if (segbits && off == first) {
       const uint32_t c = cum + P - T;
       const uint32_t base = 4u * q;
       give = c + e0 >= O ? base + 1 : (c + e0 + e1 >= O ? base + 2 : (c + e0 + e1 + e2 >= O ? base + 3 : base + 4));
     }
-    const uint32_t got = __shfl_sync(FULL, give, (int)(segbits ? segbase + first : segbase + L - 1u));
+    const uint32_t got = gshfl<G>(give, (int)(segbits ? segbase + first : segbase + L - 1u));
     if (pending) {
       if (segbits) {
         S = got;
@@ -80,134 +161,344 @@ __device__ __forceinline__ uint32_t spec_steps(const WarpRing& R, uint32_t k0, u
       }
     }
   }
-  return __shfl_sync(FULL, S, (lane << lg) & 31);
+  return gshfl<G>(S, (li << lg) & (G - 1));
 }
 
-// K-th largest value of buf[0..n) (1 <= K <= n): exact radix select, four 8-bit digits MSB first, with a
-// per-warp shared-memory histogram.
-__device__ __noinline__ uint32_t kth_largest(const uint32_t* buf, uint32_t n, uint32_t K, uint32_t* hist,
-                                             int lane) {
-  uint32_t prefix = 0, kk = K;
-#pragma unroll 1
-  for (int shift = 24; shift >= 0; shift -= 8) {
-#pragma unroll
-    for (int t = 0; t < 8; ++t) hist[lane * 8 + t] = 0;
-    __syncwarp();
-    const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-    for (uint32_t e = lane; e < n; e += 32) {
-      const uint32_t v = buf[e];
-      if ((v & hmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
-    }
-    __syncwarp();
-    uint32_t c[8], sum = 0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      c[t] = hist[lane * 8 + t];
-      sum += c[t];
-    }
-    uint32_t incl = sum;                                 // suffix sum over lanes (bins >= 8 * lane)
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_down_sync(FULL, incl, d);
-      if (lane + d < 32) incl += v;
-    }
-    const bool here = incl >= kk && incl - sum < kk;
-    const int owner = __ffs(__ballot_sync(FULL, here)) - 1;
-    uint32_t digit = 0, knew = 0;
-    if (lane == owner) {
-      uint32_t above = incl - sum;
-#pragma unroll
-      for (int t = 7; t >= 0; --t) {
-        if (knew == 0 && above + c[t] >= kk) {
-          digit = 8u * lane + t;
-          knew = kk - above;
-        }
-        above += c[t];
+// (a1) set up a newly acquired replica (group-convergent; other groups do not enter)
+template <int G>
+__device__ __forceinline__ void setup_replica(Group<G>& R, const DevWorkload& W, const slo_knobs& k, uint32_t k0,
+                                              uint32_t k1, uint32_t gamma, uint32_t& gp, int li, uint32_t gmask) {
+  gp = 0;
+  {
+    uint64_t rr = 65536;
+    for (uint32_t w = 0; w < k.draft_width; ++w) rr = (rr * (65536u - k.accept_q16)) >> 16;
+    const uint64_t ae = 65536u - rr;
+    uint64_t prev = 1ull << 32;
+    for (uint32_t a = 1; a <= gamma; ++a) {
+      prev = (prev * ae) >> 16;
+      if (prev > 0) {
+        if (li == 0) R.tm1[a - 1] = (uint32_t)(prev - 1);
+        gp = a;
       }
     }
-    digit = __shfl_sync(FULL, digit, owner);
-    kk = __shfl_sync(FULL, knew, owner);
-    prefix |= digit << shift;
-    __syncwarp();
   }
-  return prefix;
+  if (li == 0) {
+    const uint64_t g0 = W.gap_q16[0] == INF64 ? INF64 : (W.gap_q16[0] << 8) / k.rate_scale_q8;
+    const uint64_t g1 = W.gap_q16[1] == INF64 ? INF64 : (W.gap_q16[1] << 8) / k.rate_scale_q8;
+    R.g[0] = g0;
+    R.g[1] = g1;
+    R.rho[0] = g0 == INF64 ? 0 : INF64 / g0;
+    R.rho[1] = g1 == INF64 ? 0 : INF64 / g1;
+    R.last = 0;
+    R.nphase = 0;
+    R.kind = W.kind;
+    R.start_state = W.start_state;
+    R.alpha0 = gamma == 0 ? (uint64_t)W.t.dec_base_us : (uint64_t)gamma * W.t.dr_base_us + W.t.ver_base_us;
+    R.alpha1 = gamma == 0 ? (uint64_t)W.t.dec_seq_us
+                          : (uint64_t)gamma * W.t.dr_seq_us + W.t.ver_seq_us + (uint64_t)W.t.ver_tok_us * (gamma + 1);
+    R.pre_base = W.t.pre_base_us;
+    R.pre_tok = W.t.pre_tok_us;
+    R.noise = W.t.noise_step_ppm;
+    if (W.kind != 0) {
+      const uint32_t st = W.start_state & 1u;
+      uint64_t D;
+      if (W.kind == 1) {
+        const u32x4 w = philox(0, 2, 0, 0, k0, k1);
+        D = mulshr(exp_q32(w.x), W.soj[st], 32);
+        R.nphase = 1;
+      } else {
+        D = W.soj[st];
+      }
+      R.pD = D;
+      R.pU = capacity(D, R.rho[st]);
+      R.pLam = 0;
+      R.pstart = 0;
+      R.ph = 0;
+      R.pstate = st;
+    }
+  }
+  __syncwarp(gmask);
+  if (gamma > 0) {  // bucket guide for A(u)
+    for (uint32_t kk = li; kk < 256; kk += G) {
+      const uint32_t lo = kk << 24, top = lo | 0xFFFFFFu;
+      uint32_t A = 0, inside = 0;
+      for (uint32_t a = 0; a < gp; ++a) {
+        const uint32_t t = R.tm1[a];
+        A += (top <= t);
+        inside |= (t >= lo && t < top);
+      }
+      R.guide[kk] = (uint8_t)(A | (inside << 7));
+    }
+  }
+  __syncwarp(gmask);
 }
 
-// keep only values > theta (in place)
-__device__ __noinline__ uint32_t compact_above(uint32_t* buf, uint32_t n, uint32_t theta, int lane) {
-  uint32_t out = 0;
-  for (uint32_t base = 0; base < n; base += 32) {
-    const uint32_t e = base + lane;
-    const uint32_t v = e < n ? buf[e] : 0;
-    const bool keep = e < n && v > theta;
-    const uint32_t m = __ballot_sync(FULL, keep);
-    __syncwarp();
-    if (keep) buf[out + __popc(m & ((1u << lane) - 1u))] = v;
-    out += __popc(m);
-    __syncwarp();
-  }
-  return out;
-}
-
-// (a2, a3) generate requests [gen, gen + 32): Philox REQ blocks, exponential gaps (warp scan), bursty
-// time change, lengths; written to the rings.  Warp-uniform process state lives in R.
-__device__ __noinline__ void generate_chunk(WarpRing& R, const DevWorkload& W, const uint32_t* __restrict__ tables,
-                                            uint32_t k0, uint32_t k1, uint32_t gen, uint32_t N, uint32_t warmup,
-                                            int lane) {
-  const uint32_t i = gen + (uint32_t)lane;
-  const bool valid = i < N;
+// (a2, a3) generate requests [gen, gen + G) for every group with `go` (all lanes execute)
+template <int G>
+__device__ __forceinline__ void generate(Group<G>& R, const DevWorkload* __restrict__ wls, uint32_t wl,
+                                         const uint32_t* __restrict__ tables, uint32_t k0, uint32_t k1, uint32_t gen,
+                                         uint32_t N, uint32_t warmup, bool go, int lane, int li) {
+  const uint32_t i = gen + (uint32_t)li;
+  const bool valid = go && i < N;
   const u32x4 w = philox(i, 0, 0, 0, k0, k1);
   const uint64_t E = valid ? exp_q32(w.x) : 0;
-  uint64_t a = 0;
-  if (W.kind == 0) {
-    const uint64_t gap = mulshr(E, R.g[0], 48);
-    a = R.last + warp_incl_scan64(gap, lane);
-    const uint64_t last = shfl64(a, 31);
-    __syncwarp();
-    if (lane == 0) R.last = last;
-  } else {
-    const uint64_t tau = R.last + warp_incl_scan64(E, lane);
-    const uint64_t last = shfl64(tau, 31);
-    uint64_t pLam = R.pLam, pU = R.pU, pD = R.pD, pstart = R.pstart, nph = R.nphase;
-    uint32_t ph = R.ph, pstate = R.pstate;
-    bool done = !valid;
+  const uint32_t kind = go ? R.kind : 0u;
+  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : E;
+  const uint64_t last = go ? R.last : 0ull;
+  const uint64_t sc = last + gscan64<G>(x, li);     // kind 0: a_i; kinds 1, 2: tau_i
+  const uint64_t newlast = gshfl64<G>(sc, G - 1);
+  uint64_t a = sc;
+  if (__any_sync(FULL, go && kind != 0)) {          // bursty: Cox time change, phases advance in order
+    const bool bursty = go && kind != 0;
+    uint64_t pLam = 0, pU = 0, pD = 0, pstart = 0, nph = 0;
+    uint32_t ph = 0, pstate = 0;
+    if (bursty) {
+      pLam = R.pLam; pU = R.pU; pD = R.pD; pstart = R.pstart; nph = R.nphase; ph = R.ph; pstate = R.pstate;
+    }
+    bool done = !(bursty && i < N);
     for (;;) {
-      const bool here = !done && tau < pLam + pU;
-      if (here) {
-        uint64_t off = mulshr(tau - pLam, R.g[pstate], 48);
+      if (!done && sc < pLam + pU) {
+        uint64_t off = mulshr(sc - pLam, R.g[pstate], 48);
         if (off > pD - 1) off = pD - 1;
         a = pstart + off;
         done = true;
       }
-      if (__all_sync(FULL, done)) break;
-      pLam += pU;
-      pstart += pD;
-      ++ph;
-      pstate = (W.start_state + ph) & 1u;
-      if (W.kind == 1) {
-        const u32x4 pw = philox(ph, 2, 0, 0, k0, k1);
-        pD = mulshr(exp_q32(pw.x), W.soj[pstate], 32);
-        ++nph;
-      } else {
-        pD = W.soj[pstate];
+      const bool grp_open = gballot<G>(!done, lane) != 0;
+      if (!__any_sync(FULL, grp_open)) break;
+      if (grp_open) {
+        pLam += pU;
+        pstart += pD;
+        ++ph;
+        pstate = (R.start_state + ph) & 1u;
+        if (R.kind == 1) {
+          const u32x4 pw = philox(ph, 2, 0, 0, k0, k1);
+          pD = mulshr(exp_q32(pw.x), wls[wl].soj[pstate], 32);
+          ++nph;
+        } else {
+          pD = wls[wl].soj[pstate];
+        }
+        pU = capacity(pD, R.rho[pstate]);
       }
-      pU = capacity(pD, R.rho[pstate]);
     }
-    __syncwarp();
-    if (lane == 0) {
-      R.last = last;
+    if (bursty && li == 0) {
       R.pLam = pLam; R.pU = pU; R.pD = pD; R.pstart = pstart; R.ph = ph; R.pstate = pstate; R.nphase = nph;
     }
   }
+  if (go && li == 0) R.last = newlast;
   if (valid) {
+    const DevWorkload& W = wls[wl];
     const uint32_t P = length_of(tables + W.p_off, W.p_ncw, W.p_lo, w.y);
     const uint32_t O = length_of(tables + W.o_off, W.o_ncw, W.o_lo, w.z);
-    R.a[i & 63] = a;
-    R.po[i & 63] = P | (O << 16);
-    R.w3[i & 63] = w.w;
+    R.a[i % Group<G>::RING] = a;
+    R.po[i % Group<G>::RING] = P | (O << 16);
+    R.w3[i % Group<G>::RING] = w.w;
     if (i == warmup) R.a_w = a;
   }
   __syncwarp();
+}
+
+// bitonic sort of u32 keys over the G lanes of each group (ascending)
+template <int G>
+__device__ __forceinline__ uint32_t gsort(uint32_t key, int li) {
+#pragma unroll
+  for (int kk = 2; kk <= G; kk <<= 1) {
+#pragma unroll
+    for (int jj = kk >> 1; jj >= 1; jj >>= 1) {
+      const uint32_t other = __shfl_xor_sync(FULL, key, jj, G);
+      const bool up = (li & kk) == 0;
+      const bool lower = (li & jj) == 0;
+      key = (lower == up) ? min(key, other) : max(key, other);
+    }
+  }
+  return key;
+}
+
+struct Counters {   // lane-local work counters (flushed to slo_stats)
+  uint32_t steps, blocks, batches, dsteps;
+};
+
+__device__ __forceinline__ void flush_counters(const SimParams& p, Counters& ct) {
+  if (p.stats) {
+    unsigned long long* st = (unsigned long long*)p.stats;   // requests, batches, dsteps, msteps, blocks
+    if (ct.batches) atomicAdd(st + 1, (unsigned long long)ct.batches);
+    if (ct.dsteps) atomicAdd(st + 2, (unsigned long long)ct.dsteps);
+    if (ct.steps) atomicAdd(st + 3, (unsigned long long)ct.steps);
+    if (ct.blocks) atomicAdd(st + 4, (unsigned long long)ct.blocks);
+  }
+  ct = Counters{0, 0, 0, 0};
+}
+
+// ------------------------------------------------------------------------------------------------
+// one lane-group mode of K1: groups pull replicas from work list `cls` until it is exhausted
+// ------------------------------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
+  constexpr int RING = Group<G>::RING;
+  const int g = lane / G, li = lane % G;
+  Group<G>& R = reinterpret_cast<Group<G>*>(wsmem)[g];
+  const uint32_t gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
+  const uint32_t N = p.warmup + p.seg;
+  const uint32_t count = p.counts[cls];
+  const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
+
+  uint32_t r = 0, h = 0, gen = 0, k0 = 0, k1 = 0, C = 1, B = 1, mw = 0, gamma = 0, gp = 0, wl = 0;
+  uint64_t t_idle = 0;
+  uint32_t my_slo = 0;
+  uint64_t my_sum = 0;
+  bool active = false, exhausted = false;
+
+  for (;;) {
+    // ---- acquire replicas for idle groups
+    bool want = !active && !exhausted;
+    while (__any_sync(FULL, want)) {
+      uint32_t idx = 0;
+      if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
+      idx = gshfl<G>(idx, 0);
+      if (want) {
+        if (idx >= count) {
+          exhausted = true;
+        } else {
+          r = list[idx];
+          const uint32_t ci = r / p.n_seeds;
+          const slo_knobs k = p.cfg[ci];
+          if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
+            if (li == 0) {
+              p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+              if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+            }
+          } else {
+            const DevWorkload& W = p.wl[k.workload];
+            const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+            const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+            k0 = (uint32_t)seed;
+            k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+            C = k.conc;
+            B = k.max_num_seqs;
+            mw = k.max_wait_us;
+            gamma = k.spec_on ? k.draft_len : 0u;
+            wl = k.workload;
+            setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
+            h = 0;
+            gen = 0;
+            t_idle = 0;
+            my_slo = 0;
+            my_sum = 0;
+            active = true;
+          }
+        }
+      }
+      want = !active && !exhausted;
+    }
+    if (!__any_sync(FULL, active)) break;
+
+    // ---- (a2, a3) keep [h, h + G) generated (groups with room generate ahead to share the pass)
+    bool need = active && gen < N && gen < h + G;
+    while (__any_sync(FULL, need)) {
+      const bool go = active && gen < N && gen < h + 3 * G;
+      generate<G>(R, p.wl, wl, p.tables, k0, k1, gen, N, p.warmup, go, lane, li);
+      if (go) gen += G;
+      need = active && gen < N && gen < h + G;
+    }
+
+    // ---- (a4) issue times over the window j = h + li: s_j = max(a_j, kappa_{j-C})
+    const uint32_t j = h + li;
+    uint64_t sj = INF64;
+    if (active && (uint32_t)li < C && j < N) {
+      const uint64_t aj = R.a[j % RING];
+      const uint64_t kj = j >= C ? R.kap[(j - C) % RING] : 0;
+      sj = aj > kj ? aj : kj;
+    }
+    // ---- (a5) formation instant and batch size
+    const uint64_t sh = gshfl64<G>(sj, 0);
+    uint64_t t_form = t_idle > sh ? t_idle : sh;
+    const uint64_t sl = gshfl64<G>(sj, (int)(B - 1) & (G - 1));    // INF if B > C or beyond N
+    if (mw > 0) {                                                 // (mw is group-uniform, not warp-uniform)
+      const uint64_t dl = sh + mw;
+      const uint64_t x = dl < sl ? dl : sl;
+      if (x > t_form) t_form = x;
+    }
+    uint32_t b = __popc(gballot<G>(sj <= t_form, lane));
+    if (b > B) b = B;
+    if (!active) b = 0;                     // an idle group has s_j = t_form = INF: no batch
+    const bool member = (uint32_t)li < b;
+    const uint32_t po = member ? R.po[j % RING] : 0u;
+
+    // ---- (a7) decode: S_m = min{s : sum_{j<s} (A(u_{m,j}) + 1) >= O_m}
+    uint32_t S = po >> 16;
+    if (__any_sync(FULL, active && gamma > 0)) {
+      const uint32_t Ss = spec_steps<G>(R, k0, k1, h, b, gp, active && gamma > 0, lane, li);
+      if (gamma > 0) S = member ? Ss : 0u;
+    }
+
+    // ---- (a6) prefill with the head's noise factor
+    const uint32_t w3h = R.w3[h % RING];
+    const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
+    const uint64_t f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)R.noise);
+    const uint32_t maxP = gmax<G>(po & 0xFFFFu);
+    const uint64_t t0 = t_form + f * ((uint64_t)R.pre_base + (uint64_t)R.pre_tok * maxP) / 1000000u;
+
+    // completion order = order of (S, member): at sorted position k,
+    // sum_m' min(S_m', S_(k)) = sum_{i<k} S_(i) + (b - k) S_(k)
+    const uint32_t key = gsort<G>(member ? (S << 5) | (uint32_t)li : 0xFFFFFFFFu, li);
+    const uint32_t Sk = member ? key >> 5 : 0u;
+    const uint32_t orig = key & 31u;
+    uint32_t incl = Sk;
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(FULL, incl, d, G);
+      if (li >= d) incl += v;
+    }
+    const uint32_t summin = incl - Sk + (b - (uint32_t)li) * Sk;
+    const uint64_t cum = R.alpha0 * Sk + R.alpha1 * summin;
+    const uint64_t c = t0 + (f * cum) / 1000000u;
+    if (member) R.kap[(h + li) % RING] = c;
+    const int lastm = (int)(b > 0 ? b - 1 : 0);
+    const uint64_t tend = gshfl64<G>(c, lastm);
+    const uint32_t maxS = gshfl<G>(Sk, lastm);
+
+    // ---- (a8) latency of the member at sorted position k; SLO count, sum, HBM row for the p99
+    const uint32_t i = h + orig;
+    const bool measured = member && i >= p.warmup;
+    const uint64_t l = c - (member ? R.a[i % RING] : c);
+    if (measured) {
+      my_slo += (l <= p.slo_us);
+      my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
+      my_sum += l;
+    }
+    if (member) p.lat[(size_t)(r - p.r_base) * N + i] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
+
+    // work counters, lane-local
+    ct.steps += Sk;
+    ct.blocks += gamma > 0 ? (Sk + 3u) >> 2 : 0u;
+    if (active && li == 0) {
+      ct.batches += 1;
+      ct.dsteps += maxS;
+    }
+    if (active) {
+      t_idle = tend;
+      h += b;
+    }
+
+    // ---- groups that finished their replica: outputs (p99 and goodput follow in K1b)
+    const bool fin = active && h >= N;
+    if (__any_sync(FULL, fin)) {
+      const uint32_t slo_met = gsum<G>(my_slo & 0x7FFFFFFFu);
+      const uint64_t sum = gsum64<G>(my_sum);
+      const bool sat = gballot<G>((my_slo >> 31) != 0, lane) != 0;
+      if (fin && li == 0) {
+        const uint64_t Tw = t_idle - R.a_w;
+        p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
+        if (p.stats) {
+          unsigned long long* st = (unsigned long long*)p.stats;
+          atomicAdd(st + 0, (unsigned long long)N);
+          atomicAdd(st + 4, (unsigned long long)(N + R.nphase));
+          atomicAdd(st + 5, 1ull);
+        }
+      }
+      if (fin) active = false;
+    }
+    if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u) flush_counters(p, ct);  // rare
+  }
 }
 
 #ifndef SLO_MAXNREG
@@ -216,241 +507,128 @@ __device__ __noinline__ void generate_chunk(WarpRing& R, const DevWorkload& W, c
 __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  WarpRing& R = *reinterpret_cast<WarpRing*>(smem + (size_t)warp * p.warp_bytes);
-  uint32_t* cand = reinterpret_cast<uint32_t*>(smem + (size_t)warp * p.warp_bytes + sizeof(WarpRing));
-  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
+  Counters ct{0, 0, 0, 0};
+  run_mode<8>(p, 0, wsmem, lane, ct);
+  run_mode<16>(p, 1, wsmem, lane, ct);
+  run_mode<32>(p, 2, wsmem, lane, ct);
+  if (p.stats) {
+    const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
+    const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
+    if (lane == 0) {
+      unsigned long long* st = (unsigned long long*)p.stats;
+      atomicAdd(st + 1, (unsigned long long)batches);
+      atomicAdd(st + 2, (unsigned long long)dsteps);
+      atomicAdd(st + 3, (unsigned long long)steps);
+      atomicAdd(st + 4, (unsigned long long)blocks);
+    }
+  }
+}
+
+size_t group_warp_bytes() {
+  size_t m = 4 * sizeof(Group<8>);
+  if (2 * sizeof(Group<16>) > m) m = 2 * sizeof(Group<16>);
+  if (sizeof(Group<32>) > m) m = sizeof(Group<32>);
+  return m;
+}
+
+// ------------------------------------------------------------------------------------------------
+// K0: work lists by lane-group size
+// ------------------------------------------------------------------------------------------------
+__global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, uint32_t n_seeds, uint32_t r_base,
+                                    uint32_t n_chunk, uint32_t n_wl, uint32_t* __restrict__ counts,
+                                    uint32_t* __restrict__ lists) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_chunk) return;
+  const uint32_t r = r_base + t;
+  const slo_knobs k = cfg[r / n_seeds];
+  const uint32_t need = knobs_valid(k, n_wl) ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : 1u;
+  const uint32_t cls = need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
+  const uint32_t pos = atomicAdd(counts + cls, 1u);
+  lists[(size_t)cls * n_chunk + pos] = r;
+}
+
+// ------------------------------------------------------------------------------------------------
+// K1b: exact nearest-rank p99 by shared-memory radix select; goodput (Eq. 1)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint32_t smem_vals) {
+  extern __shared__ __align__(16) uint32_t sv[];   // [256 hist][smem_vals values]
+  uint32_t* hist = sv;
+  uint32_t* vals = sv + 256;
+  __shared__ uint32_t s_digit, s_kk;
   const uint32_t N = p.warmup + p.seg;
-
-  for (;;) {
-    uint32_t r = 0;
-    if (lane == 0) r = atomicAdd(p.queue, 1u);
-    r = __shfl_sync(FULL, r, 0);
-    if (r >= p.n_rep) break;
-
-    const uint32_t ci = r / p.n_seeds;
-    const slo_knobs k = p.cfg[ci];
-    if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
-      if (lane == 0) {
+  const uint32_t n = p.seg;
+  const uint32_t rank = (uint32_t)((99ull * n + 99ull) / 100ull);
+  const uint32_t K = n - rank + 1;                  // K-th largest = rank-th smallest
+  for (uint32_t t = blockIdx.x; t < p.n_chunk; t += gridDim.x) {
+    const uint32_t r = p.r_base + t;
+    const slo_replica_result pr = p.part[r];
+    if (pr.flags & 1u) {
+      if (threadIdx.x == 0) {
         p.p99[r] = 0xFFFFFFFFu;
         p.goodput[r] = -1.0;
-        if (p.detail) p.detail[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
-        if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+        if (p.detail) p.detail[r] = pr;
       }
       continue;
     }
-    const DevWorkload& W = p.wl[k.workload];
-    const uint64_t seed = p.seeds[r - ci * p.n_seeds];
-    const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
-    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
-    const uint32_t C = k.conc, B = k.max_num_seqs, mw = k.max_wait_us;
-    const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
-
-    // ---- (a1) replica setup: thresholds, step costs, arrival state
-    uint32_t gp = 0;
-    {
-      uint64_t rr = 65536;
-      for (uint32_t w = 0; w < k.draft_width; ++w) rr = (rr * (65536u - k.accept_q16)) >> 16;
-      const uint64_t ae = 65536u - rr;
-      uint64_t prev = 1ull << 32;
-      for (uint32_t a = 1; a <= gamma; ++a) {
-        prev = (prev * ae) >> 16;
-        if (prev > 0) {
-          if (lane == 0) R.tm1[a - 1] = (uint32_t)(prev - 1);
-          gp = a;
+    const uint32_t* row = p.lat + (size_t)t * N + p.warmup;
+    const bool staged = n <= smem_vals;
+    if (staged) {
+      for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) vals[e] = row[e];
+    }
+    uint32_t prefix = 0, kk = K;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      hist[threadIdx.x] = 0;
+      __syncthreads();
+      const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+      for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+        const uint32_t v = staged ? vals[e] : row[e];
+        if ((v & hmask) == prefix) atomicAdd(hist + ((v >> shift) & 255u), 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {  // warp 0: suffix sums over 8 bins per lane, find the digit
+        const int lane = threadIdx.x;
+        uint32_t c[8], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          c[q] = hist[lane * 8 + q];
+          sum += c[q];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t v = __shfl_down_sync(FULL, incl, d);
+          if (lane + d < 32) incl += v;
+        }
+        if (incl >= kk && incl - sum < kk) {
+          uint32_t above = incl - sum, dg = 0, kn = 0;
+#pragma unroll
+          for (int q = 7; q >= 0; --q) {
+            if (kn == 0 && above + c[q] >= kk) {
+              dg = 8u * lane + q;
+              kn = kk - above;
+            }
+            above += c[q];
+          }
+          s_digit = dg;
+          s_kk = kn;
         }
       }
+      __syncthreads();
+      prefix |= s_digit << shift;
+      kk = s_kk;
+      __syncthreads();
     }
-    if (lane == 0) {
-      const uint64_t g0 = W.gap_q16[0] == INF64 ? INF64 : (W.gap_q16[0] << 8) / k.rate_scale_q8;
-      const uint64_t g1 = W.gap_q16[1] == INF64 ? INF64 : (W.gap_q16[1] << 8) / k.rate_scale_q8;
-      R.g[0] = g0;
-      R.g[1] = g1;
-      R.rho[0] = g0 == INF64 ? 0 : INF64 / g0;
-      R.rho[1] = g1 == INF64 ? 0 : INF64 / g1;
-      R.last = 0;
-      R.nphase = 0;
-      R.alpha0 = gamma == 0 ? (uint64_t)W.t.dec_base_us : (uint64_t)gamma * W.t.dr_base_us + W.t.ver_base_us;
-      R.alpha1 = gamma == 0 ? (uint64_t)W.t.dec_seq_us
-                            : (uint64_t)gamma * W.t.dr_seq_us + W.t.ver_seq_us + (uint64_t)W.t.ver_tok_us * (gamma + 1);
-      R.pre_base = W.t.pre_base_us;
-      R.pre_tok = W.t.pre_tok_us;
-      R.noise = W.t.noise_step_ppm;
-      if (W.kind != 0) {
-        const uint32_t st = W.start_state & 1u;
-        uint64_t D;
-        if (W.kind == 1) {
-          const u32x4 w = philox(0, 2, 0, 0, k0, k1);
-          D = mulshr(exp_q32(w.x), W.soj[st], 32);
-          R.nphase = 1;
-        } else {
-          D = W.soj[st];
-        }
-        R.pD = D;
-        R.pU = capacity(D, R.rho[st]);
-        R.pLam = 0;
-        R.pstart = 0;
-        R.ph = 0;
-        R.pstate = st;
+    if (threadIdx.x == 0) {
+      p.p99[r] = prefix;
+      p.goodput[r] = (double)((uint64_t)pr.slo_met * 1000000ull) / (double)pr.window_us;
+      if (p.detail) {
+        slo_replica_result d = pr;
+        d.p99_us = prefix;
+        p.detail[r] = d;
       }
     }
-    __syncwarp();
-    if (gamma > 0) {  // bucket guide for A(u)
-      for (uint32_t kk = lane; kk < 256; kk += 32) {
-        const uint32_t lo = kk << 24, top = lo | 0xFFFFFFu;
-        uint32_t A = 0, inside = 0;
-        for (uint32_t a = 0; a < gp; ++a) {
-          const uint32_t t = R.tm1[a];
-          A += (top <= t);
-          inside |= (t >= lo && t < top);
-        }
-        R.guide[kk] = (uint8_t)(A | (inside << 7));
-      }
-      __syncwarp();
-    }
-
-    // ---- replica loop state (warp-uniform) and per-lane accumulators
-    uint32_t h = 0, gen = 0;
-    uint64_t t_idle = 0;
-    uint32_t theta = 0, n_cand = 0;
-    uint32_t my_slo = 0;         // lane m: SLO-met count of the members it held; bit 31: a latency saturated
-    uint64_t my_sum = 0;         // lane m: sum of latencies
-    uint32_t my_steps = 0;       // lane m: sum of S over the members it held
-    uint32_t my_blk = 0;         // lane m: sum of ceil(S/4) (SPEC blocks of the definition)
-    uint32_t my_bd = 0;          // lane 0: batches; lane 1: sum over batches of max S (decode steps)
-    const bool big = N > (1u << 19);   // only then can a u32 lane counter overflow within a replica
-    const uint32_t K = p.topk;
-
-    while (h < N) {
-      while (gen < N && gen < h + 32) {
-        generate_chunk(R, W, p.tables, k0, k1, gen, N, p.warmup, lane);
-        gen += 32;
-      }
-
-      // ---- (a4) issue times over the window j = h + lane: s_j = max(a_j, kappa_{j-C})
-      const uint32_t j = h + lane;
-      uint64_t sj = INF64;
-      if ((uint32_t)lane < C && j < N) {
-        const uint64_t aj = R.a[j & 63];
-        const uint64_t kj = j >= C ? R.kap[(j - C) & 63] : 0;
-        sj = aj > kj ? aj : kj;
-      }
-      // ---- (a5) formation instant and batch size
-      const uint64_t sh = shfl64(sj, 0);
-      uint64_t t_form = t_idle > sh ? t_idle : sh;
-      if (mw > 0) {
-        const uint64_t sl = shfl64(sj, (int)(B - 1));   // INF if B > C or beyond N
-        const uint64_t dl = sh + mw;
-        const uint64_t x = dl < sl ? dl : sl;
-        if (x > t_form) t_form = x;
-      }
-      uint32_t b = __popc(__ballot_sync(FULL, sj <= t_form));
-      if (b > B) b = B;
-      const bool member = (uint32_t)lane < b;
-      const uint32_t po = member ? R.po[j & 63] : 0u;
-
-      // ---- (a7) decode: per-member step counts S_m = min{s : sum_{j<s} (A(u_{m,j}) + 1) >= O_m}
-      uint32_t S;
-      if (gamma == 0) {
-        S = po >> 16;
-      } else {
-        S = spec_steps(R, k0, k1, h, b, gp, lane);
-      }
-
-      // ---- (a6) prefill with the head's noise factor
-      const uint32_t w3h = R.w3[h & 63];
-      const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
-      const uint64_t f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)R.noise);
-      const uint32_t maxP = __reduce_max_sync(FULL, po & 0xFFFFu);
-      const uint64_t t0 = t_form + f * ((uint64_t)R.pre_base + (uint64_t)R.pre_tok * maxP) / 1000000u;
-
-      // Completion order = order of S (ties by member index): bitonic sort of (S, member) over the first
-      // 2^ceil(log2 b) lanes; at sorted position k, sum_m' min(S_m', S_(k)) = sum_{i<k} S_(i) + (b-k) S_(k)
-      // and Cum_(k) = alpha0 S_(k) + alpha1 * that (d(n) = alpha0 + alpha1 n).
-      const int lgn = 32 - __clz(b - 1u);
-      uint32_t key = member ? (S << 5) | (uint32_t)lane : 0xFFFFFFFFu;
-      for (int kk = 1; kk <= lgn; ++kk) {
-        for (int jj = kk - 1; jj >= 0; --jj) {
-          const uint32_t other = __shfl_xor_sync(FULL, key, 1 << jj);
-          const bool up = ((lane >> kk) & 1) == 0;
-          const bool lower = ((lane >> jj) & 1) == 0;
-          key = (lower == up) ? min(key, other) : max(key, other);
-        }
-      }
-      const uint32_t Sk = member ? key >> 5 : 0u;       // sorted step count at position k = lane
-      const uint32_t orig = key & 31u;                   // member index of position k
-      uint32_t incl = Sk;
-      for (int d = 1; d < (1 << lgn); d <<= 1) {
-        const uint32_t v = __shfl_up_sync(FULL, incl, d);
-        if (lane >= d) incl += v;
-      }
-      const uint32_t summin = incl - Sk + (b - (uint32_t)lane) * Sk;
-      const uint64_t cum = R.alpha0 * Sk + R.alpha1 * summin;
-      const uint64_t c = t0 + (f * cum) / 1000000u;
-      if (member) R.kap[(h + lane) & 63] = c;
-      t_idle = shfl64(c, (int)b - 1);
-      const uint32_t maxS = __shfl_sync(FULL, Sk, (int)b - 1);
-
-      // ---- (a8) latencies, SLO count, sums, p99 candidates (position k holds member orig)
-      const uint32_t i = h + orig;
-      const bool measured = member && i >= p.warmup;
-      const uint64_t l = c - (member ? R.a[i & 63] : c);
-      const uint32_t ls = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
-      if (measured) {
-        my_slo += (l <= p.slo_us);
-        my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
-        my_sum += l;
-      }
-      if (p.lat != nullptr && member) p.lat[(size_t)r * N + i] = ls;
-      const bool ins = measured && ls > theta;
-      const uint32_t im = __ballot_sync(FULL, ins);
-      if (ins) cand[n_cand + __popc(im & lanemask_lt)] = ls;
-      n_cand += __popc(im);
-      if (n_cand > p.cap - 32) {
-        __syncwarp();
-        theta = kth_largest(cand, n_cand, K, R.hist, lane);
-        n_cand = compact_above(cand, n_cand, theta, lane);
-      }
-      // work counters, lane-local (flushed to the warp's totals before they could overflow)
-      my_steps += Sk;
-      my_blk += gamma > 0 ? (Sk + 3u) >> 2 : 0u;
-      my_bd += lane == 0 ? 1u : maxS;
-      if (big && (my_steps >= 0x80000000u || my_bd >= 0x80000000u)) {
-        if (p.stats) {
-          unsigned long long* st = (unsigned long long*)p.stats;
-          atomicAdd(st + 3, (unsigned long long)my_steps);
-          atomicAdd(st + 4, (unsigned long long)my_blk);
-          if (lane < 2) atomicAdd(st + 1 + lane, (unsigned long long)my_bd);
-        }
-        my_steps = my_blk = my_bd = 0;
-      }
-      h += b;
-    }
-
-    // ---- (a9, a10) replica outputs
-    __syncwarp();
-    const uint32_t p99 = n_cand >= K ? kth_largest(cand, n_cand, K, R.hist, lane) : theta;
-    const uint32_t slo_met = __reduce_add_sync(FULL, my_slo & 0x7FFFFFFFu);
-    const uint64_t sum = warp_sum64(my_sum);
-    const bool sat = __any_sync(FULL, (my_slo >> 31) != 0);
-    if (lane == 0) {
-      const uint64_t Tw = t_idle - R.a_w;
-      const uint64_t T = Tw < 1 ? 1 : Tw;
-      p.p99[r] = p99;
-      p.goodput[r] = (double)((uint64_t)slo_met * 1000000ull) / (double)T;
-      if (p.detail) p.detail[r] = slo_replica_result{p99, slo_met, p.seg, sat ? 2u : 0u, T, sum};
-    }
-    if (p.stats) {  // requests, batches, decode steps, member steps, Philox blocks, replicas
-      const uint64_t msteps = warp_sum64(my_steps);
-      const uint64_t blocks = warp_sum64(my_blk);
-      unsigned long long* st = (unsigned long long*)p.stats;
-      if (lane < 2) atomicAdd(st + 1 + lane, (unsigned long long)my_bd);
-      if (lane == 2) atomicAdd(st + 3, (unsigned long long)msteps);
-      if (lane == 3) atomicAdd(st + 4, (unsigned long long)(blocks + N + R.nphase));
-      if (lane == 4) atomicAdd(st + 0, (unsigned long long)N);
-      if (lane == 5) atomicAdd(st + 5, 1ull);
-    }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
