@@ -92,7 +92,8 @@ struct alignas(16) Group {
   uint64_t g[2], rho[2];              // scaled mean gaps, floor((2^64-1)/g)
   uint64_t last;                      // last generated a (kind 0) or tau (kinds 1, 2)
   uint64_t pstart, pD, pU, pLam, nphase, a_w, alpha0, alpha1;
-  uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, pad;
+  uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, gp;
+  uint32_t k0, k1, pad[2];
 };
 
 // A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
@@ -106,53 +107,77 @@ __device__ __forceinline__ uint32_t accepted(const Group<G>& R, uint32_t u, uint
   return A;
 }
 
-// Lane-parallel step counts of a speculative batch of b members in a G-lane group: member m owns the
-// L = G / 2^ceil(log2 b) lanes [m L, (m+1) L); each round every lane of an unfinished member computes one
-// Philox SPEC block (4 decode steps), a segmented scan of block token sums finds the block where the
-// member's cumulative tokens reach O_m, and that lane resolves the exact step.  Blocks
-// past the crossing are computed speculatively and discarded.  Returns S_m in group lane m (m < b).
+// Warp-pooled speculative step counts: every lane holding a speculative batch member
+// (`mine`: member of an active group with gamma > 0) is a pending item, whatever its group.  Each round the
+// u pending members get L = 32 / 2^ceil(log2 u) consecutive lanes of the whole warp; each lane computes one
+// Philox SPEC block (4 decode steps) of its member, a segmented scan of the block token sums finds the
+// block where the member's cumulative tokens reach O, and that lane resolves the exact step.  Members
+// that finish release their lanes to the others in the next round.  Blocks past a crossing are computed
+// speculatively and discarded (the definition's work is ceil(S/4) blocks per member).  Returns S_m in the
+// member's own lane.
 template <int G>
-__device__ __forceinline__ uint32_t spec_steps(const Group<G>& R, uint32_t k0, uint32_t k1, uint32_t h, uint32_t b,
-                                               uint32_t gp, bool run, int lane, int li) {
-  constexpr int LOGG = G == 8 ? 3 : (G == 16 ? 4 : 5);
-  const uint32_t bb = b > 0 ? b : 1u;
-  const int lg = LOGG - (32 - __clz(bb - 1u));      // log2 L
-  const uint32_t L = 1u << lg;
-  const uint32_t m = (uint32_t)li >> lg, off = (uint32_t)li & (L - 1u);
-  const uint32_t segbase = m << lg;
-  const uint32_t j = h + m;
-  const uint32_t O = (run && m < b) ? (R.po[j % Group<G>::RING] >> 16) : 0u;
-  const uint32_t lowmask = (L >= 32u) ? FULL : ((1u << L) - 1u);
-  uint32_t cum = 0, q = off, S = 0;
-  bool pending = run && m < b;
-  while (__any_sync(FULL, pending)) {
+__device__ __forceinline__ uint32_t spec_steps(const Group<G>* Rw, uint8_t* slots, uint32_t j, uint32_t O, bool mine,
+                                               int lane, uint32_t lanemask_lt) {
+  uint32_t S = 0, cum = 0, q = 0;
+  bool pending = mine;
+  uint32_t pend = __ballot_sync(FULL, pending);
+  while (pend) {
+    const uint32_t u = __popc(pend);
+    const int lg = __clz(u - 1u) - 27;                 // log2 L, L = 32 / 2^ceil(log2 u)
+    const uint32_t L = 1u << lg;
+    const uint32_t lowmask = FULL >> (32 - L);
+    const uint32_t myslot = __popc(pend & lanemask_lt);
+    if (pending) slots[myslot] = (uint8_t)lane;
+    __syncwarp();
+    const uint32_t slot = (uint32_t)lane >> lg, off = (uint32_t)lane & (L - 1u);
+    const bool active = slot < u;
+    const int src = active ? slots[slot] : lane;
+    __syncwarp();
+    const uint32_t mj = __shfl_sync(FULL, j, src);
+    const uint32_t moc = __shfl_sync(FULL, O | (cum << 16), src);   // O, cum < 2^16
+    const uint32_t mq = __shfl_sync(FULL, q, src) + off;            // this lane's SPEC block
+    const uint32_t mO = moc & 0xFFFFu, mcum = moc >> 16;
+    const Group<G>& Rm = Rw[src / G];
     uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-    if (pending) {
-      const u32x4 w = philox(j, 1, q, 0, k0, k1);
-      e0 = accepted(R, w.x, gp) + 1;
-      e1 = accepted(R, w.y, gp) + 1;
-      e2 = accepted(R, w.z, gp) + 1;
-      e3 = accepted(R, w.w, gp) + 1;
+    if (active) {
+      const u32x4 w = philox(mj, 1, mq, 0, Rm.k0, Rm.k1);
+      const uint32_t g0 = Rm.guide[w.x >> 24], g1 = Rm.guide[w.y >> 24];
+      const uint32_t g2 = Rm.guide[w.z >> 24], g3 = Rm.guide[w.w >> 24];
+      e0 = (g0 & 0x7Fu) + 1;
+      e1 = (g1 & 0x7Fu) + 1;
+      e2 = (g2 & 0x7Fu) + 1;
+      e3 = (g3 & 0x7Fu) + 1;
+      if ((g0 | g1 | g2 | g3) & 0x80u) {               // a threshold inside one of the buckets (rare)
+        const uint32_t gp = Rm.gp;
+        e0 = accepted(Rm, w.x, gp) + 1;
+        e1 = accepted(Rm, w.y, gp) + 1;
+        e2 = accepted(Rm, w.z, gp) + 1;
+        e3 = accepted(Rm, w.w, gp) + 1;
+      }
     }
     const uint32_t T = e0 + e1 + e2 + e3;
-    uint32_t P = T;  // segmented inclusive scan over the L lanes
+    uint32_t P = T;                                    // segmented inclusive scan over the L lanes
 #pragma unroll
-    for (int d = 1; d < G; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(FULL, P, d, G);
-      if ((uint32_t)d < L && (int)off >= d) P += v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(FULL, P, d);
+      if ((int)off >= d) P += v;                       // off < L, so d <= off stays inside the segment
     }
-    const bool cross = pending && (cum + P >= O);
-    const uint32_t segbits = (gballot<G>(cross, lane) >> segbase) & lowmask;
-    const uint32_t first = __ffs(segbits) - 1u;
+    // the cumulative token count is non-decreasing along a segment, so its crossing lanes are a suffix:
+    // with nc crossing lanes the first one is at segbase + L - nc
+    const bool cross = active && (mcum + P >= mO);
+    const uint32_t cb = __ballot_sync(FULL, cross);
+    const uint32_t up = __shfl_up_sync(FULL, (uint32_t)cross, 1);
+    const uint32_t nprev = off > 0 ? up : 0u;
     uint32_t give = P;
-    if (segbits && off == first) {
-      const uint32_t c = cum + P - T;
-      const uint32_t base = 4u * q;
-      give = c + e0 >= O ? base + 1 : (c + e0 + e1 >= O ? base + 2 : (c + e0 + e1 + e2 >= O ? base + 3 : base + 4));
+    if (cross && !nprev) {                             // first crossing lane: exact step inside the block
+      const uint32_t c = mcum + P - T;                 // tokens before this block
+      give = 4u * mq + 1u + (c + e0 < mO) + (c + e0 + e1 < mO) + (c + e0 + e1 + e2 < mO);
     }
-    const uint32_t got = gshfl<G>(give, (int)(segbits ? segbase + first : segbase + L - 1u));
+    const uint32_t nc = __popc((cb >> ((myslot << lg) & 31u)) & lowmask);
+    const int from = (int)(((myslot + 1u) << lg) - (nc ? nc : 1u)) & 31;
+    const uint32_t got = __shfl_sync(FULL, give, from);
     if (pending) {
-      if (segbits) {
+      if (nc) {
         S = got;
         pending = false;
       } else {
@@ -160,8 +185,9 @@ __device__ __forceinline__ uint32_t spec_steps(const Group<G>& R, uint32_t k0, u
         q += L;
       }
     }
+    pend = __ballot_sync(FULL, pending);
   }
-  return gshfl<G>(S, (li << lg) & (G - 1));
+  return S;
 }
 
 // (a1) set up a newly acquired replica (group-convergent; other groups do not enter)
@@ -216,6 +242,11 @@ __device__ __forceinline__ void setup_replica(Group<G>& R, const DevWorkload& W,
       R.ph = 0;
       R.pstate = st;
     }
+  }
+  if (li == 0) {
+    R.gp = gp;
+    R.k0 = k0;
+    R.k1 = k1;
   }
   __syncwarp(gmask);
   if (gamma > 0) {  // bucket guide for A(u)
@@ -332,8 +363,10 @@ __device__ __forceinline__ void flush_counters(const SimParams& p, Counters& ct)
 // one lane-group mode of K1: groups pull replicas from work list `cls` until it is exhausted
 // ------------------------------------------------------------------------------------------------
 template <int G>
-__device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
+__device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, uint8_t* slots, int lane,
+                                         Counters& ct) {
   constexpr int RING = Group<G>::RING;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
   const int g = lane / G, li = lane % G;
   Group<G>& R = reinterpret_cast<Group<G>*>(wsmem)[g];
   const uint32_t gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
@@ -425,9 +458,10 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 
     // ---- (a7) decode: S_m = min{s : sum_{j<s} (A(u_{m,j}) + 1) >= O_m}
     uint32_t S = po >> 16;
-    if (__any_sync(FULL, active && gamma > 0)) {
-      const uint32_t Ss = spec_steps<G>(R, k0, k1, h, b, gp, active && gamma > 0, lane, li);
-      if (gamma > 0) S = member ? Ss : 0u;
+    if (__any_sync(FULL, member && gamma > 0)) {
+      const uint32_t Ss = spec_steps<G>(reinterpret_cast<const Group<G>*>(wsmem), slots, j, po >> 16,
+                                        member && gamma > 0, lane, lanemask_lt);
+      if (gamma > 0) S = Ss;
     }
 
     // ---- (a6) prefill with the head's noise factor
@@ -502,16 +536,17 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 }
 
 #ifndef SLO_MAXNREG
-#define SLO_MAXNREG 80
+#define SLO_MAXNREG 96
 #endif
 __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
+  uint8_t* slots = wsmem + p.warp_bytes - 32;            // spec-decode slot map (last 32 B of the warp area)
   Counters ct{0, 0, 0, 0};
-  run_mode<8>(p, 0, wsmem, lane, ct);
-  run_mode<16>(p, 1, wsmem, lane, ct);
-  run_mode<32>(p, 2, wsmem, lane, ct);
+  run_mode<8>(p, 0, wsmem, slots, lane, ct);
+  run_mode<16>(p, 1, wsmem, slots, lane, ct);
+  run_mode<32>(p, 2, wsmem, slots, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -529,7 +564,7 @@ size_t group_warp_bytes() {
   size_t m = 4 * sizeof(Group<8>);
   if (2 * sizeof(Group<16>) > m) m = 2 * sizeof(Group<16>);
   if (sizeof(Group<32>) > m) m = sizeof(Group<32>);
-  return m;
+  return m + 32;   // + spec-decode slot map
 }
 
 // ------------------------------------------------------------------------------------------------
