@@ -114,6 +114,8 @@ class Clocks:
         self.path = os.path.join("/tmp", f"slo_clocks_{os.getpid()}.csv")
 
     def start(self):
+        if os.environ.get("CUDA_INJECTION64_PATH") or os.environ.get("NV_NSIGHT_INJECTION_TRANSPORT_TYPE"):
+            return          # under a profiler: never spawn nvidia-smi next to ncu's injected process
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                           "-i", str(self.index), "-lms", "200"], stdout=open(self.path, "w"),
@@ -213,8 +215,15 @@ def main():
                       blocks_per_sm=args.blocks_per_sm)
     info = S.info()
 
-    # weak scaling: every rank runs the full grid on its own seed block
-    seeds = inputs.seeds(cfg.n_seeds, cfg.seed_offset + rank * cfg.n_seeds)
+    from paper_2603_11340_b200.dist import seed_block, sweep_seed_offset
+    if args.workload == "c4":
+        # the climb is seed-sharded (strong scaling): the pooled aggregates equal the 1-GPU ones exactly
+        lo, hi = seed_block(cfg.n_seeds, rank, world)
+        seeds = cfg.seeds()[lo:hi]
+    else:
+        # sweeps are weak-scaled: every rank runs the full grid on its own seed block
+        seeds = inputs.seeds(cfg.n_seeds, sweep_seed_offset(cfg.n_seeds, rank, cfg.seed_offset))
+    n_seeds_local = len(seeds)
     n_cfg = len(cfg.knobs)
     N = cfg.segment_len + cfg.warmup_len
     seeds_t = sim.seeds_tensor(seeds, device=dev)
@@ -225,7 +234,7 @@ def main():
         state = S.climb_state(cfg.knobs[0])
     else:
         cands = sim.knobs_tensor(cfg.knobs, device=dev)
-    R = n_cfg * cfg.n_seeds
+    R = n_cfg * n_seeds_local
     out = S.alloc_outputs(R, detail=True, stats=True)
     agg = torch.empty((n_cfg, 32), dtype=torch.uint8, device=dev)
     parts = torch.empty((world * n_cfg, 32), dtype=torch.uint8, device=dev) if world > 1 else None
@@ -234,7 +243,8 @@ def main():
     k1_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k1_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     st_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches_per_step = 2 + (1 if world > 1 else 0) + (1 if args.workload == "c4" else 0)
+    # K0 classify + K1 simulate + K1b select + K2 aggregate (+ K2b reduce for N>1 sweeps, K3 for the climb)
+    launches_per_step = 4 + (1 if (world > 1 and args.workload != "c4") else 0) + (1 if args.workload == "c4" else 0)
 
     def step(i=None):
         if i is not None:
@@ -242,14 +252,13 @@ def main():
         S.run_batch(cands, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out, stream=stream)
         if i is not None:
             k1_end[i].record(stream)
-        S.aggregate(out["detail"], n_cfg, cfg.n_seeds, out=agg, stream=stream)
-        total = agg
+        S.aggregate(out["detail"], n_cfg, n_seeds_local, out=agg, stream=stream)
         if world > 1:
-            dist.all_gather_into_tensor(parts, agg)
+            dist.all_gather_into_tensor(parts, agg)                 # the one exchange
+        if args.workload == "c4":                                    # K3 sums the per-rank parts itself
+            S.hillclimb_step(space, sp, cands, parts if world > 1 else agg, world, state, stream=stream)
+        elif world > 1:
             S.aggregate_reduce(parts, world, n_cfg, out=pooled, stream=stream)
-            total = pooled
-        if args.workload == "c4":
-            S.hillclimb_step(space, sp, cands, total, 1, state, stream=stream)
         if i is not None:
             st_end[i].record(stream)
 
@@ -318,12 +327,13 @@ def main():
         line = {
             "metric": "simulated requests/s", "value": value, "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong" if args.workload == "c4" else "weak",
+            "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded Philox streams; LL/STRESS presets of DESIGN.md §5)",
             "config": {"workload": DESCR[args.workload], "replicas_per_gpu": R, "requests_per_replica": N,
                        "requests_per_step_per_gpu": req_per_step, "preset": "LL" if args.workload != "c5" else "STRESS",
                        "l2": "flushed between timed steps (256 MiB write, untimed); inputs are < 1 MB",
-                       "parallelism": f"dp{world} over replicas (seed blocks)",
+                       "parallelism": f"dp{world} over replicas ({'seed-sharded climb' if args.workload == 'c4' else 'weak: full grid, per-rank seed block'})",
                        "launch": {"blocks_per_sm": info["blocks_per_sm"], "warps_per_block": info["warps_per_block"],
                                   "regs_per_thread": info["regs_per_thread"]}},
             "replica_segments_per_s": world * R * args.steps / t_total,
@@ -333,7 +343,8 @@ def main():
                                       "decode_steps": int(stats["decode_steps"])},
             "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
                          "frac": achieved_gops / peak_gops, "traffic": traffic,
-                         "kernel": "slo_sim_kernel (K1)",
+                         "kernel": "slo_sim_run_batch = K0 classify + K1 simulate + K1b p99 select (K1 dominates, "
+                                   "see profiles/ launch list)",
                          "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
                                  "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)"},
             "gpu_launches": launches_per_step * args.steps,

@@ -107,7 +107,9 @@ typedef struct {
   uint32_t crn;                 /* 1 (default): cfgkey = workload.stream_id; 0: FNV-1a of the knob record */
   uint32_t warps_per_block;     /* 0 = default (4)                                                        */
   uint32_t blocks_per_sm;       /* 0 = as many as fit                                                     */
-  uint32_t reserved[5];         /* must be 0                                                              */
+  uint32_t scratch_mb;          /* latency-row scratch per launch chunk in MiB; 0 = default (4096). A run */
+                                /* whose rows exceed it is split into chunks of replicas (same results)  */
+  uint32_t reserved[4];         /* must be 0                                                              */
 } slo_sim_opts;
 
 typedef struct {                /* read-only launch facts of a handle                                    */

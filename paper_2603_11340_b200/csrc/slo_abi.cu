@@ -124,7 +124,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   o.crn = 1;
   if (opts) {
     o = *opts;
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < 4; ++i)
       if (o.reserved[i]) return fail(nullptr, SLO_E_INVAL, "create: opts.reserved must be 0");
     if (o.crn > 1) return fail(nullptr, SLO_E_INVAL, "create: opts.crn must be 0 or 1");
     if (o.warps_per_block > (uint32_t)slo::kMaxWarpsPerBlock)
@@ -194,6 +194,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   h->crn = o.crn;
   if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
+  if (o.scratch_mb) h->lat_budget = (size_t)o.scratch_mb << 20;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel) == cudaSuccess) h->regs = fa.numRegs;
   cudaError_t e;

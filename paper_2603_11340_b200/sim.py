@@ -104,7 +104,7 @@ class Simulator:
     """One libslosim handle on one CUDA device."""
 
     def __init__(self, workloads: Sequence[Dict], device: Optional[int] = None, crn: int = 1,
-                 warps_per_block: int = 0, blocks_per_sm: int = 0):
+                 warps_per_block: int = 0, blocks_per_sm: int = 0, scratch_mb: int = 0):
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
@@ -130,6 +130,7 @@ class Simulator:
             w.stream_id = d["stream_id"]
         opts = _lib.slo_sim_opts()
         opts.crn, opts.warps_per_block, opts.blocks_per_sm = crn, warps_per_block, blocks_per_sm
+        opts.scratch_mb = scratch_mb
         h = C.c_void_p()
         check(lib().slo_sim_create(self.device, arr, n, C.byref(opts), C.byref(h)))
         self.h = h

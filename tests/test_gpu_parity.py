@@ -259,3 +259,40 @@ def test_launch_shapes_agree(S, orc):
     for wpb, bps in ((1, 1), (8, 0), (2, 3)):
         g = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=True, warps_per_block=wpb, blocks_per_sm=bps)
         assert np.array_equal(g["lat"], base["lat"]) and np.array_equal(g["gp"], base["gp"])
+    # latency-row scratch split into many launch chunks (1 MiB -> 524 replicas per chunk of 63 x 4 = 252... )
+    base_nl = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=False)
+    g = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=False, scratch_mb=1)
+    assert np.array_equal(g["p99"], base_nl["p99"]) and np.array_equal(g["gp"], base_nl["gp"])
+    assert g["detail"].tobytes() == base_nl["detail"].tobytes()
+    cfg2 = inputs.config_c3(n_seeds=40, segment_len=3000)            # 2520 replicas x 12 KB rows > 1 MiB
+    a = _run_gpu(S, wls, cfg2.knobs, cfg2.seeds(), 3000, latencies=False)
+    b = _run_gpu(S, wls, cfg2.knobs, cfg2.seeds(), 3000, latencies=False, scratch_mb=1)
+    assert np.array_equal(a["p99"], b["p99"]) and a["detail"].tobytes() == b["detail"].tobytes()
+    assert a["stats"].tobytes() == b["stats"].tobytes()
+
+
+def test_device_climb_seed_sharded_parts(S):
+    """The N>1 layout: per-rank aggregates over seed slices, stacked in rank order and summed by K3,
+    give exactly the single-part climb step (integer sums)."""
+    from paper_2603_11340_b200._lib import CLIMB_DTYPE
+    from paper_2603_11340_b200.dist import seed_block
+    cfg = inputs.config_c4(n_seeds=10, segment_len=300)
+    space, sp = cfg.extra["space"], cfg.extra["score"]
+    s = S.Simulator(cfg.workloads, device=0)
+    seeds = cfg.seeds()
+    states, cands_out = [], []
+    for world in (1, 3):
+        cands = s.candidates(space, cfg.knobs[0], 32)
+        state = s.climb_state(cfg.knobs[0])
+        for _ in range(3):
+            parts = []
+            for rank in range(world):
+                lo, hi = seed_block(len(seeds), rank, world)
+                out = s.run_batch(cands, S.seeds_tensor(seeds[lo:hi]), cfg.segment_len)
+                parts.append(s.aggregate(out["detail"], 32, hi - lo))
+            s.hillclimb_step(space, sp, cands, torch.cat(parts), world, state)
+        torch.cuda.synchronize()
+        states.append(S.unpack(state, CLIMB_DTYPE)[0].tobytes())
+        cands_out.append(cands.cpu().numpy().tobytes())
+    assert states[0] == states[1] and cands_out[0] == cands_out[1]
+    s.close()
