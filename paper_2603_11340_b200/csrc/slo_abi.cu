@@ -27,7 +27,7 @@ struct slo_sim {
   uint32_t crn = 1;
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
-  uint32_t* d_ctl = nullptr;        // [8]: K0 list counts [3], K1 list cursors [3]
+  uint32_t* d_ctl = nullptr;        // [104]: list lengths [3], K1 cursors [3], K0 bucket counts/cursors [96]
   // run scratch (grow-only): work lists, latency rows, per-replica partial results
   uint32_t* d_lists = nullptr;
   size_t lists_cap = 0;
@@ -200,7 +200,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
-      (e = cudaMalloc(&h->d_ctl, sizeof(uint32_t) * 8)) != cudaSuccess) {
+      (e = cudaMalloc(&h->d_ctl, sizeof(uint32_t) * 104)) != cudaSuccess) {
     slo_sim_destroy(h);
     return fail(nullptr, SLO_E_NOMEM, "create: cudaMalloc: %s", cudaGetErrorString(e));
   }
@@ -307,7 +307,10 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     p.n_chunk = nc;
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
-    CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * 8, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * 104, st));
+    slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, n_seeds, (uint32_t)r0, nc, h->n_wl,
+                                                                    h->d_ctl);
+    CUDA_TRY(h, cudaGetLastError());
     slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, n_seeds, (uint32_t)r0, nc, h->n_wl, h->d_ctl,
                                                               h->d_lists);
     CUDA_TRY(h, cudaGetLastError());

@@ -24,7 +24,7 @@ struct SimParams {
   const uint64_t* seeds;
   const DevWorkload* wl;
   const uint32_t* tables;
-  uint32_t* counts;            // [3] replicas per work list (K0)
+  uint32_t* counts;            // [3] replicas per work list (K0); ctl[8..104) K0 bucket counters
   uint32_t* cursor;            // [3] next list entry (K1)
   const uint32_t* lists;       // [3][n_chunk] replica indices by lane-group size 8 / 16 / 32
   uint32_t* lat;               // [n_chunk][N] stored latency of every request of the chunk's replicas
@@ -40,8 +40,10 @@ struct SimParams {
 };
 
 __global__ void slo_sim_kernel(const SimParams p);
+__global__ void slo_classify_count_kernel(const slo_knobs* cfg, uint32_t n_seeds, uint32_t r_base,
+                                          uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl);
 __global__ void slo_classify_kernel(const slo_knobs* cfg, uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk,
-                                    uint32_t n_wl, uint32_t* counts, uint32_t* lists);
+                                    uint32_t n_wl, uint32_t* ctl, uint32_t* lists);
 __global__ void slo_select_kernel(const SimParams p, uint32_t smem_vals);
 size_t group_warp_bytes();   // per-warp shared memory of K1
 __global__ void slo_aggregate_kernel(const slo_replica_result* detail, uint32_t n_cfg, uint32_t n_seeds,

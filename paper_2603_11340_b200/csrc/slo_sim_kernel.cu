@@ -93,7 +93,8 @@ struct alignas(16) Group {
   uint64_t last;                      // last generated a (kind 0) or tau (kinds 1, 2)
   uint64_t pstart, pD, pU, pLam, nphase, a_w, alpha0, alpha1;
   uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, gp;
-  uint32_t k0, k1, pad[2];
+  uint32_t k0, k1, wl, pad;
+  uint4 knob;                         // C, B, max_wait_us, gamma_eff (kept here, not in registers)
 };
 
 // A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
@@ -374,7 +375,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   const uint32_t count = p.counts[cls];
   const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
 
-  uint32_t r = 0, h = 0, gen = 0, k0 = 0, k1 = 0, C = 1, B = 1, mw = 0, gamma = 0, gp = 0, wl = 0;
+  uint32_t r = 0, h = 0, gen = 0;
   uint64_t t_idle = 0;
   uint32_t my_slo = 0;
   uint64_t my_sum = 0;
@@ -403,13 +404,13 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
             const DevWorkload& W = p.wl[k.workload];
             const uint64_t seed = p.seeds[r - ci * p.n_seeds];
             const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
-            k0 = (uint32_t)seed;
-            k1 = (uint32_t)(seed >> 32) ^ cfgkey;
-            C = k.conc;
-            B = k.max_num_seqs;
-            mw = k.max_wait_us;
-            gamma = k.spec_on ? k.draft_len : 0u;
-            wl = k.workload;
+            const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+            const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+            uint32_t gp;
+            if (li == 0) {
+              R.knob = make_uint4(k.conc, k.max_num_seqs, k.max_wait_us, gamma);
+              R.wl = k.workload;
+            }
             setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
             h = 0;
             gen = 0;
@@ -428,12 +429,14 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     bool need = active && gen < N && gen < h + G;
     while (__any_sync(FULL, need)) {
       const bool go = active && gen < N && gen < h + 3 * G;
-      generate<G>(R, p.wl, wl, p.tables, k0, k1, gen, N, p.warmup, go, lane, li);
+      generate<G>(R, p.wl, R.wl, p.tables, R.k0, R.k1, gen, N, p.warmup, go, lane, li);
       if (go) gen += G;
       need = active && gen < N && gen < h + G;
     }
 
     // ---- (a4) issue times over the window j = h + li: s_j = max(a_j, kappa_{j-C})
+    const uint4 kn = R.knob;
+    const uint32_t C = kn.x, B = kn.y, mw = kn.z;
     const uint32_t j = h + li;
     uint64_t sj = INF64;
     if (active && (uint32_t)li < C && j < N) {
@@ -458,10 +461,11 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 
     // ---- (a7) decode: S_m = min{s : sum_{j<s} (A(u_{m,j}) + 1) >= O_m}
     uint32_t S = po >> 16;
-    if (__any_sync(FULL, member && gamma > 0)) {
+    const bool spec = kn.w > 0;
+    if (__any_sync(FULL, member && spec)) {
       const uint32_t Ss = spec_steps<G>(reinterpret_cast<const Group<G>*>(wsmem), slots, j, po >> 16,
-                                        member && gamma > 0, lane, lanemask_lt);
-      if (gamma > 0) S = Ss;
+                                        member && spec, lane, lanemask_lt);
+      if (spec) S = Ss;
     }
 
     // ---- (a6) prefill with the head's noise factor
@@ -503,7 +507,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 
     // work counters, lane-local
     ct.steps += Sk;
-    ct.blocks += gamma > 0 ? (Sk + 3u) >> 2 : 0u;
+    ct.blocks += spec ? (Sk + 3u) >> 2 : 0u;
     if (active && li == 0) {
       ct.batches += 1;
       ct.dsteps += maxS;
@@ -536,7 +540,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 }
 
 #ifndef SLO_MAXNREG
-#define SLO_MAXNREG 96
+#define SLO_MAXNREG 80
 #endif
 __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -568,18 +572,50 @@ size_t group_warp_bytes() {
 }
 
 // ------------------------------------------------------------------------------------------------
-// K0: work lists by lane-group size
+// K0: work lists by lane-group size, longest expected replicas first (a 16-bucket counting sort)
 // ------------------------------------------------------------------------------------------------
+// bucket 0 = most expensive: speculative first, then the smaller the effective batch min(C, B) the more
+// batches a segment takes; invalid records (no work) last.
+__device__ __forceinline__ uint32_t work_class(const slo_knobs& k, uint32_t n_wl, uint32_t& bucket) {
+  if (!knobs_valid(k, n_wl)) {
+    bucket = 15;
+    return 0;
+  }
+  const uint32_t need = max((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
+  const uint32_t beff = min((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
+  const bool spec = k.spec_on && k.draft_len > 0;
+  bucket = (spec ? 0u : 8u) + (beff >= 8 ? 7u : beff - 1u);
+  return need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
+}
+
+__global__ void slo_classify_count_kernel(const slo_knobs* __restrict__ cfg, uint32_t n_seeds, uint32_t r_base,
+                                          uint32_t n_chunk, uint32_t n_wl, uint32_t* __restrict__ ctl) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_chunk) return;
+  uint32_t bucket;
+  const uint32_t cls = work_class(cfg[(r_base + t) / n_seeds], n_wl, bucket);
+  atomicAdd(ctl + 8 + cls * 16 + bucket, 1u);     // ctl[8 + 48): per (class, bucket) counts
+}
+
 __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, uint32_t n_seeds, uint32_t r_base,
-                                    uint32_t n_chunk, uint32_t n_wl, uint32_t* __restrict__ counts,
+                                    uint32_t n_chunk, uint32_t n_wl, uint32_t* __restrict__ ctl,
                                     uint32_t* __restrict__ lists) {
+  __shared__ uint32_t off[48];
+  if (threadIdx.x < 3) {                           // exclusive offsets of the buckets inside each list
+    uint32_t acc = 0;
+    for (int bkt = 0; bkt < 16; ++bkt) {
+      off[threadIdx.x * 16 + bkt] = acc;
+      acc += ctl[8 + threadIdx.x * 16 + bkt];
+    }
+    if (blockIdx.x == 0) ctl[threadIdx.x] = acc;   // list lengths (read by K1)
+  }
+  __syncthreads();
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_chunk) return;
   const uint32_t r = r_base + t;
-  const slo_knobs k = cfg[r / n_seeds];
-  const uint32_t need = knobs_valid(k, n_wl) ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : 1u;
-  const uint32_t cls = need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
-  const uint32_t pos = atomicAdd(counts + cls, 1u);
+  uint32_t bucket;
+  const uint32_t cls = work_class(cfg[r / n_seeds], n_wl, bucket);
+  const uint32_t pos = off[cls * 16 + bucket] + atomicAdd(ctl + 56 + cls * 16 + bucket, 1u);
   lists[(size_t)cls * n_chunk + pos] = r;
 }
 
