@@ -574,8 +574,9 @@ size_t group_warp_bytes() {
 // ------------------------------------------------------------------------------------------------
 // K0: work lists by lane-group size, longest expected replicas first (a 16-bucket counting sort)
 // ------------------------------------------------------------------------------------------------
-// bucket 0 = most expensive: speculative first, then the smaller the effective batch min(C, B) the more
-// batches a segment takes; invalid records (no work) last.
+// Expected cost ~ (batches per segment) x (cost per batch); a saturated replica runs ~N / min(C, B) batches
+// and a speculative batch costs ~3x a plain one.  bucket = floor(log2(beff^2)) (+3 ~ 2 log2 3 if not
+// speculative), so bucket 0 = most expensive; invalid records (no work) go last.
 __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, uint32_t n_wl, uint32_t& bucket) {
   if (!knobs_valid(k, n_wl)) {
     bucket = 15;
@@ -584,7 +585,7 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, uint32_t n_wl
   const uint32_t need = max((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
   const uint32_t beff = min((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
   const bool spec = k.spec_on && k.draft_len > 0;
-  bucket = (spec ? 0u : 8u) + (beff >= 8 ? 7u : beff - 1u);
+  bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
   return need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
 }
 
