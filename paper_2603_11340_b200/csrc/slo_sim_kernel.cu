@@ -108,9 +108,18 @@ __device__ __forceinline__ uint32_t accepted(const Group<G>& R, uint32_t u, uint
   return A;
 }
 
+// lanes per pending member for u = 1..32 pending members (floor(32/u)) and ceil(2^16 / L), so that
+// slot = (lane * recip) >> 16 = floor(lane / L) for every lane < 32
+__constant__ uint32_t kSegL[33] = {32, 32, 16, 10, 8, 6, 5, 4, 4, 3, 3, 2, 2, 2, 2, 2, 2,
+                                   1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+__constant__ uint32_t kSegRecip[33] = {2048, 2048, 4096, 6554, 8192, 10923, 13108, 16384, 16384, 21846, 21846,
+                                       32768, 32768, 32768, 32768, 32768, 32768, 65536, 65536, 65536, 65536,
+                                       65536, 65536, 65536, 65536, 65536, 65536, 65536, 65536, 65536, 65536,
+                                       65536, 65536};
+
 // Warp-pooled speculative step counts: every lane holding a speculative batch member
 // (`mine`: member of an active group with gamma > 0) is a pending item, whatever its group.  Each round the
-// u pending members get L = 32 / 2^ceil(log2 u) consecutive lanes of the whole warp; each lane computes one
+// u pending members get L = floor(32 / u) consecutive lanes of the whole warp; each lane computes one
 // Philox SPEC block (4 decode steps) of its member, a segmented scan of the block token sums finds the
 // block where the member's cumulative tokens reach O, and that lane resolves the exact step.  Members
 // that finish release their lanes to the others in the next round.  Blocks past a crossing are computed
@@ -124,13 +133,13 @@ __device__ __forceinline__ uint32_t spec_steps(const Group<G>* Rw, uint8_t* slot
   uint32_t pend = __ballot_sync(FULL, pending);
   while (pend) {
     const uint32_t u = __popc(pend);
-    const int lg = __clz(u - 1u) - 27;                 // log2 L, L = 32 / 2^ceil(log2 u)
-    const uint32_t L = 1u << lg;
+    const uint32_t L = kSegL[u];                       // floor(32 / u) lanes per pending member
     const uint32_t lowmask = FULL >> (32 - L);
     const uint32_t myslot = __popc(pend & lanemask_lt);
     if (pending) slots[myslot] = (uint8_t)lane;
     __syncwarp();
-    const uint32_t slot = (uint32_t)lane >> lg, off = (uint32_t)lane & (L - 1u);
+    const uint32_t slot = ((uint32_t)lane * kSegRecip[u]) >> 16;
+    const uint32_t off = (uint32_t)lane - slot * L;
     const bool active = slot < u;
     const int src = active ? slots[slot] : lane;
     __syncwarp();
@@ -174,8 +183,8 @@ __device__ __forceinline__ uint32_t spec_steps(const Group<G>* Rw, uint8_t* slot
       const uint32_t c = mcum + P - T;                 // tokens before this block
       give = 4u * mq + 1u + (c + e0 < mO) + (c + e0 + e1 < mO) + (c + e0 + e1 + e2 < mO);
     }
-    const uint32_t nc = __popc((cb >> ((myslot << lg) & 31u)) & lowmask);
-    const int from = (int)(((myslot + 1u) << lg) - (nc ? nc : 1u)) & 31;
+    const uint32_t nc = __popc((cb >> ((myslot * L) & 31u)) & lowmask);
+    const int from = (int)(((myslot + 1u) * L) - (nc ? nc : 1u)) & 31;
     const uint32_t got = __shfl_sync(FULL, give, from);
     if (pending) {
       if (nc) {
