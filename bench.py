@@ -201,13 +201,17 @@ def main():
     if rank == 0 or world == 1:
         __graft_entry__.build()
     if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # NCCL over NVLink/NVSwitch in production; SLO_BENCH_BACKEND=gloo lets several ranks share one GPU
+        # to exercise this code path on a single-GPU box (never used for a reported number)
+        backend = os.environ.get("SLO_BENCH_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
         dist.barrier()
         if rank != 0:
             __graft_entry__.build()
     from paper_2603_11340_b200 import inputs, sim
     from paper_2603_11340_b200._lib import STATS_DTYPE
 
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -254,7 +258,10 @@ def main():
             k1_end[i].record(stream)
         S.aggregate(out["detail"], n_cfg, n_seeds_local, out=agg, stream=stream)
         if world > 1:
-            dist.all_gather_into_tensor(parts, agg)                 # the one exchange
+            if dist.get_backend() == "nccl":
+                dist.all_gather_into_tensor(parts, agg)             # the one exchange
+            else:
+                dist.all_gather(list(parts.view(world, n_cfg, 32).unbind(0)), agg)
         if args.workload == "c4":                                    # K3 sums the per-rank parts itself
             S.hillclimb_step(space, sp, cands, parts if world > 1 else agg, world, state, stream=stream)
         elif world > 1:

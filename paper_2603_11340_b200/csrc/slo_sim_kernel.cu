@@ -321,10 +321,12 @@ __device__ __forceinline__ void generate(Group<G>& R, const DevWorkload* __restr
         pU = capacity(pD, R.rho[pstate]);
       }
     }
+    __syncwarp();   // every lane has read the phase state above
     if (bursty && li == 0) {
       R.pLam = pLam; R.pU = pU; R.pD = pD; R.pstart = pstart; R.ph = ph; R.pstate = pstate; R.nphase = nph;
     }
   }
+  __syncwarp();     // every lane has read R.last
   if (go && li == 0) R.last = newlast;
   if (valid) {
     const DevWorkload& W = wls[wl];
@@ -391,6 +393,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   bool active = false, exhausted = false;
 
   for (;;) {
+    __syncwarp();   // lanes of other groups read this group's record in the pooled decode: order before reuse
     // ---- acquire replicas for idle groups
     bool want = !active && !exhausted;
     while (__any_sync(FULL, want)) {
@@ -433,6 +436,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
       want = !active && !exhausted;
     }
     if (!__any_sync(FULL, active)) break;
+    __syncwarp();   // orders this iteration's ring reads/writes after the previous iteration's (ring reuse)
 
     // ---- (a2, a3) keep [h, h + G) generated (groups with room generate ahead to share the pass)
     bool need = active && gen < N && gen < h + G;
