@@ -262,9 +262,11 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                              slo_stats* d_stats, cudaStream_t st) {
   const uint32_t n_rep = (uint32_t)((uint64_t)n_configs * n_seeds);
   const uint32_t N = warmup_len + segment_len;
-  // replicas per launch chunk: the latency rows of a chunk stay within the budget (unless the caller
-  // provides the full latency buffer, which is then written in place)
-  uint64_t chunk = d_lat ? n_rep : h->lat_budget / ((uint64_t)N * 4u);
+  // replicas per launch chunk: the latency rows of a chunk stay within the budget (a caller-provided
+  // latency buffer is written in place, chunk by chunk)
+  // (K1 indexes a chunk's rows with 32-bit offsets: chunk * N < 2^31 elements)
+  uint64_t chunk = h->lat_budget / ((uint64_t)N * 4u);
+  if (chunk * N >= (1ull << 31)) chunk = ((1ull << 31) - 1) / N;
   if (chunk < 1) chunk = 1;
   if (chunk > n_rep) chunk = n_rep;
   slo_status s;

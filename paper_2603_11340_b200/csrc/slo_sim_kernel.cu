@@ -136,7 +136,7 @@ __device__ __forceinline__ uint32_t spec_steps(const Group<G>* Rw, uint8_t* slot
     const uint32_t L = kSegL[u];                       // floor(32 / u) lanes per pending member
     const uint32_t lowmask = FULL >> (32 - L);
     const uint32_t myslot = __popc(pend & lanemask_lt);
-    if (pending) slots[myslot] = (uint8_t)lane;
+    slots[pending ? myslot : 32u + (uint32_t)lane] = (uint8_t)lane;   // non-pending lanes: dummy slots
     __syncwarp();
     const uint32_t slot = ((uint32_t)lane * kSegRecip[u]) >> 16;
     const uint32_t off = (uint32_t)lane - slot * L;
@@ -340,11 +340,12 @@ __device__ __forceinline__ void generate(Group<G>& R, const DevWorkload* __restr
   __syncwarp();
 }
 
-// bitonic sort of u32 keys over the G lanes of each group (ascending)
-template <int G>
-__device__ __forceinline__ uint32_t gsort(uint32_t key, int li) {
+// bitonic sort of u32 keys over the first 2^LG lanes of each G-lane group (ascending)
+template <int G, int LG>
+__device__ __forceinline__ uint32_t gsort_n(uint32_t key, int li) {
+  constexpr int n = (1 << LG) < G ? (1 << LG) : G;
 #pragma unroll
-  for (int kk = 2; kk <= G; kk <<= 1) {
+  for (int kk = 2; kk <= n; kk <<= 1) {
 #pragma unroll
     for (int jj = kk >> 1; jj >= 1; jj >>= 1) {
       const uint32_t other = __shfl_xor_sync(FULL, key, jj, G);
@@ -354,6 +355,18 @@ __device__ __forceinline__ uint32_t gsort(uint32_t key, int li) {
     }
   }
   return key;
+}
+
+// inclusive prefix sum over the first 2^LG lanes of each G-lane group
+template <int G, int LG>
+__device__ __forceinline__ uint32_t gscan_n(uint32_t v, int li) {
+  constexpr int n = (1 << LG) < G ? (1 << LG) : G;
+#pragma unroll
+  for (int d = 1; d < n; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(FULL, v, d, G);
+    if (li >= d) v += o;
+  }
+  return v;
 }
 
 struct Counters {   // lane-local work counters (flushed to slo_stats)
@@ -386,7 +399,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   const uint32_t count = p.counts[cls];
   const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
 
-  uint32_t r = 0, h = 0, gen = 0;
+  uint32_t r = 0, h = 0, gen = 0, rowoff = 0;   // rowoff = (r - r_base) * N: this replica's latency row
   uint64_t t_idle = 0;
   uint32_t my_slo = 0;
   uint64_t my_sum = 0;
@@ -424,6 +437,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
               R.wl = k.workload;
             }
             setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
+            rowoff = (r - p.r_base) * N;           // < 2^32: a chunk's rows are capped by the scratch budget
             h = 0;
             gen = 0;
             t_idle = 0;
@@ -490,15 +504,22 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 
     // completion order = order of (S, member): at sorted position k,
     // sum_m' min(S_m', S_(k)) = sum_{i<k} S_(i) + (b - k) S_(k)
-    const uint32_t key = gsort<G>(member ? (S << 5) | (uint32_t)li : 0xFFFFFFFFu, li);
+    // only the first n = 2^ceil(log2 max b) lanes of each group hold members: a bitonic network on n
+    // lanes (the first stages of the G-lane network) sorts them, and the prefix sum needs log2 n steps
+    const uint32_t bmax = __reduce_max_sync(FULL, b);
+    const int lgn = bmax > 1 ? 32 - __clz(bmax - 1u) : 0;
+    uint32_t key = member ? (S << 5) | (uint32_t)li : 0xFFFFFFFFu;
+    uint32_t incl;
+    switch (lgn) {
+      case 0: incl = member ? key >> 5 : 0u; break;
+      case 1: key = gsort_n<G, 1>(key, li); incl = gscan_n<G, 1>(member ? key >> 5 : 0u, li); break;
+      case 2: key = gsort_n<G, 2>(key, li); incl = gscan_n<G, 2>(member ? key >> 5 : 0u, li); break;
+      case 3: key = gsort_n<G, 3>(key, li); incl = gscan_n<G, 3>(member ? key >> 5 : 0u, li); break;
+      case 4: key = gsort_n<G, 4>(key, li); incl = gscan_n<G, 4>(member ? key >> 5 : 0u, li); break;
+      default: key = gsort_n<G, 5>(key, li); incl = gscan_n<G, 5>(member ? key >> 5 : 0u, li); break;
+    }
     const uint32_t Sk = member ? key >> 5 : 0u;
     const uint32_t orig = key & 31u;
-    uint32_t incl = Sk;
-#pragma unroll
-    for (int d = 1; d < G; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(FULL, incl, d, G);
-      if (li >= d) incl += v;
-    }
     const uint32_t summin = incl - Sk + (b - (uint32_t)li) * Sk;
     const uint64_t cum = R.alpha0 * Sk + R.alpha1 * summin;
     const uint64_t c = t0 + (f * cum) / 1000000u;
@@ -516,7 +537,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
       my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
       my_sum += l;
     }
-    if (member) p.lat[(size_t)(r - p.r_base) * N + i] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
+    if (member) p.lat[rowoff + i] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
 
     // work counters, lane-local
     ct.steps += Sk;
@@ -559,7 +580,7 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
-  uint8_t* slots = wsmem + p.warp_bytes - 32;            // spec-decode slot map (last 32 B of the warp area)
+  uint8_t* slots = wsmem + p.warp_bytes - 64;            // spec-decode slot map (last 64 B of the warp area)
   Counters ct{0, 0, 0, 0};
   run_mode<8>(p, 0, wsmem, slots, lane, ct);
   run_mode<16>(p, 1, wsmem, slots, lane, ct);
@@ -581,7 +602,7 @@ size_t group_warp_bytes() {
   size_t m = 4 * sizeof(Group<8>);
   if (2 * sizeof(Group<16>) > m) m = 2 * sizeof(Group<16>);
   if (sizeof(Group<32>) > m) m = sizeof(Group<32>);
-  return m + 32;   // + spec-decode slot map
+  return m + 64;   // + spec-decode slot map (32 slots + 32 dummies)
 }
 
 // ------------------------------------------------------------------------------------------------
