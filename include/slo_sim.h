@@ -162,11 +162,18 @@ typedef struct {
   int32_t lo[5], hi[5], step[5];
 } slo_space;
 
-/* Eq. (2)-(3) and Alg. 1 parameters in fixed point.  Defaults: 5000, 10000, 10000, 20000, 20000. */
+/* Eq. (2)-(3) and Alg. 1 parameters in fixed point.  Live controller: 5000, 10000,
+ * 10000, 20000, 20000, w_W = w_k = 0, viol_mult 1, ema 0.  The paper's simulator controller (P:173-174,
+ * P:188) sets viol_mult = 10, w_W/w_k > 0 and ema_beta_q16 > 0. */
 typedef struct {
   int64_t lambda_milli, w_conc_micro, w_max_micro, w_spec_micro, delta_micro;
   uint32_t slo_us, strict_alg1;
-} slo_score_params;
+  int64_t w_W_micro, w_k_micro;   /* draft/verifier cost w_W*W + w_k*(k_max - gamma) when speculating */
+  uint32_t viol_mult;             /* violation term multiplier: 1 live, 10 simulator ("10 lambda")     */
+  uint32_t k_max;                 /* verifier-cadence reference of w_k (16)                             */
+  uint32_t ema_beta_q16;          /* EMA weight of the current point's p99 in Q16; 0 = raw p99          */
+  uint32_t reserved;              /* must be 0                                                          */
+} slo_score_params;             /* 80 B */
 
 typedef struct {
   slo_knobs K, K_best;
@@ -175,8 +182,9 @@ typedef struct {
   int32_t moved;                /* last step: 1 if K moved                                               */
   uint32_t argmax;              /* last step: index of K* among the candidates                           */
   uint32_t n_next;              /* number of valid candidates written for the next step                  */
-  uint32_t reserved;
-} slo_climb_state;              /* 96 B */
+  uint32_t has_ema;             /* ema_p99_us holds a value                                              */
+  uint64_t ema_p99_us;          /* EMA of the current point's seed-mean p99 (ema_beta_q16 > 0)           */
+} slo_climb_state;              /* 104 B */
 
 /* Host helper: neighbours of K, written to out[0..*n) (cap >= 31 recommended). */
 slo_status slo_neighbors(const slo_space* space, const slo_knobs* K, slo_knobs* out, uint32_t cap,

@@ -7,6 +7,10 @@ written from DESIGN.md §2.9 with Python's unbounded integers (no overflow reaso
 * score   — Eq. (3), PAPER.md:128-140; lambda = 5.0 (P:140).
 * neighbours — PAPER.md:142 (live stencil), S:83 (sim stencil), R21 (wide-32).
 * step    — Alg. 1; move rule P:142 / P:164.
+* simulator-controller variant: violation term x viol_mult (10 for the
+  simulator: "multiplying the violation term by 10 lambda"), draft/verifier cost w_W*W + w_k*(k_max - k)
+  added to Eq. (2) when speculation is on, and the current point judged by the EMA of its p99,
+  p_hat(t) = beta p99(t) + (1 - beta) p_hat(t-1) (beta in Q16, floor), started at the first sample.
 """
 from __future__ import annotations
 
@@ -30,20 +34,36 @@ def aggregate(results: Sequence[Dict]) -> Dict:
 
 
 def hw_cost_micro(k: Dict, sp: Dict) -> int:
-    """Eq. (2): w_conc*concurrency + w_max*max_num_seqs + w_spec*num_spec_tokens (0 when spec is off)."""
+    """Eq. (2): w_conc*concurrency + w_max*max_num_seqs + w_spec*num_spec_tokens (0 when spec is off),
+    plus the simulator's draft/verifier cost w_W*W + w_k*(k_max - k) when speculation is on."""
     gamma = k["draft_len"] if k["spec_on"] else 0
-    return sp["w_conc_micro"] * k["conc"] + sp["w_max_micro"] * k["max_num_seqs"] + sp["w_spec_micro"] * gamma
+    cost = sp["w_conc_micro"] * k["conc"] + sp["w_max_micro"] * k["max_num_seqs"] + sp["w_spec_micro"] * gamma
+    if gamma > 0:
+        cost += sp.get("w_W_micro", 0) * k["draft_width"] + sp.get("w_k_micro", 0) * (sp.get("k_max", 16) - gamma)
+    return cost
 
 
-def score_micro(agg: Dict, k: Dict, sp: Dict) -> int:
-    """Eq. (3) in micro-rps: goodput - lambda*max(0, p99 - SLO) - hw_cost, pooled over seeds (R17)."""
+def score_micro(agg: Dict, k: Dict, sp: Dict, p99_ema_us=None) -> int:
+    """Eq. (3) in micro-rps: goodput - m*lambda*max(0, p99 - SLO) - hw_cost, pooled over seeds (R17).
+    With p99_ema_us the violation uses that EMA value (integer us) instead of the seed-mean p99."""
     n = agg["n_seeds"]
     if n == 0 or (agg["flags"] & 1):
         return INT64_MIN
+    mult = sp.get("viol_mult", 1)
     goodput = (agg["sum_slo_met"] * 10**12) // agg["sum_window_us"]
-    excess = max(0, agg["sum_p99_us"] - n * sp["slo_us"])
-    penalty = (sp["lambda_milli"] * excess) // (1000 * n)
+    if p99_ema_us is None:
+        excess = max(0, agg["sum_p99_us"] - n * sp["slo_us"])
+        penalty = (mult * sp["lambda_milli"] * excess) // (1000 * n)
+    else:
+        penalty = (mult * sp["lambda_milli"] * max(0, p99_ema_us - sp["slo_us"])) // 1000
     return goodput - penalty - hw_cost_micro(k, sp)
+
+
+def ema_update(prev, sample: int, beta_q16: int) -> int:
+    """p_hat(t) = beta p99(t) + (1 - beta) p_hat(t-1) in integer us (floor); the first sample starts it."""
+    if prev is None:
+        return sample
+    return (beta_q16 * sample + (65536 - beta_q16) * prev) >> 16
 
 
 def _clamp(v: int, lo: int, hi: int) -> int:
@@ -104,15 +124,24 @@ def step(state: Dict, cands: Sequence[Dict], aggs: Sequence[Dict], sp: Dict) -> 
     """One Alg. 1 iteration given measured candidates [K, neighbours...] (cands[0] == state['K']).
 
     Returns (new_state, moved, argmax_index, scores)."""
-    scores = [score_micro(a, c, sp) for a, c in zip(aggs, cands)]
     st = dict(state)
+    beta = sp.get("ema_beta_q16", 0)
+    ema = None
+    a0 = aggs[0]
+    if beta and a0["n_seeds"] > 0 and not (a0["flags"] & 1):
+        ema = ema_update(st.get("ema") if st.get("has_ema") else None, a0["sum_p99_us"] // a0["n_seeds"], beta)
+        st["ema"], st["has_ema"] = ema, 1
+    scores = [score_micro(a, c, sp, ema if i == 0 else None) for i, (a, c) in enumerate(zip(aggs, cands))]
     s0 = scores[0]
     if not st["has_best"] or s0 > st["S_best"]:
         st["S_best"], st["K_best"], st["has_best"] = s0, cands[0], 1
     moved, idx = False, 0
     if len(cands) > 1:
         idx = max(range(1, len(cands)), key=lambda i: (scores[i], -i))
-        violated = aggs[0]["n_seeds"] > 0 and aggs[0]["sum_p99_us"] > aggs[0]["n_seeds"] * sp["slo_us"]
+        if ema is not None:
+            violated = ema > sp["slo_us"]
+        else:
+            violated = a0["n_seeds"] > 0 and a0["sum_p99_us"] > a0["n_seeds"] * sp["slo_us"]
         moved = decide_move(s0, violated, scores[idx], sp["delta_micro"])
         if not sp["strict_alg1"] and scores[idx] > st["S_best"]:
             st["S_best"], st["K_best"] = scores[idx], cands[idx]
@@ -122,4 +151,4 @@ def step(state: Dict, cands: Sequence[Dict], aggs: Sequence[Dict], sp: Dict) -> 
 
 
 def initial_state(k0: Dict) -> Dict:
-    return dict(K=dict(k0), K_best=dict(k0), S_best=INT64_MIN, step=0, has_best=0)
+    return dict(K=dict(k0), K_best=dict(k0), S_best=INT64_MIN, step=0, has_best=0, ema=0, has_ema=0)

@@ -72,7 +72,9 @@ class slo_space(C.Structure):
 class slo_score_params(C.Structure):
     _fields_ = [("lambda_milli", C.c_int64), ("w_conc_micro", C.c_int64), ("w_max_micro", C.c_int64),
                 ("w_spec_micro", C.c_int64), ("delta_micro", C.c_int64), ("slo_us", C.c_uint32),
-                ("strict_alg1", C.c_uint32)]
+                ("strict_alg1", C.c_uint32), ("w_W_micro", C.c_int64), ("w_k_micro", C.c_int64),
+                ("viol_mult", C.c_uint32), ("k_max", C.c_uint32), ("ema_beta_q16", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 # numpy views of the 32-byte PODs (little-endian)
@@ -88,9 +90,9 @@ STATS_DTYPE = np.dtype([("requests", "<u8"), ("batches", "<u8"), ("decode_steps"
                         ("reserved", "<u8", (2,))])
 CLIMB_DTYPE = np.dtype([("K", KNOB_DTYPE), ("K_best", KNOB_DTYPE), ("S_best_micro", "<i8"), ("step", "<u4"),
                         ("has_best", "<u4"), ("moved", "<i4"), ("argmax", "<u4"), ("n_next", "<u4"),
-                        ("reserved", "<u4")])
+                        ("has_ema", "<u4"), ("ema_p99_us", "<u8")])
 assert KNOB_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 32 and AGG_DTYPE.itemsize == 32
-assert STATS_DTYPE.itemsize == 64 and CLIMB_DTYPE.itemsize == 96
+assert STATS_DTYPE.itemsize == 64 and CLIMB_DTYPE.itemsize == 104
 
 _lib = None
 vp = C.c_void_p

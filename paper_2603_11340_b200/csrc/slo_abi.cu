@@ -16,7 +16,8 @@ static_assert(sizeof(slo_config_agg) == 32, "slo_config_agg must be 32 B");
 static_assert(sizeof(slo_stats) == 64, "slo_stats must be 64 B");
 static_assert(sizeof(slo_timing) == 40, "slo_timing must be 40 B");
 static_assert(sizeof(slo_arrivals) == 40, "slo_arrivals must be 40 B");
-static_assert(sizeof(slo_climb_state) == 96, "slo_climb_state must be 96 B");
+static_assert(sizeof(slo_climb_state) == 104, "slo_climb_state must be 104 B");
+static_assert(sizeof(slo_score_params) == 80, "slo_score_params must be 80 B");
 
 struct slo_sim {
   int device = 0;
@@ -437,7 +438,8 @@ slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_scor
   if (!h) return fail(nullptr, SLO_E_INVAL, "hillclimb_step: null handle");
   if (!space_ok(space) || !sp || !d_cands || !d_aggs || !d_state || n_cand == 0 || n_cand > 32 || n_parts == 0)
     return fail(h, SLO_E_INVAL, "hillclimb_step: bad arguments");
-  if (sp->lambda_milli < 0 || sp->delta_micro < 0) return fail(h, SLO_E_INVAL, "hillclimb_step: negative weight");
+  if (sp->lambda_milli < 0 || sp->delta_micro < 0 || sp->viol_mult < 1 || sp->ema_beta_q16 > 65536 || sp->reserved)
+    return fail(h, SLO_E_INVAL, "hillclimb_step: bad score parameters");
   DeviceGuard g(h->device);
   slo::slo_climb_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*space, *sp, d_cands, n_cand, d_aggs, n_parts, d_state,
                                                             d_scores);

@@ -137,18 +137,29 @@ __host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& 
 // ------------------------------------------------------------------------------------------------
 // K3: one warp; lane k scores candidate k (Eq. 3), warp argmax, Alg. 1 move + best, next stencil.
 // ------------------------------------------------------------------------------------------------
-__device__ static inline int64_t score_micro(const slo_config_agg& a, const slo_knobs& k,
-                                             const slo_score_params& sp) {
+__device__ static inline int64_t hw_cost_micro(const slo_knobs& k, const slo_score_params& sp) {
+  const int64_t gamma = k.spec_on ? k.draft_len : 0;
+  int64_t hw = sp.w_conc_micro * k.conc + sp.w_max_micro * k.max_num_seqs + sp.w_spec_micro * gamma;
+  if (gamma > 0) hw += sp.w_W_micro * k.draft_width + sp.w_k_micro * ((int64_t)sp.k_max - gamma);
+  return hw;
+}
+
+// Eq. (3) in micro-rps; `ema` >= 0 replaces the seed-mean p99 of the violation term (current point of the
+// simulator controller); the violation term is multiplied by viol_mult (10 lambda).
+__device__ static inline int64_t score_micro(const slo_config_agg& a, const slo_knobs& k, const slo_score_params& sp,
+                                             int64_t ema) {
   if (a.n_seeds == 0 || (a.flags & 1u) || a.sum_window_us == 0) return INT64_MIN;
   const unsigned __int128 gp = ((unsigned __int128)a.sum_slo_met * 1000000000000ull) / a.sum_window_us;
-  const unsigned __int128 bound = (unsigned __int128)a.n_seeds * sp.slo_us;
   unsigned __int128 pen = 0;
-  if ((unsigned __int128)a.sum_p99_us > bound)
-    pen = ((unsigned __int128)sp.lambda_milli * ((unsigned __int128)a.sum_p99_us - bound)) /
-          ((unsigned __int128)1000u * a.n_seeds);
-  const int64_t gamma = k.spec_on ? k.draft_len : 0;
-  const int64_t hw = sp.w_conc_micro * k.conc + sp.w_max_micro * k.max_num_seqs + sp.w_spec_micro * gamma;
-  return (int64_t)gp - (int64_t)pen - hw;
+  const unsigned __int128 lam = (unsigned __int128)sp.lambda_milli * sp.viol_mult;
+  if (ema >= 0) {
+    if ((uint64_t)ema > sp.slo_us) pen = (lam * ((uint64_t)ema - sp.slo_us)) / 1000u;
+  } else {
+    const unsigned __int128 bound = (unsigned __int128)a.n_seeds * sp.slo_us;
+    if ((unsigned __int128)a.sum_p99_us > bound)
+      pen = (lam * ((unsigned __int128)a.sum_p99_us - bound)) / ((unsigned __int128)1000u * a.n_seeds);
+  }
+  return (int64_t)gp - (int64_t)pen - hw_cost_micro(k, sp);
 }
 
 __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs* cands, uint32_t n_cand,
@@ -159,6 +170,7 @@ __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs
   slo_knobs mine{};
   slo_config_agg a{0, 0, 0, 0, 0};
   int64_t s = INT64_MIN;
+  int64_t ema_new = -1;
   if ((uint32_t)lane < n_cand) {
     mine = cands[lane];
     for (uint32_t p = 0; p < n_parts; ++p) {
@@ -169,8 +181,17 @@ __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs
       a.n_seeds += x.n_seeds;
       a.flags |= x.flags;
     }
-    s = score_micro(a, mine, sp);
+    int64_t ema = -1;
+    if (lane == 0 && sp.ema_beta_q16 > 0 && a.n_seeds > 0 && !(a.flags & 1u)) {  // EMA of p99
+      const uint64_t sample = a.sum_p99_us / a.n_seeds;
+      const slo_climb_state& st0 = *state;
+      ema = st0.has_ema ? (int64_t)((sp.ema_beta_q16 * (unsigned __int128)sample +
+                                     (65536u - sp.ema_beta_q16) * (unsigned __int128)st0.ema_p99_us) >> 16)
+                        : (int64_t)sample;
+    }
+    s = score_micro(a, mine, sp, ema);
     if (scores) scores[lane] = s;
+    if (lane == 0) ema_new = ema;
   }
   // argmax over k >= 1, lowest index on ties
   int64_t bs = (lane >= 1 && (uint32_t)lane < n_cand) ? s : INT64_MIN;
@@ -199,10 +220,15 @@ __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs
     }
     int moved_ = 0;
     uint32_t idx = 0;
+    if (ema_new >= 0) {
+      st.ema_p99_us = (uint64_t)ema_new;
+      st.has_ema = 1;
+    }
     if (n_cand > 1) {
       idx = (uint32_t)bi;
       const __int128 diff = (__int128)bs - (__int128)s0;
-      const bool violated = n0 > 0 && (unsigned __int128)p99sum0 > (unsigned __int128)n0 * sp.slo_us;
+      const bool violated = ema_new >= 0 ? (uint64_t)ema_new > sp.slo_us
+                                         : n0 > 0 && (unsigned __int128)p99sum0 > (unsigned __int128)n0 * sp.slo_us;
       moved_ = (diff >= (__int128)sp.delta_micro) || (violated && bs > s0);
       if (!sp.strict_alg1 && bs > st.S_best_micro) {
         st.S_best_micro = bs;

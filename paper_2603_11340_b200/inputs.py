@@ -228,7 +228,11 @@ SPACE_WIDE32 = dict(stencil=2, lo=[1, 1, 0, 1, 0], hi=[32, 32, 16, 4, 50_000], s
 K0 = knobs(conc=8, max_num_seqs=8, draft_len=8, spec_on=1, accept_q16=q16(0.5))   # Alg. 1 init
 
 SCORE_DEFAULTS = dict(lambda_milli=5000, w_conc_micro=10_000, w_max_micro=10_000, w_spec_micro=20_000,
-                      delta_micro=20_000, slo_us=1_200_000, strict_alg1=1)
+                      delta_micro=20_000, slo_us=1_200_000, strict_alg1=1, viol_mult=1, k_max=16,
+                      w_W_micro=0, w_k_micro=0, ema_beta_q16=0)
+# the paper's simulator controller: 10 lambda violation term,
+# draft/verifier cost, EMA(beta = 0.5) of the current point's p99
+SCORE_SIM = dict(SCORE_DEFAULTS, viol_mult=10, w_W_micro=20_000, w_k_micro=5_000, ema_beta_q16=32768)
 
 
 def config_c4(n_seeds=128, segment_len=5000) -> Config:

@@ -75,8 +75,9 @@ def space_struct(space: Dict) -> slo_space:
 
 def score_struct(sp: Dict) -> slo_score_params:
     s = slo_score_params()
+    defaults = dict(w_W_micro=0, w_k_micro=0, viol_mult=1, k_max=16, ema_beta_q16=0, reserved=0)
     for f, _ in slo_score_params._fields_:
-        setattr(s, f, sp[f])
+        setattr(s, f, sp.get(f, defaults.get(f)))
     return s
 
 

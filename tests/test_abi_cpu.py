@@ -94,4 +94,4 @@ def test_pod_layouts(L):
     assert C.sizeof(L.slo_timing) == 40
     assert C.sizeof(L.slo_arrivals) == 40
     assert C.sizeof(L.slo_space) == 64
-    assert C.sizeof(L.slo_score_params) == 48
+    assert C.sizeof(L.slo_score_params) == 80

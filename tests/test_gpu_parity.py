@@ -214,13 +214,17 @@ def test_aggregate_kernels(S, orc):
     s.close()
 
 
-def test_device_climb_matches_oracle(S, orc):
-    """K3 (score, argmax, move, best-so-far, next stencil) over several Alg. 1 steps, against oracle/climb.py
-    fed with oracle replicas: identical scores, moves and trajectories (C4-shaped, reduced sizes)."""
+@pytest.mark.parametrize("variant", ["live-wide32", "sim-controller", "sim-space"])
+def test_device_climb_matches_oracle(S, orc, variant):
+    """K3 (score, argmax, move, best-so-far, EMA, next stencil) over several Alg. 1 steps, against
+    oracle/climb.py fed with oracle replicas: identical scores, moves and trajectories (C4-shaped, reduced
+    sizes); also the paper's simulator controller (10 lambda, draft/verifier cost, EMA p99: P:173-174)."""
     from oracle import climb
     from paper_2603_11340_b200._lib import CLIMB_DTYPE
     wls = [inputs.preset_ll()]
-    space, sp = inputs.SPACE_WIDE32, dict(inputs.SCORE_DEFAULTS)
+    space, sp = {"live-wide32": (inputs.SPACE_WIDE32, dict(inputs.SCORE_DEFAULTS)),
+                 "sim-controller": (inputs.SPACE_WIDE32, dict(inputs.SCORE_SIM)),
+                 "sim-space": (inputs.SPACE_SIM, dict(inputs.SCORE_SIM, strict_alg1=0))}[variant]
     n_seeds, N, n_cand = 4, 400, 32
     seeds = inputs.seeds(n_seeds, 31)
     s = S.Simulator(wls, device=0)
@@ -245,6 +249,7 @@ def test_device_climb_matches_oracle(S, orc):
         assert S.unpack_knobs(st["K"])[0] == ost["K"]
         assert int(st["S_best_micro"]) == ost["S_best"]
         assert S.unpack_knobs(st["K_best"])[0] == ost["K_best"]
+        assert int(st["has_ema"]) == int(ost["has_ema"]) and int(st["ema_p99_us"]) == int(ost["ema"])
         ocands = [ost["K"]] + climb.neighbours(space, ost["K"])
         ocands += [inputs.PAD_KNOBS] * (n_cand - len(ocands))
         assert S.unpack_knobs(cands_t.cpu().numpy())[: int(st["n_next"])] == ocands[: int(st["n_next"])]

@@ -104,3 +104,63 @@ def test_climb_converges_on_concave_surface():
         st, moved, idx, scores = climb.step(st, cands, aggs, sp)
     assert st["K"]["conc"] == 10
     assert st["K_best"]["conc"] in (8, 10)   # strict Alg. 1: best only from measured current points
+
+
+# ---------------------------------------------------------------------------------------------------
+# simulator-controller variant (NEXT-3: P:173-174 EMA, P:188 10-lambda violation + draft/verifier cost)
+# ---------------------------------------------------------------------------------------------------
+def test_sim_violation_is_ten_lambda():
+    """goodput 1.29, p99 1.30, SLO 1.2, lambda 5 -> violation 10*5*0.10 = 5.0; and the sim
+    penalty is exactly 10x the live one."""
+    k = inputs.knobs(conc=8, max_num_seqs=8, draft_len=0, spec_on=0)
+    agg = _agg_for(1.29, 1.30)
+    live = climb.score_micro(agg, k, SP)
+    sim = climb.score_micro(agg, k, dict(SP, viol_mult=10))
+    assert live == 1_290_000 - 500_000 - 160_000
+    assert sim == 1_290_000 - 5_000_000 - 160_000
+    assert (1_290_000 - 160_000 - sim) == 10 * (1_290_000 - 160_000 - live)
+    # S:220: no violation -> goodput - hw cost only
+    assert climb.score_micro(_agg_for(1.29, 1.10), k, dict(SP, viol_mult=10)) == 1_290_000 - 160_000
+
+
+def test_sim_draft_verifier_cost_monotone():
+    """equal goodput and p99, larger W -> strictly lower score; sparser verification (larger k)
+    costs less; the terms vanish with speculation off."""
+    sp = dict(inputs.SCORE_SIM)
+    agg = _agg_for(10.0, 1.0)
+    base = inputs.knobs(conc=8, max_num_seqs=8, draft_len=8, spec_on=1, draft_width=1)
+    s1 = climb.score_micro(agg, base, sp)
+    s2 = climb.score_micro(agg, dict(base, draft_width=2), sp)
+    assert s1 - s2 == sp["w_W_micro"]
+    s_k4 = climb.score_micro(agg, dict(base, draft_len=4), sp)
+    assert s_k4 - s1 == 4 * sp["w_spec_micro"] - 4 * sp["w_k_micro"]
+    off = dict(base, spec_on=0)
+    assert climb.score_micro(agg, off, sp) == climb.score_micro(agg, off, SP)
+
+
+def test_ema_examples():
+    """S:153-155 / S:442: EMA 1.4 then 1.0 at beta .5 -> 1.2; 1.5, beta .3, sample 1.0 -> 1.35."""
+    e = climb.ema_update(None, 1_400_000, 32768)
+    assert e == 1_400_000
+    assert climb.ema_update(e, 1_000_000, 32768) == 1_200_000
+    e3 = climb.ema_update(1_500_000, 1_000_000, int(round(0.3 * 65536)))
+    assert abs(e3 - 1_350_000) <= 2          # Q16 beta (0.3 -> 19661/65536) and the floor
+    # stays inside the hull of the samples
+    x = None
+    for v in (900_000, 1_800_000, 1_100_000, 1_300_000):
+        x = climb.ema_update(x, v, 20000)
+        assert 900_000 <= x <= 1_800_000
+
+
+def test_sim_controller_uses_ema_for_the_move():
+    """With the EMA below the SLO while the raw p99 violates it, a small improvement no longer escapes."""
+    sp = dict(inputs.SCORE_SIM)
+    k0 = inputs.knobs(conc=8, max_num_seqs=8, draft_len=8, spec_on=1)
+    st = climb.initial_state(k0)
+    st["ema"], st["has_ema"] = 800_000, 1
+    cands = [k0, dict(k0, conc=10)]
+    a0 = _agg_for(10.0, 1.30)           # raw p99 violates; EMA = (1.3 + 0.8)/2 = 1.05 s does not
+    a1 = dict(a0)
+    a1["sum_slo_met"] += 0              # identical measurements: neighbour differs only by hw cost
+    st2, moved, idx, scores = climb.step(st, cands, [a0, a1], sp)
+    assert st2["ema"] == 1_050_000 and not moved
