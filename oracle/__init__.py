@@ -67,7 +67,7 @@ class Knobs(C.Structure):
 class Result(C.Structure):
     _fields_ = [("p99_us", C.c_uint32), ("slo_met", C.c_uint32), ("n_measured", C.c_uint32),
                 ("flags", C.c_uint32), ("window_us", C.c_uint64), ("sum_latency_us", C.c_uint64),
-                ("goodput", C.c_double)]
+                ("goodput", C.c_double), ("p50_us", C.c_uint32), ("p95_us", C.c_uint32)]
 
 
 class Counters(C.Structure):
@@ -105,7 +105,7 @@ def lib():
                               C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Result),
                               C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
         L.orc_run_trace.argtypes = [C.POINTER(Timing), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
-                                    C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                                    C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32, C.POINTER(Result),
                                     C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
@@ -202,6 +202,7 @@ def request_draws(workloads: Sequence[Dict], knobs: Dict, seed: int, n: int, crn
 def _pack(res: Result, cnt: Counters, lat, trace) -> Dict:
     out = dict(p99_us=res.p99_us, slo_met=res.slo_met, n_measured=res.n_measured, flags=res.flags,
                window_us=res.window_us, sum_latency_us=res.sum_latency_us, goodput=res.goodput,
+               p50_us=res.p50_us, p95_us=res.p95_us,
                counters=dict(philox_blocks=cnt.philox_blocks, batches=cnt.batches,
                              decode_steps=cnt.decode_steps, member_steps=cnt.member_steps))
     if lat is not None:
@@ -230,7 +231,8 @@ def run(workloads: Sequence[Dict], knobs: Dict, seed: int, segment_len: int, war
 
 def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_us: int,
               a: Sequence[int], P: Sequence[int], O: Sequence[int], f: Optional[Sequence[int]] = None,
-              A: Optional[Sequence[Sequence[int]]] = None, warmup_len: int = 0, slo_us: int = 1_200_000) -> Dict:
+              A: Optional[Sequence[Sequence[int]]] = None, warmup_len: int = 0, slo_us: int = 1_200_000,
+              issue_origin: int = 0) -> Dict:
     """Trace mode: explicit requests (a, P, O), per-request noise factor f (ppm) and accepted-prefix draws."""
     n = len(a)
     tm = Timing(**timing)
@@ -249,7 +251,8 @@ def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_u
     res, cnt = Result(), Counters()
     lat = np.zeros(n, np.uint32)
     tr = (Req * n)()
-    rc = lib().orc_run_trace(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, n, a_, P_, O_, f_, off_, val_,
+    rc = lib().orc_run_trace(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, issue_origin, n, a_, P_, O_, f_,
+                             off_, val_,
                              warmup_len, slo_us, C.byref(res), lat.ctypes.data_as(C.POINTER(C.c_uint32)), tr,
                              C.byref(cnt))
     if rc != 0:

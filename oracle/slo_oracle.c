@@ -190,7 +190,9 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
     uint32_t w[4];
     block(k0, k1, i, 0, 0, w);
     uint64_t E = orc_exp_q32(w[0]);
-    if (kind == 0) {
+    if (kind == 3) {           /* closed loop, zero think time: every request is waiting from t = 0 */
+      a[i] = 0;
+    } else if (kind == 0) {
       uint64_t gap = (uint64_t)(((u128)E * g[0]) >> 48);
       a[i] = prev + gap;
       prev = a[i];
@@ -218,7 +220,7 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
     O[i] = orc_length(W->output_cw, W->output_ncw, W->output_lo, w[2]);
     w3[i] = w[3];
   }
-  return (int)(kind != 0 ? p + 1 : 0); /* number of phases drawn (kind 1 consumes one block each) */
+  return (int)((kind == 1 || kind == 2) ? p + 1 : 0); /* phases drawn (kind 1 consumes one block each) */
 }
 
 /* ---------------------------------------------------------------------------------------------- */
@@ -258,7 +260,7 @@ static int cmp_u32(const void* x, const void* y) {
   return (a > b) - (a < b);
 }
 
-static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t mw,
+static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t mw, uint32_t issue_origin,
                     uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
                     const uint32_t* f, adraw* ad, uint32_t warmup, uint32_t slo_us,
                     orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
@@ -356,12 +358,13 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
     }
   }
 
-  /* outputs */
+  /* outputs; latency from arrival (open loop, R2) or from issue (closed loop, §2.11) */
+  const uint64_t* origin = issue_origin ? s : a;
   uint32_t n = N - warmup;
   uint32_t slo_met = 0, flags = 0;
   uint64_t sum = 0, cmax = 0;
   for (uint32_t i = 0; i < N; ++i) {
-    uint64_t l = c[i] - a[i];
+    uint64_t l = c[i] - origin[i];
     lat[i] = l > U32MAX ? U32MAX : (uint32_t)l;
     if (i >= warmup) {
       if (l > U32MAX) flags |= 2u;
@@ -376,10 +379,12 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
   qsort(sorted, n, sizeof(uint32_t), cmp_u32);
   uint32_t r = (uint32_t)((99ull * n + 99ull) / 100ull); /* nearest rank, ceil(0.99 n) */
   res->p99_us = sorted[r - 1];
+  res->p50_us = sorted[(uint32_t)((50ull * n + 99ull) / 100ull) - 1];   /* ceil(0.50 n) */
+  res->p95_us = sorted[(uint32_t)((95ull * n + 99ull) / 100ull) - 1];   /* ceil(0.95 n) */
   res->slo_met = slo_met;
   res->n_measured = n;
   res->flags = flags;
-  uint64_t T = cmax - a[warmup];
+  uint64_t T = cmax - origin[warmup];
   res->window_us = T < 1 ? 1 : T;
   res->sum_latency_us = sum;
   res->goodput = (double)((uint64_t)slo_met * 1000000ull) / (double)res->window_us;
@@ -445,7 +450,7 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
   orc_thresholds(k->accept_q16, k->draft_width, gamma, T);
   uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
   adraw ad = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, T, NULL, NULL, 0};
-  int rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, N, a, P, O, f, &ad,
+  int rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, W->arr.kind == 3, N, a, P, O, f, &ad,
                     warmup_len, slo_us, res, latencies, trace, cnt);
   if (cnt) cnt->philox_blocks += N + (W->arr.kind == 1 ? (uint64_t)phases : 0);
   free(a); free(P); free(O); free(w3); free(f);
@@ -453,7 +458,7 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
 }
 
 int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
-                  uint32_t max_wait_us, uint32_t n, const uint64_t* a, const uint32_t* P,
+                  uint32_t max_wait_us, uint32_t issue_origin, uint32_t n, const uint64_t* a, const uint32_t* P,
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
@@ -466,6 +471,6 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
     if (O[i] < 1) return -1;
   if (cnt) memset(cnt, 0, sizeof(*cnt));
   adraw ad = {0, 0, 0, NULL, A_off, A_val, 0};
-  return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, n, a, P, O, f, &ad, warmup_len,
+  return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, warmup_len,
                   slo_us, res, latencies, trace, cnt);
 }

@@ -14,7 +14,8 @@ extern "C" {
 #endif
 
 typedef struct {
-  uint32_t kind;              /* 0 Poisson, 1 MMPP-2 (exponential sojourns), 2 on/off (fixed sojourns) */
+  uint32_t kind;              /* 0 Poisson, 1 MMPP-2 (exponential sojourns), 2 on/off (fixed sojourns),
+                                 3 closed loop: C users, zero think time (every a_i = 0, latency from issue) */
   uint32_t start_state;
   uint64_t mean_gap_q16[2];   /* Q48.16 us; UINT64_MAX = no arrivals in that state */
   uint64_t mean_sojourn_us[2];
@@ -45,6 +46,7 @@ typedef struct {
   uint32_t p99_us, slo_met, n_measured, flags;
   uint64_t window_us, sum_latency_us;
   double goodput;           /* (double)(slo_met * 10^6) / (double)window_us, Eq. (1) */
+  uint32_t p50_us, p95_us;  /* nearest-rank p50 and p95 */
 } orc_result;
 
 typedef struct {
@@ -86,7 +88,7 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
  * the request heads a batch), and per-request accepted-prefix draws A_val[A_off[i] + j] for decode step
  * j of request i (A_off has n+1 entries).  gamma_eff is given directly. */
 int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
-                  uint32_t max_wait_us, uint32_t n, const uint64_t* a, const uint32_t* P,
+                  uint32_t max_wait_us, uint32_t issue_origin, uint32_t n, const uint64_t* a, const uint32_t* P,
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);

@@ -124,6 +124,14 @@ def preset_sim(rate=12.0, stream_id=0) -> Dict:
                     timing=SIM_TIMING, stream_id=stream_id)
 
 
+def preset_closed(stream_id=0) -> Dict:
+    """CLOSED: the paper's live client: a single replayed prompt, 64-token output cap and a
+    closed loop of `conc` users with zero think time (arrival kind 3); latency from issue."""
+    w = preset_ll(stream_id=stream_id)
+    w["arrivals"]["kind"] = 3
+    return w
+
+
 def preset_stress(rate=10.0, stream_id=0, kind=1) -> Dict:
     """STRESS: LL lengths x1.5, MMPP-2 with lambda_H = 1.8 rate, lambda_L = 0.2 rate, 2 s sojourns."""
     return workload(kind=kind, prompt=point_mass(60),

@@ -352,3 +352,65 @@ def test_p99_nearest_rank_examples():
     assert nearest_rank([7], 99, 100) == 7
     assert nearest_rank([3, 1, 2], 1, 2) == 2
     assert nearest_rank([500] * 99 + [5000], 99, 100) == 500   # R23: S:145 contradicts S:123
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-1: closed-loop clients (kind 3, zero think time, latency from issue) and p50 / p95
+# ------------------------------------------------------------------------------------------------
+def _closed(P=40, O=64, noise=0):
+    w = inputs.preset_closed()
+    w["prompt"] = inputs.point_mass(P)
+    w["output"] = inputs.point_mass(O)
+    w["timing"] = dict(inputs.LL_TIMING, noise_step_ppm=noise)
+    return w
+
+
+@pytest.mark.parametrize("C,B", [(4, 8), (8, 8), (8, 2), (12, 4), (16, 16)])
+def test_closed_loop_closed_form(orc, C, B):
+    """Deterministic service, C users, zero think time: batches of b = min(B, C) run back to back, each
+    taking D = pre_base + pre_tok P + O (dec_base + dec_seq b).  The first C requests (all issued at 0) wait
+    for floor(i/b) batches; afterwards, with C a multiple of b, every request waits C/b - 1 batches, so its
+    latency from issue is (C/b) D and the throughput is b/D (Little's law for a closed system: C = X R)."""
+    tm = inputs.LL_TIMING
+    b = min(B, C)
+    D = tm["pre_base_us"] + tm["pre_tok_us"] * 40 + 64 * (tm["dec_base_us"] + tm["dec_seq_us"] * b)
+    N = 40 * C
+    r = orc.run([_closed()], inputs.knobs(conc=C, max_num_seqs=B), 7, N, latencies=True, trace=True)
+    lat = r["latencies"].astype(np.int64)
+    assert np.all(lat[:C] == (np.arange(C) // b + 1) * D)
+    assert np.all(lat[C:] == (C // b) * D)
+    assert r["p50_us"] == r["p95_us"] == r["p99_us"] == (C // b) * D
+    assert r["window_us"] == (N // b) * D                 # first issue at 0, last completion after N/b batches
+    tr = r["trace"]
+    assert np.all(tr["a"] == 0) and np.all(tr["s"][:C] == 0)
+
+
+def test_closed_loop_matches_brute_force(orc):
+    """Trace mode with every a_i = 0 and issue-origin latencies equals the per-microsecond brute force."""
+    rng = random.Random(77)
+    for case in range(60):
+        gamma = rng.choice([0, 0, 2])
+        tm = dict(pre_base_us=rng.randrange(0, 5), pre_tok_us=rng.randrange(0, 4), dec_base_us=rng.randrange(1, 12),
+                  dec_seq_us=rng.randrange(0, 4), dr_base_us=rng.randrange(0, 4), dr_seq_us=rng.randrange(0, 2),
+                  ver_base_us=rng.randrange(0, 8), ver_seq_us=rng.randrange(0, 3), ver_tok_us=rng.randrange(0, 2),
+                  noise_step_ppm=0)
+        n = rng.randrange(1, 12)
+        _, P, O, f, A = _random_trace(rng, n, gamma)
+        a = [0] * n
+        C, B = rng.randrange(1, 6), rng.randrange(1, 6)
+        s_bf, c_bf = brute_force(tm, C, B, gamma, 0, a, P, O, f, A)
+        r = orc.run_trace(tm, C, B, gamma, 0, a, P, O, f=f, A=A if gamma else None, issue_origin=1)
+        assert list(r["latencies"]) == [c - s for c, s in zip(c_bf, s_bf)]
+
+
+def test_percentiles_nearest_rank(orc):
+    """p50 / p95 / p99 are the ceil(q n)-th smallest measured latencies, monotone in q."""
+    for k, wl in ((inputs.knobs(conc=8, max_num_seqs=4, draft_len=4, spec_on=1), inputs.preset_ll()),
+                  (inputs.knobs(conc=6, max_num_seqs=3), inputs.preset_closed()),
+                  (inputs.knobs(conc=12, max_num_seqs=6), inputs.preset_stress())):
+        for n, w in ((1, 0), (7, 3), (100, 0), (1999, 17)):
+            r = orc.run([wl], k, 5, n, warmup_len=w, latencies=True)
+            srt = np.sort(r["latencies"][w:])
+            for key, q in (("p50_us", 50), ("p95_us", 95), ("p99_us", 99)):
+                assert r[key] == srt[(q * n + 99) // 100 - 1]
+            assert r["p50_us"] <= r["p95_us"] <= r["p99_us"]
