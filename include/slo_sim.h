@@ -54,7 +54,9 @@ typedef struct {
 
 /* Arrival process. */
 typedef struct {
-  uint32_t kind;                /* 0 Poisson, 1 MMPP-2 (exponential sojourns), 2 on/off (fixed sojourns) */
+  uint32_t kind;                /* 0 Poisson, 1 MMPP-2 (exponential sojourns), 2 on/off (fixed sojourns), */
+                                /* 3 closed loop: `conc` users with zero think time — every request is    */
+                                /*   waiting from t = 0 and latency is measured from issue */
   uint32_t start_state;         /* 0 or 1                                                               */
   uint64_t mean_gap_q16[2];     /* per-state mean gap, Q48.16 us, <= 2^48; UINT64_MAX = no arrivals     */
   uint64_t mean_sojourn_us[2];  /* kinds 1, 2: per-state mean/fixed sojourn, >= 1                       */
@@ -137,6 +139,22 @@ slo_status slo_sim_run_batch(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                              uint32_t warmup_len, uint32_t slo_us, uint32_t* d_p99_us, double* d_goodput,
                              slo_replica_result* d_detail, uint32_t* d_latencies, slo_stats* d_stats,
                              void* stream);
+
+/* Extended form of slo_sim_run_batch (the latter is slo_sim_run with the extra outputs NULL). */
+typedef struct {
+  const slo_knobs* d_configs;   uint32_t n_configs;
+  const uint64_t* d_seeds;      uint32_t n_seeds;
+  uint32_t segment_len, warmup_len, slo_us;
+  uint32_t* d_p99_us;           /* [R] nearest-rank p99 (required)                                       */
+  double* d_goodput;            /* [R] Eq. (1) (required)                                                 */
+  slo_replica_result* d_detail; /* [R] or NULL                                                            */
+  uint32_t* d_latencies;        /* [R x (warmup_len + segment_len)] or NULL                              */
+  slo_stats* d_stats;           /* or NULL                                                                */
+  uint32_t* d_p50_us;           /* [R] nearest-rank p50 or NULL                             */
+  uint32_t* d_p95_us;           /* [R] nearest-rank p95 or NULL                                           */
+  uint32_t reserved[4];         /* must be 0                                                              */
+} slo_run_args;
+slo_status slo_sim_run(slo_sim* h, const slo_run_args* args, void* stream);
 
 /* The same call on HOST buffers (end-to-end use): copies h_configs / h_seeds to the handle's device
  * scratch, runs K1 on `stream`, copies the outputs back and synchronises `stream` before returning.

@@ -19,7 +19,7 @@ STATUS = {0: "ok", -1: "SLO_E_INVAL", -2: "SLO_E_NOMEM", -3: "SLO_E_CUDA", -4: "
           -5: "SLO_E_DEVICE", -6: "SLO_E_UNSUPPORTED"}
 
 # symbols include/slo_sim.h declares (checked by tests/test_abi_cpu.py)
-EXPORTS = ("slo_sim_create", "slo_sim_destroy", "slo_sim_get_info", "slo_sim_run_batch",
+EXPORTS = ("slo_sim_create", "slo_sim_destroy", "slo_sim_get_info", "slo_sim_run", "slo_sim_run_batch",
            "slo_sim_run_batch_host", "slo_aggregate", "slo_aggregate_reduce", "slo_neighbors",
            "slo_hillclimb_step", "slo_status_string", "slo_last_error")
 
@@ -63,6 +63,14 @@ class slo_knobs(C.Structure):
                 ("spec_on", C.c_uint8), ("draft_width", C.c_uint8), ("workload", C.c_uint8),
                 ("rate_scale_q8", C.c_uint16), ("accept_q16", C.c_uint32), ("max_wait_us", C.c_uint32),
                 ("reserved", C.c_uint32 * 4)]
+
+
+class slo_run_args(C.Structure):
+    _fields_ = [("d_configs", C.c_void_p), ("n_configs", C.c_uint32), ("d_seeds", C.c_void_p),
+                ("n_seeds", C.c_uint32), ("segment_len", C.c_uint32), ("warmup_len", C.c_uint32),
+                ("slo_us", C.c_uint32), ("d_p99_us", C.c_void_p), ("d_goodput", C.c_void_p),
+                ("d_detail", C.c_void_p), ("d_latencies", C.c_void_p), ("d_stats", C.c_void_p),
+                ("d_p50_us", C.c_void_p), ("d_p95_us", C.c_void_p), ("reserved", C.c_uint32 * 4)]
 
 
 class slo_space(C.Structure):
@@ -110,6 +118,7 @@ def lib():
                                      C.POINTER(vp)]
         L.slo_sim_destroy.argtypes = [vp]
         L.slo_sim_get_info.argtypes = [vp, C.POINTER(slo_sim_info)]
+        L.slo_sim_run.argtypes = [vp, C.POINTER(slo_run_args), vp]
         L.slo_sim_run_batch.argtypes = [vp, vp, C.c_uint32, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                         vp, vp, vp, vp, vp, vp]
         L.slo_sim_run_batch_host.argtypes = [vp, vp, C.c_uint32, vp, C.c_uint32, C.c_uint32, C.c_uint32,

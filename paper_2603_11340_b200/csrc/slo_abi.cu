@@ -137,13 +137,13 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   for (uint32_t w = 0; w < n_wl; ++w) {
     const slo_workload& x = wl[w];
     const uint64_t NOA = ~0ull;
-    if (x.arr.kind > 2 || x.arr.start_state > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: bad arrival kind", w);
+    if (x.arr.kind > 3 || x.arr.start_state > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: bad arrival kind", w);
     for (int s = 0; s < 2; ++s)
       if (x.arr.mean_gap_q16[s] != NOA && x.arr.mean_gap_q16[s] > (1ull << 48))
         return fail(nullptr, SLO_E_INVAL, "workload %u: mean_gap_q16 > 2^48", w);
     if (x.arr.kind == 0 && (x.arr.mean_gap_q16[0] == NOA || x.arr.mean_gap_q16[0] == 0))
       return fail(nullptr, SLO_E_INVAL, "workload %u: Poisson needs a finite positive gap", w);
-    if (x.arr.kind != 0) {
+    if (x.arr.kind == 1 || x.arr.kind == 2) {
       if (x.arr.mean_gap_q16[0] == NOA && x.arr.mean_gap_q16[1] == NOA)
         return fail(nullptr, SLO_E_INVAL, "workload %u: no state has arrivals", w);
       for (int s = 0; s < 2; ++s) {
@@ -260,7 +260,7 @@ slo_status slo_sim_get_info(const slo_sim* hc, slo_sim_info* info) {
 static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,
                              uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
                              uint32_t* d_p99, double* d_goodput, slo_replica_result* d_detail, uint32_t* d_lat,
-                             slo_stats* d_stats, cudaStream_t st) {
+                             slo_stats* d_stats, uint32_t* d_p50, uint32_t* d_p95, cudaStream_t st) {
   const uint32_t n_rep = (uint32_t)((uint64_t)n_configs * n_seeds);
   const uint32_t N = warmup_len + segment_len;
   // replicas per launch chunk: the latency rows of a chunk stay within the budget (a caller-provided
@@ -285,6 +285,8 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   p.lists = h->d_lists;
   p.part = d_detail ? d_detail : h->d_part;
   p.p99 = d_p99;
+  p.p50 = d_p50;
+  p.p95 = d_p95;
   p.goodput = d_goodput;
   p.detail = d_detail;
   p.stats = d_stats;
@@ -341,17 +343,38 @@ static slo_status check_run_args(slo_sim* h, uint32_t n_configs, uint32_t n_seed
   return SLO_OK;
 }
 
+slo_status slo_sim_run(slo_sim* h, const slo_run_args* a, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "run: null handle");
+  if (!a || !a->d_configs || !a->d_seeds || !a->d_p99_us || !a->d_goodput)
+    return fail(h, SLO_E_INVAL, "run: null pointer");
+  for (int i = 0; i < 4; ++i)
+    if (a->reserved[i]) return fail(h, SLO_E_INVAL, "run: reserved must be 0");
+  slo_status s = check_run_args(h, a->n_configs, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us);
+  if (s != SLO_OK) return s;
+  DeviceGuard g(h->device);
+  return launch_sim(h, a->d_configs, a->n_configs, a->d_seeds, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us,
+                    a->d_p99_us, a->d_goodput, a->d_detail, a->d_latencies, a->d_stats, a->d_p50_us, a->d_p95_us,
+                    (cudaStream_t)stream);
+}
+
 slo_status slo_sim_run_batch(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,
                              uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
                              uint32_t* d_p99_us, double* d_goodput, slo_replica_result* d_detail,
                              uint32_t* d_latencies, slo_stats* d_stats, void* stream) {
-  if (!h) return fail(nullptr, SLO_E_INVAL, "run_batch: null handle");
-  if (!d_configs || !d_seeds || !d_p99_us || !d_goodput) return fail(h, SLO_E_INVAL, "run_batch: null pointer");
-  slo_status s = check_run_args(h, n_configs, n_seeds, segment_len, warmup_len, slo_us);
-  if (s != SLO_OK) return s;
-  DeviceGuard g(h->device);
-  return launch_sim(h, d_configs, n_configs, d_seeds, n_seeds, segment_len, warmup_len, slo_us, d_p99_us, d_goodput,
-                    d_detail, d_latencies, d_stats, (cudaStream_t)stream);
+  slo_run_args a{};
+  a.d_configs = d_configs;
+  a.n_configs = n_configs;
+  a.d_seeds = d_seeds;
+  a.n_seeds = n_seeds;
+  a.segment_len = segment_len;
+  a.warmup_len = warmup_len;
+  a.slo_us = slo_us;
+  a.d_p99_us = d_p99_us;
+  a.d_goodput = d_goodput;
+  a.d_detail = d_detail;
+  a.d_latencies = d_latencies;
+  a.d_stats = d_stats;
+  return slo_sim_run(h, &a, stream);
 }
 
 slo_status slo_sim_run_batch_host(slo_sim* h, const slo_knobs* h_configs, uint32_t n_configs, const uint64_t* h_seeds,
@@ -383,7 +406,7 @@ slo_status slo_sim_run_batch_host(slo_sim* h, const slo_knobs* h_configs, uint32
   s = launch_sim(h, (const slo_knobs*)(b + o_cfg), n_configs, (const uint64_t*)(b + o_seed), n_seeds, segment_len,
                  warmup_len, slo_us, (uint32_t*)(b + o_p99), (double*)(b + o_gp),
                  h_detail ? (slo_replica_result*)(b + o_det) : nullptr, nullptr,
-                 h_stats ? (slo_stats*)(b + o_st) : nullptr, st);
+                 h_stats ? (slo_stats*)(b + o_st) : nullptr, nullptr, nullptr, st);
   if (s != SLO_OK) return s;
   CUDA_TRY(h, cudaMemcpyAsync(h_p99_us, b + o_p99, 4ull * R, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaMemcpyAsync(h_goodput, b + o_gp, 8ull * R, cudaMemcpyDeviceToHost, st));

@@ -30,6 +30,8 @@ struct SimParams {
   uint32_t* lat;               // [n_chunk][N] stored latency of every request of the chunk's replicas
   slo_replica_result* part;    // [n_rep] K1 -> K1b (the caller's detail buffer when given)
   uint32_t* p99;
+  uint32_t* p50;               // optional further order statistics
+  uint32_t* p95;
   double* goodput;
   slo_replica_result* detail;
   slo_stats* stats;

@@ -235,7 +235,7 @@ __device__ __forceinline__ void setup_replica(Group<G>& R, const DevWorkload& W,
     R.pre_base = W.t.pre_base_us;
     R.pre_tok = W.t.pre_tok_us;
     R.noise = W.t.noise_step_ppm;
-    if (W.kind != 0) {
+    if (W.kind == 1 || W.kind == 2) {
       const uint32_t st = W.start_state & 1u;
       uint64_t D;
       if (W.kind == 1) {
@@ -284,13 +284,14 @@ __device__ __forceinline__ void generate(Group<G>& R, const DevWorkload* __restr
   const u32x4 w = philox(i, 0, 0, 0, k0, k1);
   const uint64_t E = valid ? exp_q32(w.x) : 0;
   const uint32_t kind = go ? R.kind : 0u;
-  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : E;
+  // kind 0: gaps; kinds 1, 2: operational-time increments; kind 3 (closed loop): every a_i = 0
+  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : (kind == 3 ? 0ull : E);
   const uint64_t last = go ? R.last : 0ull;
-  const uint64_t sc = last + gscan64<G>(x, li);     // kind 0: a_i; kinds 1, 2: tau_i
+  const uint64_t sc = last + gscan64<G>(x, li);     // kind 0: a_i; kinds 1, 2: tau_i; kind 3: 0
   const uint64_t newlast = gshfl64<G>(sc, G - 1);
   uint64_t a = sc;
-  if (__any_sync(FULL, go && kind != 0)) {          // bursty: Cox time change, phases advance in order
-    const bool bursty = go && kind != 0;
+  const bool bursty = go && (kind == 1 || kind == 2);
+  if (__any_sync(FULL, bursty)) {                   // bursty: Cox time change, phases advance in order
     uint64_t pLam = 0, pU = 0, pD = 0, pstart = 0, nph = 0;
     uint32_t ph = 0, pstate = 0;
     if (bursty) {
@@ -531,7 +532,11 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     // ---- (a8) latency of the member at sorted position k; SLO count, sum, HBM row for the p99
     const uint32_t i = h + orig;
     const bool measured = member && i >= p.warmup;
-    const uint64_t l = c - (member ? R.a[i % RING] : c);
+    // latency origin: arrival (open loop, R2) or issue (closed loop, §2.11: s_i sits in window lane orig)
+    const uint64_t s_orig = gshfl64<G>(sj, (int)orig);
+    const bool from_issue = R.kind == 3;
+    if (from_issue && member && i == p.warmup) R.a_w = s_orig;     // the goodput window starts at that issue
+    const uint64_t l = c - (member ? (from_issue ? s_orig : R.a[i % RING]) : c);
     if (measured) {
       my_slo += (l <= p.slo_us);
       my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
@@ -665,13 +670,15 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint
   const uint32_t N = p.warmup + p.seg;
   const uint32_t n = p.seg;
   const uint32_t rank = (uint32_t)((99ull * n + 99ull) / 100ull);
-  const uint32_t K = n - rank + 1;                  // K-th largest = rank-th smallest
+
   for (uint32_t t = blockIdx.x; t < p.n_chunk; t += gridDim.x) {
     const uint32_t r = p.r_base + t;
     const slo_replica_result pr = p.part[r];
     if (pr.flags & 1u) {
       if (threadIdx.x == 0) {
         p.p99[r] = 0xFFFFFFFFu;
+        if (p.p50) p.p50[r] = 0xFFFFFFFFu;
+        if (p.p95) p.p95[r] = 0xFFFFFFFFu;
         p.goodput[r] = -1.0;
         if (p.detail) p.detail[r] = pr;
       }
@@ -682,7 +689,11 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint
     if (staged) {
       for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) vals[e] = row[e];
     }
-    uint32_t prefix = 0, kk = K;
+    uint32_t res[3];
+    const uint32_t nq = (p.p50 || p.p95) ? 3u : 1u;
+    for (uint32_t qi = 0; qi < nq; ++qi) {          // p99, then p50 and p95 (nearest rank, ceil(q n))
+    const uint32_t rq = qi == 0 ? rank : (uint32_t)(((qi == 1 ? 50ull : 95ull) * n + 99ull) / 100ull);
+    uint32_t prefix = 0, kk = n - rq + 1;
     for (int shift = 24; shift >= 0; shift -= 8) {
       hist[threadIdx.x] = 0;
       __syncthreads();
@@ -725,7 +736,12 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint
       kk = s_kk;
       __syncthreads();
     }
+    res[qi] = prefix;
+    }
+    const uint32_t prefix = res[0];
     if (threadIdx.x == 0) {
+      if (p.p50) p.p50[r] = res[1];
+      if (p.p95) p.p95[r] = res[2];
       p.p99[r] = prefix;
       p.goodput[r] = (double)((uint64_t)pr.slo_met * 1000000ull) / (double)pr.window_us;
       if (p.detail) {

@@ -153,10 +153,14 @@ class Simulator:
         return {f: getattr(i, f) for f, _ in _lib.slo_sim_info._fields_ if f != "reserved"}
 
     # -------------------------------------------------------------------------------------------
-    def alloc_outputs(self, n_rep: int, detail=True, latencies_n: int = 0, stats=False) -> Dict:
+    def alloc_outputs(self, n_rep: int, detail=True, latencies_n: int = 0, stats=False,
+                      percentiles=False) -> Dict:
         dev = torch.device("cuda", self.device)
         out = dict(p99_us=torch.empty(n_rep, dtype=torch.int32, device=dev),
                    goodput=torch.empty(n_rep, dtype=torch.float64, device=dev))
+        if percentiles:
+            out["p50_us"] = torch.empty(n_rep, dtype=torch.int32, device=dev)
+            out["p95_us"] = torch.empty(n_rep, dtype=torch.int32, device=dev)
         if detail:
             out["detail"] = torch.empty((n_rep, 32), dtype=torch.uint8, device=dev)
         if latencies_n:
@@ -167,16 +171,20 @@ class Simulator:
 
     def run_batch(self, configs: torch.Tensor, seeds: torch.Tensor, segment_len: int, warmup_len: int = 0,
                   slo_us: int = 1_200_000, detail: bool = True, latencies: bool = False, stats: bool = False,
-                  out: Optional[Dict] = None, stream=None) -> Dict:
-        """K1 over n_configs x n_seeds replicas (config-major).  Asynchronous on `stream`."""
+                  percentiles: bool = False, out: Optional[Dict] = None, stream=None) -> Dict:
+        """K0/K1/K1b over n_configs x n_seeds replicas (config-major).  Asynchronous on `stream`."""
         n_cfg = configs.shape[0]
         n_seeds = seeds.shape[0]
         if out is None:
-            out = self.alloc_outputs(n_cfg * n_seeds, detail, (segment_len + warmup_len) if latencies else 0, stats)
-        check(lib().slo_sim_run_batch(self.h, configs.data_ptr(), n_cfg, seeds.data_ptr(), n_seeds, segment_len,
-                                      warmup_len, slo_us, out["p99_us"].data_ptr(), out["goodput"].data_ptr(),
-                                      _ptr(out.get("detail")), _ptr(out.get("latencies")), _ptr(out.get("stats")),
-                                      _stream_ptr(stream)), self.h)
+            out = self.alloc_outputs(n_cfg * n_seeds, detail, (segment_len + warmup_len) if latencies else 0, stats,
+                                     percentiles)
+        a = _lib.slo_run_args()
+        a.d_configs, a.n_configs, a.d_seeds, a.n_seeds = configs.data_ptr(), n_cfg, seeds.data_ptr(), n_seeds
+        a.segment_len, a.warmup_len, a.slo_us = segment_len, warmup_len, slo_us
+        a.d_p99_us, a.d_goodput = out["p99_us"].data_ptr(), out["goodput"].data_ptr()
+        a.d_detail, a.d_latencies, a.d_stats = _ptr(out.get("detail")), _ptr(out.get("latencies")), _ptr(out.get("stats"))
+        a.d_p50_us, a.d_p95_us = _ptr(out.get("p50_us")), _ptr(out.get("p95_us"))
+        check(lib().slo_sim_run(self.h, C.byref(a), _stream_ptr(stream)), self.h)
         return out
 
     def run_batch_host(self, h_configs: np.ndarray, h_seeds: np.ndarray, segment_len: int, warmup_len: int = 0,

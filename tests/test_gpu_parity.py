@@ -27,10 +27,11 @@ def S():
 def _run_gpu(sim, wls, ks, seeds, N, warmup=0, slo=1_200_000, crn=1, latencies=True, sim_obj=None, **kw):
     s = sim_obj or sim.Simulator(wls, device=0, crn=crn, **kw)
     out = s.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(seeds), N, warmup_len=warmup, slo_us=slo,
-                      latencies=latencies, stats=True)
+                      latencies=latencies, stats=True, percentiles=True)
     torch.cuda.synchronize()
     from paper_2603_11340_b200._lib import RESULT_DTYPE, STATS_DTYPE
     res = dict(p99=out["p99_us"].cpu().numpy().view(np.uint32), gp=out["goodput"].cpu().numpy(),
+               p50=out["p50_us"].cpu().numpy().view(np.uint32), p95=out["p95_us"].cpu().numpy().view(np.uint32),
                detail=sim.unpack(out["detail"], RESULT_DTYPE), stats=sim.unpack(out["stats"], STATS_DTYPE)[0])
     if latencies:
         res["lat"] = out["latencies"].cpu().numpy().view(np.uint32).reshape(len(ks) * len(seeds), N + warmup)
@@ -46,6 +47,7 @@ def _compare_replica(orc, g, r, wls, k, seed, N, warmup, slo, crn=1, check_lat=T
     if check_lat:
         assert np.array_equal(g["lat"][r], ref["latencies"]), tag
     assert int(g["p99"][r]) == ref["p99_us"], tag
+    assert int(g["p50"][r]) == ref["p50_us"] and int(g["p95"][r]) == ref["p95_us"], tag
     assert g["gp"][r] == ref["goodput"], tag
     assert int(d["p99_us"]) == ref["p99_us"] and int(d["slo_met"]) == ref["slo_met"], tag
     assert int(d["n_measured"]) == ref["n_measured"] and int(d["flags"]) == ref["flags"], tag
@@ -70,7 +72,7 @@ WLS = None
 
 def _wls():
     return [inputs.preset_ll(), inputs.preset_sim(), inputs.preset_stress(kind=1), inputs.preset_stress(kind=2),
-            inputs.preset_ll(rate=40.0, stream_id=7)]
+            inputs.preset_ll(rate=40.0, stream_id=7), inputs.preset_closed(stream_id=3)]
 
 
 @pytest.mark.parametrize("block", range(6))
@@ -84,6 +86,8 @@ def test_random_small_configs(S, orc, block):
     ks[1] = inputs.knobs(conc=1, max_num_seqs=1, draft_len=16, spec_on=1, accept_q16=0)
     ks[2] = inputs.knobs(conc=32, max_num_seqs=1, max_wait_us=50_000, workload=2)
     ks[3] = inputs.knobs(conc=1, max_num_seqs=32, max_wait_us=50_000, workload=3)
+    ks[4] = inputs.knobs(conc=24, max_num_seqs=6, draft_len=4, spec_on=1, workload=5)       # closed loop, G = 32
+    ks[5] = inputs.knobs(conc=8, max_num_seqs=8, workload=5, max_wait_us=30_000)           # closed loop, G = 8
     seeds = inputs.seeds(3, 77 * block)
     N = rng.choice([37, 333, 1000, 1234])
     warmup = rng.choice([0, 0, 17, 100])
