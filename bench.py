@@ -161,6 +161,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--warps-per-block", type=int, default=0, help="launch shape override (0 = library default)")
     ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--eager-climb", action="store_true", help="c4: host loop instead of the CUDA-graph step")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,10 +248,25 @@ def main():
     k1_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k1_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     st_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    # K0 classify + K1 simulate + K1b select + K2 aggregate (+ K2b reduce for N>1 sweeps, K3 for the climb)
-    launches_per_step = 4 + (1 if (world > 1 and args.workload != "c4") else 0) + (1 if args.workload == "c4" else 0)
+    # K0 count + K0 classify + K1 simulate + K1b select + K2 aggregate (+ K2b for N>1 sweeps, K3 for the climb)
+    launches_per_step = 5 + (1 if (world > 1 and args.workload != "c4") else 0) + (1 if args.workload == "c4" else 0)
+
+    graph = None
+    if args.workload == "c4" and not args.eager_climb and (world == 1 or dist.get_backend() == "nccl"):
+        from paper_2603_11340_b200.dist import ClimbGraph
+        graph = ClimbGraph(S, cfg, seeds, n_cand=n_cfg).capture()      # NEXT-4: one graph per climb step
+        out = graph.out                                                 # (replayed on the current stream)
+        launches_per_step = 6                                           # K0 x2, K1, K1b, K2, K3
 
     def step(i=None):
+        if graph is not None:
+            if i is not None:
+                k1_start[i].record(stream)
+            graph.graph.replay()
+            if i is not None:
+                k1_end[i].record(stream)
+                st_end[i].record(stream)
+            return
         if i is not None:
             k1_start[i].record(stream)
         S.run_batch(cands, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out, stream=stream)

@@ -59,6 +59,62 @@ def max_over_ranks(x: float, device=None) -> float:
     return float(t.item())
 
 
+class ClimbGraph:
+    """Alg. 1 with the whole step — K0/K1/K1b simulate, K2 aggregate, all-gather (N > 1), K3 climb — captured
+    once in a CUDA graph and replayed (SV §8(f) NEXT-4): no host round trip between steps.  The candidate
+    list and the climb state live in device buffers that the step rewrites in place."""
+
+    def __init__(self, sim, cfg, seeds: List[int], n_cand: int = 32, sp=None):
+        from . import sim as S
+        self.sim, self.cfg = sim, cfg
+        self.space = cfg.extra["space"]
+        self.sp = dict(sp if sp is not None else cfg.extra["score"])
+        K0 = cfg.knobs[0]
+        self.n_cand, self.n_seeds = n_cand, len(seeds)
+        self.cands = sim.candidates(self.space, K0, n_cand)
+        self.state = sim.climb_state(K0)
+        self.init_cands = self.cands.clone()
+        self.init_state = self.state.clone()
+        self.seeds = S.seeds_tensor(seeds, device=self.cands.device)
+        self.out = sim.alloc_outputs(n_cand * len(seeds), detail=True, stats=True)
+        self.agg = torch.empty((n_cand, 32), dtype=torch.uint8, device=self.cands.device)
+        _, self.w = world()
+        self.parts = (torch.empty((self.w * n_cand, 32), dtype=torch.uint8, device=self.cands.device)
+                      if self.w > 1 else self.agg)
+        self.stream = torch.cuda.Stream(device=self.cands.device)
+        self.graph = None
+
+    def _step(self):
+        c = self.cfg
+        self.sim.run_batch(self.cands, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out,
+                           stream=self.stream)
+        self.sim.aggregate(self.out["detail"], self.n_cand, self.n_seeds, out=self.agg, stream=self.stream)
+        if self.w > 1:
+            dist.all_gather_into_tensor(self.parts, self.agg)
+        self.sim.hillclimb_step(self.space, self.sp, self.cands, self.parts, self.w, self.state, stream=self.stream)
+
+    def capture(self):
+        """Warm up (allocates the library's scratch), restore the initial state, capture one step."""
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            self._step()
+        self.stream.synchronize()
+        self.cands.copy_(self.init_cands)
+        self.state.copy_(self.init_state)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._step()
+        return self
+
+    def run(self, steps: int):
+        if self.graph is None:
+            self.capture()
+        for _ in range(steps):
+            self.graph.replay()
+        return self.state, self.cands
+
+
 def hillclimb(sim, cfg, steps: int, seeds: List[int], n_cand: int = 32, stream=None):
     """Device-resident Alg. 1 over `steps` iterations on this rank's seed slice; returns the final state.
 

@@ -305,3 +305,17 @@ def test_device_climb_seed_sharded_parts(S):
         cands_out.append(cands.cpu().numpy().tobytes())
     assert states[0] == states[1] and cands_out[0] == cands_out[1]
     s.close()
+
+
+def test_climb_cuda_graph_matches_eager(S):
+    """NEXT-4: the climb step captured in a CUDA graph and replayed gives the same trajectory (state and
+    candidate lists, bit for bit) as the eager host loop."""
+    from paper_2603_11340_b200.dist import ClimbGraph, hillclimb
+    cfg = inputs.config_c4(n_seeds=6, segment_len=400)
+    s = S.Simulator(cfg.workloads, device=0)
+    st_e, c_e = hillclimb(s, cfg, 5, cfg.seeds())
+    g = ClimbGraph(s, cfg, cfg.seeds()).capture()
+    st_g, c_g = g.run(5)
+    torch.cuda.synchronize()
+    assert torch.equal(st_e, st_g) and torch.equal(c_e, c_g)
+    s.close()
