@@ -54,7 +54,7 @@ class Workload(C.Structure):
     _fields_ = [("arr", Arrivals),
                 ("prompt_cw", C.POINTER(C.c_uint32)), ("prompt_lo", C.c_uint32), ("prompt_ncw", C.c_uint32),
                 ("output_cw", C.POINTER(C.c_uint32)), ("output_lo", C.c_uint32), ("output_ncw", C.c_uint32),
-                ("timing", Timing), ("stream_id", C.c_uint32)]
+                ("timing", Timing), ("stream_id", C.c_uint32), ("batching", C.c_uint32)]
 
 
 class Knobs(C.Structure):
@@ -105,7 +105,7 @@ def lib():
                               C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Result),
                               C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
         L.orc_run_trace.argtypes = [C.POINTER(Timing), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
-                                    C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                                    C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32, C.POINTER(Result),
                                     C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
@@ -140,6 +140,7 @@ class _WorkloadSet:
             for k, v in d["timing"].items():
                 setattr(w.timing, k, v)
             w.stream_id = d["stream_id"]
+            w.batching = d.get("batching", 0)
 
 
 def make_knobs(d: Dict) -> Knobs:
@@ -232,7 +233,7 @@ def run(workloads: Sequence[Dict], knobs: Dict, seed: int, segment_len: int, war
 def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_us: int,
               a: Sequence[int], P: Sequence[int], O: Sequence[int], f: Optional[Sequence[int]] = None,
               A: Optional[Sequence[Sequence[int]]] = None, warmup_len: int = 0, slo_us: int = 1_200_000,
-              issue_origin: int = 0) -> Dict:
+              issue_origin: int = 0, continuous: int = 0) -> Dict:
     """Trace mode: explicit requests (a, P, O), per-request noise factor f (ppm) and accepted-prefix draws."""
     n = len(a)
     tm = Timing(**timing)
@@ -251,7 +252,8 @@ def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_u
     res, cnt = Result(), Counters()
     lat = np.zeros(n, np.uint32)
     tr = (Req * n)()
-    rc = lib().orc_run_trace(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, issue_origin, n, a_, P_, O_, f_,
+    rc = lib().orc_run_trace(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, issue_origin, continuous, n, a_,
+                             P_, O_, f_,
                              off_, val_,
                              warmup_len, slo_us, C.byref(res), lat.ctypes.data_as(C.POINTER(C.c_uint32)), tr,
                              C.byref(cnt))

@@ -413,6 +413,171 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
   return ad->bad ? -2 : 0;
 }
 
+/* ---------------------------------------------------------------------------------------------- */
+/* continuous (iteration-level) batching: the same instants and gate, but the server  */
+/* runs one prefill or decode iteration at a time over a running set of at most B requests.           */
+/* ---------------------------------------------------------------------------------------------- */
+typedef struct {
+  int philox;                 /* decode-iteration noise from ITER blocks (Philox mode) */
+  uint32_t k0, k1, step_ppm;
+} itnoise;
+
+static uint64_t iter_noise(const itnoise* nz, uint64_t it) {
+  if (!nz->philox || nz->step_ppm == 0) return 1000000u;
+  uint32_t w[4];
+  block(nz->k0, nz->k1, (uint32_t)it, 3, 0, w);
+  int64_t bytesum = (int64_t)(w[0] & 0xFF) + (int64_t)((w[0] >> 8) & 0xFF) + (int64_t)((w[0] >> 16) & 0xFF) +
+                    (int64_t)(w[0] >> 24);
+  return (uint64_t)(1000000 + (bytesum - 510) * (int64_t)nz->step_ppm);
+}
+
+static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t issue_origin,
+                         uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
+                         const uint32_t* f, adraw* ad, const itnoise* nz, uint32_t warmup, uint32_t slo_us,
+                         orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  uint64_t* s = (uint64_t*)calloc(N, sizeof(uint64_t));
+  uint64_t* form = (uint64_t*)calloc(N, sizeof(uint64_t));   /* admission (prefill start) */
+  uint64_t* c = (uint64_t*)calloc(N, sizeof(uint64_t));
+  uint32_t* steps = (uint32_t*)calloc(N, sizeof(uint32_t));
+  uint32_t* batch_of = (uint32_t*)calloc(N, sizeof(uint32_t)); /* prefill iteration that admitted it */
+  uint32_t* rem = (uint32_t*)calloc(N, sizeof(uint32_t));
+  uint32_t* run = (uint32_t*)calloc(B, sizeof(uint32_t));
+  uint32_t* fin = (uint32_t*)calloc(B, sizeof(uint32_t));
+  uint32_t* lat = (uint32_t*)calloc(N, sizeof(uint32_t));
+  if (!s || !form || !c || !steps || !batch_of || !rem || !run || !fin || !lat) abort();
+
+  uint32_t na = 0, ni = 0, nq = 0, inflight = 0, ndone = 0, nrun = 0;
+  uint32_t join_lo = 0, join_hi = 0;      /* requests being prefilled: they join R at the iteration end */
+  uint32_t nfin = 0;                      /* running members finishing at the iteration end */
+  int busy = 0;
+  uint64_t t = 0, iter_end = 0, it = 0, prefills = 0, decode_iters = 0, member_steps = 0, spec_blocks = 0;
+
+  while (ndone < N) {
+    uint64_t tn = U64MAX;
+    if (busy) tn = iter_end;
+    if (na < N && a[na] < tn) tn = a[na];
+    if (tn == U64MAX) abort();
+    t = tn;
+    /* (1) the iteration ending at t: completions leave, prefilled requests join */
+    if (busy && iter_end == t) {
+      for (uint32_t q = 0; q < nfin; ++q) {
+        c[fin[q]] = t;
+        --inflight;
+        ++ndone;
+      }
+      uint32_t kept = 0;                              /* drop finished members, keep admission order */
+      for (uint32_t q = 0; q < nrun; ++q)
+        if (rem[run[q]] != 0) run[kept++] = run[q];
+      nrun = kept;
+      for (uint32_t m = join_lo; m < join_hi; ++m) run[nrun++] = m;
+      nfin = 0;
+      join_lo = join_hi = 0;
+      busy = 0;
+    }
+    /* (2) arrivals at t */
+    while (na < N && a[na] == t) ++na;
+    /* (3) issues at t while fewer than C are in flight */
+    while (ni < na && inflight < C) {
+      s[ni] = t;
+      ++inflight;
+      ++ni;
+    }
+    /* (4) a free server starts the next iteration */
+    if (!busy) {
+      if (nrun < B && nq < ni) {                        /* prefill the first k queued requests */
+        uint32_t k = ni - nq < B - nrun ? ni - nq : B - nrun;
+        uint32_t maxP = 0;
+        for (uint32_t m = nq; m < nq + k; ++m) {
+          if (P[m] > maxP) maxP = P[m];
+          form[m] = t;
+          batch_of[m] = (uint32_t)prefills;
+          rem[m] = O[m];
+        }
+        uint64_t D = (uint64_t)(((u128)f[nq] * ((u128)tm->pre_base_us + (u128)tm->pre_tok_us * maxP)) / 1000000u);
+        join_lo = nq;
+        join_hi = nq + k;
+        nq += k;
+        ++prefills;
+        iter_end = t + D;
+        busy = 1;
+      } else if (nrun > 0) {                            /* one decode iteration of the running set */
+        uint64_t fi = iter_noise(nz, it);
+        uint64_t D = (uint64_t)(((u128)fi * step_cost(tm, gamma, nrun)) / 1000000u);
+        for (uint32_t q = 0; q < nrun; ++q) {
+          uint32_t m = run[q];
+          uint32_t e = 1;
+          if (gamma > 0) {
+            uint32_t A = draw_A(ad, m, steps[m], gamma);
+            e = A + 1 < rem[m] ? A + 1 : rem[m];
+          }
+          rem[m] -= e;
+          steps[m] += 1;
+          if (rem[m] == 0) fin[nfin++] = m;
+        }
+        ++it;
+        ++decode_iters;
+        iter_end = t + D;
+        busy = 1;
+      }
+    }
+  }
+  for (uint32_t m = 0; m < N; ++m) {
+    member_steps += steps[m];
+    if (gamma > 0) spec_blocks += (steps[m] + 3u) / 4u;
+  }
+
+  const uint64_t* origin = issue_origin ? s : a;
+  uint32_t n = N - warmup;
+  uint32_t slo_met = 0, flags = 0;
+  uint64_t sum = 0, cmax = 0;
+  for (uint32_t i = 0; i < N; ++i) {
+    uint64_t l = c[i] - origin[i];
+    lat[i] = l > U32MAX ? U32MAX : (uint32_t)l;
+    if (i >= warmup) {
+      if (l > U32MAX) flags |= 2u;
+      if (l <= slo_us) ++slo_met;
+      sum += l;
+      if (c[i] > cmax) cmax = c[i];
+    }
+  }
+  uint32_t* sorted = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+  if (!sorted) abort();
+  memcpy(sorted, lat + warmup, (size_t)n * sizeof(uint32_t));
+  qsort(sorted, n, sizeof(uint32_t), cmp_u32);
+  res->p99_us = sorted[(uint32_t)((99ull * n + 99ull) / 100ull) - 1];
+  res->p50_us = sorted[(uint32_t)((50ull * n + 99ull) / 100ull) - 1];
+  res->p95_us = sorted[(uint32_t)((95ull * n + 99ull) / 100ull) - 1];
+  res->slo_met = slo_met;
+  res->n_measured = n;
+  res->flags = flags;
+  uint64_t T = cmax - origin[warmup];
+  res->window_us = T < 1 ? 1 : T;
+  res->sum_latency_us = sum;
+  res->goodput = (double)((uint64_t)slo_met * 1000000ull) / (double)res->window_us;
+  if (latencies) memcpy(latencies, lat, (size_t)N * sizeof(uint32_t));
+  if (trace) {
+    for (uint32_t i = 0; i < N; ++i) {
+      trace[i].a = a[i];
+      trace[i].s = s[i];
+      trace[i].form = form[i];
+      trace[i].c = c[i];
+      trace[i].batch = batch_of[i];
+      trace[i].steps = steps[i];
+      trace[i].P = P[i];
+      trace[i].O = O[i];
+    }
+  }
+  if (cnt) {
+    cnt->batches = prefills;                 /* continuous mode: prefill iterations */
+    cnt->decode_steps = decode_iters;        /* continuous mode: decode iterations */
+    cnt->member_steps = member_steps;
+    cnt->philox_blocks = spec_blocks + ((nz->philox && nz->step_ppm) ? decode_iters : 0);
+  }
+  free(sorted);
+  free(s); free(form); free(c); free(steps); free(batch_of); free(rem); free(run); free(fin); free(lat);
+  return ad->bad ? -2 : 0;
+}
+
 static void invalid_result(orc_result* res) {
   memset(res, 0, sizeof(*res));
   res->p99_us = U32MAX;
@@ -450,15 +615,23 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
   orc_thresholds(k->accept_q16, k->draft_width, gamma, T);
   uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
   adraw ad = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, T, NULL, NULL, 0};
-  int rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, W->arr.kind == 3, N, a, P, O, f, &ad,
-                    warmup_len, slo_us, res, latencies, trace, cnt);
+  int rc;
+  if (W->batching == 1) {
+    itnoise nz = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, W->timing.noise_step_ppm};
+    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, W->arr.kind == 3, N, a, P, O, f, &ad, &nz,
+                       warmup_len, slo_us, res, latencies, trace, cnt);
+  } else {
+    rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, W->arr.kind == 3, N, a, P, O, f, &ad,
+                  warmup_len, slo_us, res, latencies, trace, cnt);
+  }
   if (cnt) cnt->philox_blocks += N + (W->arr.kind == 1 ? (uint64_t)phases : 0);
   free(a); free(P); free(O); free(w3); free(f);
   return rc;
 }
 
 int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
-                  uint32_t max_wait_us, uint32_t issue_origin, uint32_t n, const uint64_t* a, const uint32_t* P,
+                  uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
+                  const uint64_t* a, const uint32_t* P,
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
@@ -471,6 +644,11 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
     if (O[i] < 1) return -1;
   if (cnt) memset(cnt, 0, sizeof(*cnt));
   adraw ad = {0, 0, 0, NULL, A_off, A_val, 0};
+  if (continuous) {
+    itnoise nz = {0, 0, 0, 0};
+    return simulate_cont(tm, conc, max_num_seqs, gamma_eff, issue_origin, n, a, P, O, f, &ad, &nz, warmup_len,
+                         slo_us, res, latencies, trace, cnt);
+  }
   return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, warmup_len,
                   slo_us, res, latencies, trace, cnt);
 }

@@ -32,6 +32,7 @@ typedef struct {
   const uint32_t* output_cw; uint32_t output_lo, output_ncw;
   orc_timing timing;
   uint32_t stream_id;
+  uint32_t batching;          /* 0 static batches (§2.6), 1 continuous / iteration-level (§2.12) */
 } orc_workload;
 
 /* Knob record; its 32-byte little-endian layout is normative (FNV-1a key mode). */
@@ -85,10 +86,12 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
             orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);
 
 /* Trace mode: explicit arrivals a[n], lengths P[n], O[n], per-request noise factor f[n] (ppm, used when
- * the request heads a batch), and per-request accepted-prefix draws A_val[A_off[i] + j] for decode step
- * j of request i (A_off has n+1 entries).  gamma_eff is given directly. */
+ * the request heads a batch / a prefill), and per-request accepted-prefix draws A_val[A_off[i] + j] for
+ * decode step j of request i (A_off has n+1 entries).  gamma_eff is given directly.  With `continuous`
+ * the decode iterations carry no noise (f_it = 10^6). */
 int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
-                  uint32_t max_wait_us, uint32_t issue_origin, uint32_t n, const uint64_t* a, const uint32_t* P,
+                  uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
+                  const uint64_t* a, const uint32_t* P,
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);

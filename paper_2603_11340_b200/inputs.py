@@ -105,6 +105,7 @@ def workload(kind=0, rate=10.0, prompt=None, output=None, timing=None, stream_id
         "output": output if output is not None else lognormal_table(math.log(80.0), 0.4, 1, 64),
         "timing": dict(timing if timing is not None else LL_TIMING),
         "stream_id": int(stream_id),
+        "batching": 0,
     }
 
 
@@ -129,6 +130,13 @@ def preset_closed(stream_id=0) -> Dict:
     closed loop of `conc` users with zero think time (arrival kind 3); latency from issue."""
     w = preset_ll(stream_id=stream_id)
     w["arrivals"]["kind"] = 3
+    return w
+
+
+def continuous(w: Dict) -> Dict:
+    """The same workload served with continuous (iteration-level, vLLM-style) batching."""
+    w = dict(w)
+    w["batching"] = 1
     return w
 
 

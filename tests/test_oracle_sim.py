@@ -24,7 +24,7 @@ def _traces():
 @pytest.mark.parametrize("tr", _traces(), ids=lambda t: t["name"].split()[0])
 def test_hand_traces(orc, tr):
     r = orc.run_trace(tr["timing"], tr["conc"], tr["B"], tr["gamma"], tr["max_wait_us"], tr["a"], tr["P"],
-                      tr["O"], f=tr.get("f"), A=tr.get("A"), slo_us=tr["slo_us"])
+                      tr["O"], f=tr.get("f"), A=tr.get("A"), slo_us=tr["slo_us"], continuous=tr.get("continuous", 0))
     ex = tr["expect"]
     assert list(r["trace"]["c"]) == ex["c"]
     if "s" in ex:
@@ -414,3 +414,123 @@ def test_percentiles_nearest_rank(orc):
             for key, q in (("p50_us", 50), ("p95_us", 95), ("p99_us", 99)):
                 assert r[key] == srt[(q * n + 99) // 100 - 1]
             assert r["p50_us"] <= r["p95_us"] <= r["p99_us"]
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-2: continuous (iteration-level) batching
+# ------------------------------------------------------------------------------------------------
+def brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=False):
+    """Per-microsecond time stepping of DESIGN.md §2.12 (written separately from the oracle)."""
+    N = len(a)
+    s, c = [None] * N, [None] * N
+    rem = list(O)
+    steps = [0] * N
+    t = arrived = issued = admitted = done = 0
+    running, joining, finishing = [], [], []
+    end = None                      # end instant of the current iteration (None: server free)
+    while done < N:
+        again = True
+        while again:
+            again = False
+            if end == t:
+                for m in finishing:
+                    c[m] = t
+                    done += 1
+                running = [m for m in running if m not in finishing] + joining
+                finishing, joining, end = [], [], None
+            while arrived < N and a[arrived] <= t:
+                arrived += 1
+            while issued < arrived and issued - done < C:
+                s[issued] = t
+                issued += 1
+            if end is None:
+                if len(running) < B and admitted < issued:
+                    k = min(B - len(running), issued - admitted)
+                    new = list(range(admitted, admitted + k))
+                    admitted += k
+                    D = f[new[0]] * (tm["pre_base_us"] + tm["pre_tok_us"] * max(P[m] for m in new)) // 10 ** 6
+                    joining, end = new, t + D
+                elif running:
+                    n = len(running)
+                    if gamma == 0:
+                        d = tm["dec_base_us"] + tm["dec_seq_us"] * n
+                    else:
+                        d = (gamma * (tm["dr_base_us"] + tm["dr_seq_us"] * n) + tm["ver_base_us"]
+                             + tm["ver_seq_us"] * n + tm["ver_tok_us"] * (gamma + 1) * n)
+                    for m in running:
+                        e = 1 if gamma == 0 else min(A[m][steps[m]] + 1, rem[m])
+                        rem[m] -= e
+                        steps[m] += 1
+                        if rem[m] == 0:
+                            finishing.append(m)
+                    end = t + d
+                if end == t:
+                    again = True
+        t += 1
+    origin = s if issue_origin else a
+    return s, c, [ci - oi for ci, oi in zip(c, origin)]
+
+
+@pytest.mark.parametrize("case", range(150))
+def test_continuous_brute_force_agreement(orc, case):
+    rng = random.Random(5000 + case)
+    gamma = rng.choice([0, 0, 1, 3])
+    tm = dict(pre_base_us=rng.randrange(0, 5), pre_tok_us=rng.randrange(0, 4), dec_base_us=rng.randrange(0, 12),
+              dec_seq_us=rng.randrange(0, 4), dr_base_us=rng.randrange(0, 4), dr_seq_us=rng.randrange(0, 2),
+              ver_base_us=rng.randrange(0, 8), ver_seq_us=rng.randrange(0, 3), ver_tok_us=rng.randrange(0, 2),
+              noise_step_ppm=0)
+    n = rng.randrange(1, 12)
+    a, P, O, f, A = _random_trace(rng, n, gamma)
+    A = [row + [rng.randrange(0, gamma + 1) for _ in range(8)] for row in A]
+    closed = rng.random() < 0.3
+    if closed:
+        a = [0] * n
+    C, B = rng.randrange(1, 6), rng.randrange(1, 6)
+    s_bf, c_bf, l_bf = brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=closed)
+    r = orc.run_trace(tm, C, B, gamma, 0, a, P, O, f=f, A=A if gamma else None, continuous=1,
+                      issue_origin=int(closed))
+    assert list(r["trace"]["c"]) == c_bf and list(r["trace"]["s"]) == s_bf
+    assert list(r["latencies"]) == l_bf
+
+
+@pytest.mark.parametrize("wl", ["ll", "sim", "stress", "closed"])
+def test_continuous_equals_static_at_batch_one(orc, wl):
+    """With B = 1 and no noise, a prefill iteration followed by the request's decode iterations is exactly a
+    static batch of one (same cumulative cost, no per-iteration floors to differ)."""
+    w = {"ll": inputs.preset_ll(), "sim": inputs.preset_sim(), "stress": inputs.preset_stress(),
+         "closed": inputs.preset_closed()}[wl]
+    w["timing"] = dict(w["timing"], noise_step_ppm=0)
+    for k in (inputs.knobs(conc=4, max_num_seqs=1), inputs.knobs(conc=9, max_num_seqs=1, draft_len=4, spec_on=1,
+                                                                  accept_q16=inputs.q16(0.7))):
+        st = orc.run([w], k, 13, 800, latencies=True)
+        ct = orc.run([inputs.continuous(w)], k, 13, 800, latencies=True)
+        assert np.array_equal(st["latencies"], ct["latencies"])
+        assert st["counters"]["member_steps"] == ct["counters"]["member_steps"]
+
+
+def test_continuous_invariants(orc):
+    """Running set never exceeds B, in-flight never exceeds C, admission is FCFS, every request completes
+    after its admission; goodput <= throughput."""
+    rng = random.Random(9)
+    for _ in range(20):
+        wls = [inputs.continuous(inputs.preset_ll(rate=rng.choice([5.0, 10.0, 30.0]))),
+               inputs.continuous(inputs.preset_stress()), inputs.continuous(inputs.preset_closed())]
+        k = inputs.random_knobs(rng, n_wl=3)
+        N = rng.choice([50, 400])
+        r = orc.run(wls, k, rng.getrandbits(64), N, trace=True)
+        tr = r["trace"]
+        a, s, form, c = (tr[x].astype(np.int64) for x in ("a", "s", "form", "c"))
+        assert np.all(s >= a) and np.all(np.diff(s) >= 0) and np.all(np.diff(form) >= 0)
+        assert np.all(form >= s) and np.all(c > form - 1)
+        ev = sorted([(int(t), 0, -1) for t in c] + [(int(t), 1, +1) for t in s])
+        cur = 0
+        for _, _, d in ev:
+            cur += d
+            assert cur <= k["conc"]
+        # running set (admitted, not completed) never exceeds B
+        ev = sorted([(int(t), 0, -1) for t in c] + [(int(t), 1, +1) for t in form])
+        cur = 0
+        for _, _, d in ev:
+            cur += d
+            assert cur <= k["max_num_seqs"]
+        assert r["slo_met"] <= r["n_measured"]
