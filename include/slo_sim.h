@@ -71,6 +71,10 @@ typedef struct {
   uint32_t output_lo, output_ncw;
   slo_timing timing;
   uint32_t stream_id;           /* cfgkey in CRN mode                                  */
+  uint32_t batching;            /* 0: static batches; 1: continuous,         */
+                                /* iteration-level (vLLM-style): prefill or */
+                                /* decode iterations over a running set of <= max_num_seqs requests;     */
+                                /* max_wait_us is not used.  Other values: SLO_E_INVAL at create.         */
 } slo_workload;
 
 /* One logical-knob configuration, 32 B.  Validity is checked per

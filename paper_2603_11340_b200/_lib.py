@@ -45,7 +45,7 @@ class slo_workload(C.Structure):
     _fields_ = [("arr", slo_arrivals),
                 ("prompt_cw", C.POINTER(C.c_uint32)), ("prompt_lo", C.c_uint32), ("prompt_ncw", C.c_uint32),
                 ("output_cw", C.POINTER(C.c_uint32)), ("output_lo", C.c_uint32), ("output_ncw", C.c_uint32),
-                ("timing", slo_timing), ("stream_id", C.c_uint32)]
+                ("timing", slo_timing), ("stream_id", C.c_uint32), ("batching", C.c_uint32)]
 
 
 class slo_sim_opts(C.Structure):

@@ -26,9 +26,10 @@ struct slo_sim {
   int blocks_per_sm_opt = 0;
   uint32_t n_wl = 0;
   uint32_t crn = 1;
+  bool any_cont = false;            // a workload uses continuous batching: launch K1c
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
-  uint32_t* d_ctl = nullptr;        // [104]: list lengths [3], K1 cursors [3], K0 bucket counts/cursors [96]
+  uint32_t* d_ctl = nullptr;        // [136]: list lengths [4], K1 cursors [4], K0 bucket counts/cursors [128]
   // run scratch (grow-only): work lists, latency rows, per-replica partial results
   uint32_t* d_lists = nullptr;
   size_t lists_cap = 0;
@@ -158,6 +159,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     for (int i = 0; i < 9; ++i)
       if (tv[i] >= (1u << 20)) return fail(nullptr, SLO_E_INVAL, "workload %u: timing value >= 2^20", w);
     if (x.timing.noise_step_ppm > 1960) return fail(nullptr, SLO_E_INVAL, "workload %u: noise_step_ppm > 1960", w);
+    if (x.batching > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: batching must be 0 or 1", w);
     slo::DevWorkload& d = hw[w];
     memset(&d, 0, sizeof d);
     d.kind = x.arr.kind;
@@ -176,6 +178,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     tables.insert(tables.end(), x.output_cw, x.output_cw + x.output_ncw);
     d.t = x.timing;
     d.stream_id = x.stream_id;
+    d.batching = x.batching;
   }
   if (tables.empty()) tables.push_back(0);
 
@@ -192,6 +195,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   h->device = device;
   h->sm_count = prop.multiProcessorCount;
   h->n_wl = n_wl;
+  for (uint32_t w = 0; w < n_wl; ++w) h->any_cont |= wl[w].batching == 1;
   h->crn = o.crn;
   if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
@@ -201,7 +205,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
-      (e = cudaMalloc(&h->d_ctl, sizeof(uint32_t) * 104)) != cudaSuccess) {
+      (e = cudaMalloc(&h->d_ctl, sizeof(uint32_t) * slo::kCtlWords)) != cudaSuccess) {
     slo_sim_destroy(h);
     return fail(nullptr, SLO_E_NOMEM, "create: cudaMalloc: %s", cudaGetErrorString(e));
   }
@@ -271,7 +275,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   if (chunk < 1) chunk = 1;
   if (chunk > n_rep) chunk = n_rep;
   slo_status s;
-  if ((s = ensure(h, h->d_lists, h->lists_cap, (size_t)3 * chunk, st)) != SLO_OK) return s;
+  if ((s = ensure(h, h->d_lists, h->lists_cap, (size_t)slo::kLists * chunk, st)) != SLO_OK) return s;
   if (!d_lat && (s = ensure(h, h->d_lat, h->lat_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
   if (!d_detail && (s = ensure(h, h->d_part, h->part_cap, (size_t)n_rep, st)) != SLO_OK) return s;
 
@@ -281,7 +285,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   p.wl = h->d_wl;
   p.tables = h->d_tables;
   p.counts = h->d_ctl;
-  p.cursor = h->d_ctl + 3;
+  p.cursor = h->d_ctl + slo::kLists;
   p.lists = h->d_lists;
   p.part = d_detail ? d_detail : h->d_part;
   p.p99 = d_p99;
@@ -303,6 +307,15 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   if (smem > 48 * 1024)
     CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int bps = blocks_per_sm_for(h, smem);
+  int cont_bps = 1;
+  if (h->any_cont) {
+    if (smem > 48 * 1024)
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel, h->warps_per_block * 32,
+                                                      smem) != cudaSuccess || cont_bps < 1)
+      cont_bps = 1;
+  }
   const uint32_t sel_vals = segment_len <= 11008u ? segment_len : 0u;   // stage rows up to 43 KB in smem
   const size_t sel_smem = (256u + sel_vals) * sizeof(uint32_t);
   if (d_stats) CUDA_TRY(h, cudaMemsetAsync(d_stats, 0, sizeof(slo_stats), st));
@@ -312,12 +325,12 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     p.n_chunk = nc;
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
-    CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * 104, st));
-    slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, n_seeds, (uint32_t)r0, nc, h->n_wl,
-                                                                    h->d_ctl);
+    CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * slo::kCtlWords, st));
+    slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
+                                                                    h->n_wl, h->d_ctl);
     CUDA_TRY(h, cudaGetLastError());
-    slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, n_seeds, (uint32_t)r0, nc, h->n_wl, h->d_ctl,
-                                                              h->d_lists);
+    slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc, h->n_wl,
+                                                              h->d_ctl, h->d_lists);
     CUDA_TRY(h, cudaGetLastError());
     uint64_t blocks = (uint64_t)bps * h->sm_count;
     const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);
@@ -325,6 +338,13 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     if (blocks < 1) blocks = 1;
     slo::slo_sim_kernel<<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
     CUDA_TRY(h, cudaGetLastError());
+    if (h->any_cont) {   // K1c: the continuous-batching list, one replica per warp
+      uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;
+      const uint64_t cneed = ((uint64_t)nc + h->warps_per_block - 1) / h->warps_per_block;
+      if (cblocks > cneed) cblocks = cneed;
+      slo::slo_sim_cont_kernel<<<(unsigned)cblocks, h->warps_per_block * 32, smem, st>>>(p);
+      CUDA_TRY(h, cudaGetLastError());
+    }
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
     slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
     CUDA_TRY(h, cudaGetLastError());

@@ -8,6 +8,10 @@ namespace slo {
 
 constexpr int kMaxWarpsPerBlock = 8;
 constexpr int kDefaultWarpsPerBlock = 4;
+// K0 work lists: lane groups G = 8, 16, 32 (static batching) and 3 = continuous batching (one replica/warp)
+constexpr int kLists = 4;
+// control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
+constexpr int kCtlBucket = 8, kCtlWords = kCtlBucket + 2 * 16 * kLists;
 
 struct DevWorkload {      // device copy of one slo_workload
   uint32_t kind, start_state;
@@ -16,7 +20,7 @@ struct DevWorkload {      // device copy of one slo_workload
   uint32_t p_lo, p_ncw, p_off;
   uint32_t o_lo, o_ncw, o_off;
   slo_timing t;
-  uint32_t stream_id, pad;
+  uint32_t stream_id, batching;
 };
 
 struct SimParams {
@@ -24,9 +28,9 @@ struct SimParams {
   const uint64_t* seeds;
   const DevWorkload* wl;
   const uint32_t* tables;
-  uint32_t* counts;            // [3] replicas per work list (K0); ctl[8..104) K0 bucket counters
-  uint32_t* cursor;            // [3] next list entry (K1)
-  const uint32_t* lists;       // [3][n_chunk] replica indices by lane-group size 8 / 16 / 32
+  uint32_t* counts;            // [kLists] replicas per work list (K0); ctl[8..) K0 bucket counters
+  uint32_t* cursor;            // [kLists] next list entry (K1)
+  const uint32_t* lists;       // [kLists][n_chunk] replica indices: G = 8 / 16 / 32, continuous
   uint32_t* lat;               // [n_chunk][N] stored latency of every request of the chunk's replicas
   slo_replica_result* part;    // [n_rep] K1 -> K1b (the caller's detail buffer when given)
   uint32_t* p99;
@@ -42,10 +46,11 @@ struct SimParams {
 };
 
 __global__ void slo_sim_kernel(const SimParams p);
-__global__ void slo_classify_count_kernel(const slo_knobs* cfg, uint32_t n_seeds, uint32_t r_base,
-                                          uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl);
-__global__ void slo_classify_kernel(const slo_knobs* cfg, uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk,
-                                    uint32_t n_wl, uint32_t* ctl, uint32_t* lists);
+__global__ void slo_sim_cont_kernel(const SimParams p);   // K1c: continuous batching
+__global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
+                                          uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl);
+__global__ void slo_classify_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds, uint32_t r_base,
+                                    uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl, uint32_t* lists);
 __global__ void slo_select_kernel(const SimParams p, uint32_t smem_vals);
 size_t group_warp_bytes();   // per-warp shared memory of K1
 __global__ void slo_aggregate_kernel(const slo_replica_result* detail, uint32_t n_cfg, uint32_t n_seeds,

@@ -61,6 +61,17 @@ __device__ __forceinline__ uint32_t gmax(uint32_t v) {
   return v;
 }
 template <int G>
+__device__ __forceinline__ uint64_t gmax64(uint64_t v) {
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) {
+    const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m, G);
+    const uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), m, G);
+    const uint64_t o = ((uint64_t)hi << 32) | lo;
+    v = o > v ? o : v;
+  }
+  return v;
+}
+template <int G>
 __device__ __forceinline__ uint32_t gsum(uint32_t v) {
 #pragma unroll
   for (int m = G / 2; m >= 1; m >>= 1) v += __shfl_xor_sync(FULL, v, m, G);
@@ -562,8 +573,12 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
       const uint32_t slo_met = gsum<G>(my_slo & 0x7FFFFFFFu);
       const uint64_t sum = gsum64<G>(my_sum);
       const bool sat = gballot<G>((my_slo >> 31) != 0, lane) != 0;
+      // the window ends at the last MEASURED completion (§2.8): all earlier batches ended before this one
+      // formed, so it is the largest c among this last batch's measured members (not t_idle, which may be
+      // a warmup member's completion when the segment is shorter than the batch)
+      const uint64_t cm = gmax64<G>(measured ? c : 0ull);
       if (fin && li == 0) {
-        const uint64_t Tw = t_idle - R.a_w;
+        const uint64_t Tw = cm - R.a_w;
         p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
         if (p.stats) {
           unsigned long long* st = (unsigned long long*)p.stats;
@@ -575,6 +590,194 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
       if (fin) active = false;
     }
     if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u) flush_counters(p, ct);  // rare
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// continuous (iteration-level, vLLM-style) batching: one replica per warp, lane = slot of
+// the running set R (|R| <= B <= 32).  The server's free instants are iteration ends and, when it idles,
+// the next issue; at each of them the gate's closed form s_j = max(a_j, kappa_{j-C}) (which holds for any
+// service order, since issue is in index order and completions only free slots) gives the queue, a ballot
+// counts it, and the warp runs one prefill or decode iteration.  Per decode iteration every running lane
+// takes its next acceptance draw from a per-lane FIFO of precomputed A values (refilled 4 steps = one SPEC
+// block at a time, pooled: when any lane runs dry, every lane with room refills in the same pass).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
+  constexpr int RING = Group<32>::RING;
+  Group<32>& R = *reinterpret_cast<Group<32>*>(wsmem);
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const uint32_t N = p.warmup + p.seg;
+  const uint32_t count = p.counts[cls];
+  const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
+
+  for (;;) {
+    __syncwarp();
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(p.cursor + cls, 1u);
+    idx = __shfl_sync(FULL, idx, 0);
+    if (idx >= count) break;
+    const uint32_t r = list[idx];
+    const uint32_t ci = r / p.n_seeds;
+    const slo_knobs k = p.cfg[ci];
+    if (!knobs_valid(k, p.n_wl)) {   // (K0 puts invalid records in list 0; kept for safety)
+      if (lane == 0) {
+        p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+        if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+      }
+      continue;
+    }
+    const DevWorkload& W = p.wl[k.workload];
+    const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+    const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+    const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+    uint32_t gp;
+    if (lane == 0) R.wl = k.workload;
+    setup_replica<32>(R, W, k, k0, k1, gamma, gp, lane, FULL);
+    const uint32_t C = k.conc, B = k.max_num_seqs;
+    const bool closed = W.kind == 3;
+    const uint32_t noise = W.t.noise_step_ppm;
+    const uint64_t alpha0 = R.alpha0, alpha1 = R.alpha1;
+    const uint32_t pre_base = W.t.pre_base_us, pre_tok = W.t.pre_tok_us;
+    const uint32_t rowoff = (r - p.r_base) * N;
+
+    uint64_t t = 0, cmax = 0, a_w = 0;
+    uint32_t nq = 0, ndone = 0, gen = 0, it = 0, nzw = 0;
+    // lane = one slot of the running set
+    bool run = false;
+    uint32_t mi = 0, rem = 0, steps = 0, q = 0, acnt = 0;
+    uint64_t origin = 0, abuf = 0;
+    uint32_t my_slo = 0;
+    uint64_t my_sum = 0;
+
+    while (ndone < N) {
+      __syncwarp();   // ring writes of the previous iteration before this iteration's reads
+      // (a2, a3) keep [nq, nq + 32) generated
+      while (gen < N && gen < nq + 32u) {
+        generate<32>(R, p.wl, k.workload, p.tables, k0, k1, gen, N, p.warmup, true, lane, lane);
+        gen += 32;
+      }
+      // (a4) queue at t: issued (s_j <= t), not yet admitted, j in [nq, min(N, ndone + C))
+      const uint32_t j = nq + (uint32_t)lane;
+      const uint32_t lim = min(N, ndone + C);
+      uint64_t sj = INF64;
+      if (j < lim) {
+        const uint64_t aj = R.a[j % RING];
+        const uint64_t kj = j >= C ? R.kap[(j - C) % RING] : 0;
+        sj = aj > kj ? aj : kj;
+      }
+      const uint32_t avail = __popc(__ballot_sync(FULL, sj <= t));
+      const uint32_t runmask = __ballot_sync(FULL, run);
+      const uint32_t nrun = __popc(runmask);
+      if (nrun < B && avail > 0) {
+        // ---- prefill iteration: admit the first k queued requests into free slots
+        const uint32_t kk = min(B - nrun, avail);
+        const uint32_t rank = __popc(~runmask & lanemask_lt);
+        const bool adm = !run && rank < kk;
+        const uint64_t s_r = shfl64(sj, (int)(rank & 31u));
+        uint32_t P = 0;
+        if (adm) {
+          const uint32_t i = nq + rank;
+          const uint32_t po = R.po[i % RING];
+          P = po & 0xFFFFu;
+          mi = i;
+          rem = po >> 16;
+          origin = closed ? s_r : R.a[i % RING];
+          steps = 0;
+          q = 0;
+          acnt = 0;
+          abuf = 0;
+          run = true;
+        }
+        if (closed && p.warmup >= nq && p.warmup < nq + kk) a_w = shfl64(sj, (int)((p.warmup - nq) & 31u));
+        const uint32_t maxP = __reduce_max_sync(FULL, P);
+        const uint32_t w3h = R.w3[nq % RING];
+        const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
+        const uint64_t f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+        t += f * ((uint64_t)pre_base + (uint64_t)pre_tok * maxP) / 1000000u;
+        nq += kk;
+        if (lane == 0) ct.batches += 1;
+      } else if (nrun > 0) {
+        // ---- decode iteration over the running set
+        uint64_t f = 1000000u;
+        if (noise) {
+          if ((it & 31u) == 0) nzw = philox(it + (uint32_t)lane, 3, 0, 0, k0, k1).x;   // ITER blocks, 32 ahead
+          const uint32_t w = __shfl_sync(FULL, nzw, (int)(it & 31u));
+          const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
+          f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+        }
+        t += f * (alpha0 + alpha1 * nrun) / 1000000u;
+        uint32_t e = 1;
+        if (gamma > 0) {
+          if (__any_sync(FULL, run && acnt == 0)) {     // pooled refill: every lane with room takes a block
+            if (run && acnt <= 4) {
+              const u32x4 w = philox(mi, 1, q, 0, k0, k1);
+              uint32_t g0 = R.guide[w.x >> 24], g1 = R.guide[w.y >> 24];
+              uint32_t g2 = R.guide[w.z >> 24], g3 = R.guide[w.w >> 24];
+              if ((g0 | g1 | g2 | g3) & 0x80u) {
+                g0 = accepted(R, w.x, gp);
+                g1 = accepted(R, w.y, gp);
+                g2 = accepted(R, w.z, gp);
+                g3 = accepted(R, w.w, gp);
+              }
+              const uint32_t pk = (g0 & 0x7Fu) | ((g1 & 0x7Fu) << 8) | ((g2 & 0x7Fu) << 16) | ((g3 & 0x7Fu) << 24);
+              abuf |= (uint64_t)pk << (8u * acnt);
+              acnt += 4;
+              ++q;
+            }
+          }
+          const uint32_t A = (uint32_t)abuf & 0xFFu;
+          abuf >>= 8;
+          --acnt;
+          e = min(A + 1u, rem);
+        }
+        if (run) {
+          rem -= e;
+          ++steps;
+        }
+        const bool fin = run && rem == 0;
+        const uint32_t finmask = __ballot_sync(FULL, fin);
+        const uint32_t nf = __popc(finmask);
+        if (fin) {                                     // (a8) completions at t
+          const uint64_t l = t - origin;
+          p.lat[rowoff + mi] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
+          if (mi >= p.warmup) {
+            my_slo += (l <= p.slo_us);
+            my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
+            my_sum += l;
+          }
+          ct.steps += steps;
+          ct.blocks += gamma > 0 ? (steps + 3u) >> 2 : 0u;
+          run = false;
+        }
+        if (__any_sync(FULL, fin && mi >= p.warmup)) cmax = t;
+        if ((uint32_t)lane < nf) R.kap[(ndone + lane) % RING] = t;
+        ndone += nf;
+        ++it;
+        if (lane == 0) {
+          ct.dsteps += 1;
+          ct.blocks += noise ? 1u : 0u;
+        }
+      } else {
+        t = shfl64(sj, 0);                             // idle until the next issue, s_nq
+      }
+      if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u) flush_counters(p, ct);  // rare
+    }
+    // ---- replica outputs (p99 and goodput follow in K1b)
+    const uint32_t slo_met = gsum<32>(my_slo & 0x7FFFFFFFu);
+    const uint64_t sum = gsum64<32>(my_sum);
+    const bool sat = __ballot_sync(FULL, (my_slo >> 31) != 0) != 0;
+    if (lane == 0) {
+      const uint64_t a0 = closed ? a_w : R.a_w;
+      const uint64_t Tw = cmax - a0;
+      p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
+      if (p.stats) {
+        unsigned long long* st = (unsigned long long*)p.stats;
+        atomicAdd(st + 0, (unsigned long long)N);
+        atomicAdd(st + 4, (unsigned long long)(N + R.nphase));
+        atomicAdd(st + 5, 1ull);
+      }
+    }
   }
 }
 
@@ -603,6 +806,29 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
   }
 }
 
+// K1c: the continuous-batching work list, launched only when a workload uses it
+#ifndef SLO_CONT_MAXNREG
+#define SLO_CONT_MAXNREG 96
+#endif
+__global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel(const SimParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
+  Counters ct{0, 0, 0, 0};
+  run_cont(p, 3, wsmem, lane, ct);
+  if (p.stats) {
+    const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
+    const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
+    if (lane == 0) {
+      unsigned long long* st = (unsigned long long*)p.stats;
+      atomicAdd(st + 1, (unsigned long long)batches);
+      atomicAdd(st + 2, (unsigned long long)dsteps);
+      atomicAdd(st + 3, (unsigned long long)steps);
+      atomicAdd(st + 4, (unsigned long long)blocks);
+    }
+  }
+}
+
 size_t group_warp_bytes() {
   size_t m = 4 * sizeof(Group<8>);
   if (2 * sizeof(Group<16>) > m) m = 2 * sizeof(Group<16>);
@@ -616,7 +842,8 @@ size_t group_warp_bytes() {
 // Expected cost ~ (batches per segment) x (cost per batch); a saturated replica runs ~N / min(C, B) batches
 // and a speculative batch costs ~3x a plain one.  bucket = floor(log2(beff^2)) (+3 ~ 2 log2 3 if not
 // speculative), so bucket 0 = most expensive; invalid records (no work) go last.
-__device__ __forceinline__ uint32_t work_class(const slo_knobs& k, uint32_t n_wl, uint32_t& bucket) {
+__device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWorkload* __restrict__ wl, uint32_t n_wl,
+                                               uint32_t& bucket) {
   if (!knobs_valid(k, n_wl)) {
     bucket = 15;
     return 0;
@@ -625,27 +852,32 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, uint32_t n_wl
   const uint32_t beff = min((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
   const bool spec = k.spec_on && k.draft_len > 0;
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
+  if (wl[k.workload].batching) {      // continuous batching: one replica per warp, ~N*O/beff iterations
+    bucket = min(14u, (31u - __clz(beff)) + (spec ? 0u : 2u));
+    return 3u;
+  }
   return need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
 }
 
-__global__ void slo_classify_count_kernel(const slo_knobs* __restrict__ cfg, uint32_t n_seeds, uint32_t r_base,
-                                          uint32_t n_chunk, uint32_t n_wl, uint32_t* __restrict__ ctl) {
+__global__ void slo_classify_count_kernel(const slo_knobs* __restrict__ cfg, const DevWorkload* __restrict__ wl,
+                                          uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk, uint32_t n_wl,
+                                          uint32_t* __restrict__ ctl) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_chunk) return;
   uint32_t bucket;
-  const uint32_t cls = work_class(cfg[(r_base + t) / n_seeds], n_wl, bucket);
-  atomicAdd(ctl + 8 + cls * 16 + bucket, 1u);     // ctl[8 + 48): per (class, bucket) counts
+  const uint32_t cls = work_class(cfg[(r_base + t) / n_seeds], wl, n_wl, bucket);
+  atomicAdd(ctl + kCtlBucket + cls * 16 + bucket, 1u);     // per (class, bucket) counts
 }
 
-__global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, uint32_t n_seeds, uint32_t r_base,
-                                    uint32_t n_chunk, uint32_t n_wl, uint32_t* __restrict__ ctl,
-                                    uint32_t* __restrict__ lists) {
-  __shared__ uint32_t off[48];
-  if (threadIdx.x < 3) {                           // exclusive offsets of the buckets inside each list
+__global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, const DevWorkload* __restrict__ wl,
+                                    uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk, uint32_t n_wl,
+                                    uint32_t* __restrict__ ctl, uint32_t* __restrict__ lists) {
+  __shared__ uint32_t off[16 * kLists];
+  if (threadIdx.x < kLists) {                      // exclusive offsets of the buckets inside each list
     uint32_t acc = 0;
     for (int bkt = 0; bkt < 16; ++bkt) {
       off[threadIdx.x * 16 + bkt] = acc;
-      acc += ctl[8 + threadIdx.x * 16 + bkt];
+      acc += ctl[kCtlBucket + threadIdx.x * 16 + bkt];
     }
     if (blockIdx.x == 0) ctl[threadIdx.x] = acc;   // list lengths (read by K1)
   }
@@ -654,8 +886,8 @@ __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, uint32_t 
   if (t >= n_chunk) return;
   const uint32_t r = r_base + t;
   uint32_t bucket;
-  const uint32_t cls = work_class(cfg[r / n_seeds], n_wl, bucket);
-  const uint32_t pos = off[cls * 16 + bucket] + atomicAdd(ctl + 56 + cls * 16 + bucket, 1u);
+  const uint32_t cls = work_class(cfg[r / n_seeds], wl, n_wl, bucket);
+  const uint32_t pos = off[cls * 16 + bucket] + atomicAdd(ctl + kCtlBucket + 16 * kLists + cls * 16 + bucket, 1u);
   lists[(size_t)cls * n_chunk + pos] = r;
 }
 

@@ -207,6 +207,12 @@ def config_c2(n_seeds=64, segment_len=10_000) -> Config:
     return Config("C2", [preset_ll()], ks, n_seeds, segment_len)
 
 
+def config_c2_cont(n_seeds=64, segment_len=10_000) -> Config:
+    """C2's knob grid with continuous (iteration-level) batching (SV §8(f) NEXT-2)."""
+    c = config_c2(n_seeds, segment_len)
+    return Config("C2-cont", [continuous(preset_ll())], c.knobs, n_seeds, segment_len)
+
+
 def config_c3(n_seeds=256, segment_len=10_000) -> Config:
     """C3: draft length 0-8 x acceptance .3-.9, C = B = 8 (K0), 256 seeds."""
     ks = []

@@ -129,6 +129,7 @@ class Simulator:
             for f, v in d["timing"].items():
                 setattr(w.timing, f, v)
             w.stream_id = d["stream_id"]
+            w.batching = d.get("batching", 0)
         opts = _lib.slo_sim_opts()
         opts.crn, opts.warps_per_block, opts.blocks_per_sm = crn, warps_per_block, blocks_per_sm
         opts.scratch_mb = scratch_mb

@@ -319,3 +319,91 @@ def test_climb_cuda_graph_matches_eager(S):
     torch.cuda.synchronize()
     assert torch.equal(st_e, st_g) and torch.equal(c_e, c_g)
     s.close()
+
+
+def test_short_segment_window_ends_at_last_measured_completion(S, orc):
+    """Segments shorter than a batch with warmup: the goodput window T ends at the last MEASURED completion
+    (DESIGN.md §2.8), which can precede a warmup member's completion in the same final batch."""
+    wls = [inputs.preset_ll(rate=100.0), inputs.workload(kind=0, rate=400.0)]
+    ks = [inputs.knobs(conc=16, max_num_seqs=16), inputs.knobs(conc=32, max_num_seqs=32, workload=1),
+          inputs.knobs(conc=8, max_num_seqs=8, draft_len=4, spec_on=1)]
+    seeds = inputs.seeds(40, 4321)
+    for N, warm in ((1, 3), (2, 5), (3, 4), (5, 10)):
+        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm)
+        for ci, k in enumerate(ks):
+            for si, sd in enumerate(seeds):
+                _compare_replica(orc, g, ci * len(seeds) + si, wls, k, sd, N, warm, 1_200_000)
+
+
+def _wls_cont():
+    """Continuous-batching workloads next to a static one in the same handle, so one launch
+    runs K1 and K1c side by side."""
+    c = inputs.continuous
+    return [c(inputs.preset_ll()), c(inputs.preset_sim()), c(inputs.preset_stress(kind=1)),
+            c(inputs.preset_stress(kind=2)), c(inputs.preset_ll(rate=40.0, stream_id=7)),
+            c(inputs.preset_closed(stream_id=3)), inputs.preset_ll(rate=20.0, stream_id=9),
+            c(inputs.workload(kind=0, rate=200.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0), stream_id=5))]
+
+
+@pytest.mark.parametrize("block", range(6))
+def test_continuous_random_configs(S, orc, block):
+    """Continuous batching: random knob records over every arrival kind (incl. the closed loop), noise on
+    and off, speculation, several 32-request windows, ragged tails and warmup — every latency, p50/p95/p99,
+    goodput and the work counters bit-exact against the oracle's iteration-level event loop."""
+    rng = random.Random(900 + block)
+    wls = _wls_cont()
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)]
+    ks[0] = inputs.knobs(conc=32, max_num_seqs=32, draft_len=16, spec_on=1, accept_q16=65536, workload=1)
+    ks[1] = inputs.knobs(conc=1, max_num_seqs=1, draft_len=16, spec_on=1, accept_q16=0)
+    ks[2] = inputs.knobs(conc=32, max_num_seqs=1, workload=2)
+    ks[3] = inputs.knobs(conc=1, max_num_seqs=32, workload=3)
+    ks[4] = inputs.knobs(conc=24, max_num_seqs=6, draft_len=4, spec_on=1, workload=5)       # closed loop
+    ks[5] = inputs.knobs(conc=32, max_num_seqs=32, workload=7, draft_len=5, spec_on=1)      # no noise, overload
+    ks[6] = inputs.knobs(conc=8, max_num_seqs=8, workload=6)                                # static, same launch
+    seeds = inputs.seeds(3, 31 * block)
+    N = rng.choice([37, 333, 1000, 1234])
+    warmup = rng.choice([0, 0, 17, 100])
+    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup)
+    tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
+    for ci, k in enumerate(ks):
+        for si, sd in enumerate(seeds):
+            ref = _compare_replica(orc, g, ci * len(seeds) + si, wls, k, sd, N, warmup, 1_200_000)
+            for f in tot:
+                tot[f] += ref["counters"][f]
+    for f in tot:
+        assert int(g["stats"][f]) == tot[f], f
+
+
+def test_continuous_edge_cases(S, orc):
+    """Continuous batching at degenerate sizes: one request, N < 32, exactly 32/33/65, short segments with a
+    long warmup, B = 1 (pinned equal to static batching), invalid records mixed in."""
+    wls = _wls_cont()
+    ks = [inputs.knobs(conc=8, max_num_seqs=16), inputs.knobs(conc=0), inputs.knobs(max_num_seqs=1, conc=4),
+          inputs.knobs(conc=32, max_num_seqs=32, workload=7), inputs.knobs(conc=3, max_num_seqs=2, workload=7,
+                                                                            draft_len=3, spec_on=1),
+          inputs.knobs(conc=16, max_num_seqs=4, workload=5, draft_len=8, spec_on=1, draft_width=3)]
+    seeds = inputs.seeds(3, 1900)
+    for N, warm in ((1, 0), (1, 5), (2, 5), (31, 0), (32, 1), (33, 0), (65, 64)):
+        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm)
+        for ci, k in enumerate(ks):
+            for si, sd in enumerate(seeds):
+                r = ci * len(seeds) + si
+                if not orc.knobs_valid(k, len(wls)):
+                    assert int(g["p99"][r]) == 0xFFFFFFFF and g["gp"][r] == -1.0 and g["detail"][r]["flags"] == 1
+                    continue
+                _compare_replica(orc, g, r, wls, k, sd, N, warm, 1_200_000)
+
+
+def test_continuous_full_size_sampled(S, orc):
+    """The C2 knob grid served with continuous batching at full size (32,768 replicas x 10k requests) in the
+    bench's launch configuration; sampled replicas bit-exact, properties on all."""
+    cfg = inputs.config_c2_cont()
+    g = _run_gpu(S, cfg.workloads, cfg.knobs, cfg.seeds(), cfg.segment_len, latencies=False)
+    rng = random.Random(12)
+    for ci in _sample_rows(len(cfg.knobs), 12, rng, must=(0, len(cfg.knobs) - 1)):
+        si = rng.randrange(cfg.n_seeds)
+        _compare_replica(orc, g, ci * cfg.n_seeds + si, cfg.workloads, cfg.knobs[ci], cfg.seeds()[si],
+                         cfg.segment_len, 0, cfg.slo_us, check_lat=False)
+    d = g["detail"]
+    assert np.all(d["slo_met"] <= d["n_measured"]) and np.all(d["flags"] & 1 == 0)
+    assert int(g["stats"]["requests"]) == cfg.requests
