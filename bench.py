@@ -30,6 +30,8 @@ DESCR = {
     "c2": "C2 knob grid 16 concurrency x 8 batch limits x 4 speculation settings x 64 seeds, 10k-request segments",
     "c3": "C3 speculative sweep: draft length 0-8 x acceptance .3-.9, C=B=8, 256 seeds, 10k-request segments",
     "c4": "C4 hill-climb step: 32 candidates (wide-32 stencil) x 128 seeds, 5k-request segments",
+    "c2c": "C2 knob grid (16 C x 8 B x 4 spec x 64 seeds, 10k-request segments) served with continuous "
+           "(iteration-level, vLLM-style) batching, DESIGN.md 2.12",
     "c5": "C5 stress grid slice: MMPP-2 bursty arrivals, 65,536 configs x 16 seeds, 2k-request segments",
 }
 # Philox4x32-10 minimum integer lane-ops per block: 10 rounds x (2 widening multiplies + 2 three-input
@@ -43,6 +45,8 @@ def make_config(name):
         return inputs.config_c1()
     if name == "c2":
         return inputs.config_c2()
+    if name == "c2c":
+        return inputs.config_c2_cont()
     if name == "c3":
         return inputs.config_c3()
     if name == "c4":
@@ -250,6 +254,8 @@ def main():
     st_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     # K0 count + K0 classify + K1 simulate + K1b select + K2 aggregate (+ K2b for N>1 sweeps, K3 for the climb)
     launches_per_step = 5 + (1 if (world > 1 and args.workload != "c4") else 0) + (1 if args.workload == "c4" else 0)
+    if any(w.get("batching", 0) for w in cfg.workloads):
+        launches_per_step += 1                                          # K1c (continuous batching)
 
     graph = None
     if args.workload == "c4" and not args.eager_climb and (world == 1 or dist.get_backend() == "nccl"):
@@ -366,8 +372,10 @@ def main():
                                       "decode_steps": int(stats["decode_steps"])},
             "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
                          "frac": achieved_gops / peak_gops, "traffic": traffic,
-                         "kernel": "slo_sim_run_batch = K0 classify + K1 simulate + K1b p99 select (K1 dominates, "
-                                   "see profiles/ launch list)",
+                         "kernel": ("slo_sim_run_batch = K0 classify + K1c continuous-batching simulate + K1b p99 "
+                                    "select (K1c dominates)" if args.workload == "c2c" else
+                                    "slo_sim_run_batch = K0 classify + K1 simulate + K1b p99 select (K1 dominates, "
+                                    "see profiles/ launch list)"),
                          "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
                                  "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)"},
             "gpu_launches": launches_per_step * args.steps,

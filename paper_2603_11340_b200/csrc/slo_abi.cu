@@ -308,13 +308,16 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int bps = blocks_per_sm_for(h, smem);
   int cont_bps = 1;
+  slo::SimParams pc{};
+  const size_t cont_smem = slo::cont_warp_bytes() * h->warps_per_block;
   if (h->any_cont) {
-    if (smem > 48 * 1024)
+    if (cont_smem > 48 * 1024)
       CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+                                       (int)cont_smem));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel, h->warps_per_block * 32,
-                                                      smem) != cudaSuccess || cont_bps < 1)
+                                                      cont_smem) != cudaSuccess || cont_bps < 1)
       cont_bps = 1;
+    if (h->blocks_per_sm_opt > 0 && h->blocks_per_sm_opt < cont_bps) cont_bps = h->blocks_per_sm_opt;
   }
   const uint32_t sel_vals = segment_len <= 11008u ? segment_len : 0u;   // stage rows up to 43 KB in smem
   const size_t sel_smem = (256u + sel_vals) * sizeof(uint32_t);
@@ -342,7 +345,9 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;
       const uint64_t cneed = ((uint64_t)nc + h->warps_per_block - 1) / h->warps_per_block;
       if (cblocks > cneed) cblocks = cneed;
-      slo::slo_sim_cont_kernel<<<(unsigned)cblocks, h->warps_per_block * 32, smem, st>>>(p);
+      pc = p;
+      pc.warp_bytes = (uint32_t)slo::cont_warp_bytes();
+      slo::slo_sim_cont_kernel<<<(unsigned)cblocks, h->warps_per_block * 32, cont_smem, st>>>(pc);
       CUDA_TRY(h, cudaGetLastError());
     }
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;

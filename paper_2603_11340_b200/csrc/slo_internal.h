@@ -8,10 +8,11 @@ namespace slo {
 
 constexpr int kMaxWarpsPerBlock = 8;
 constexpr int kDefaultWarpsPerBlock = 4;
-// K0 work lists: lane groups G = 8, 16, 32 (static batching) and 3 = continuous batching (one replica/warp)
-constexpr int kLists = 4;
+// K0 work lists: static batching by lane-group size G = 8, 16, 32 >= max(C, B) (K1), then continuous
+// batching by G = 8, 16, 32 >= B (K1c)
+constexpr int kLists = 6;
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
-constexpr int kCtlBucket = 8, kCtlWords = kCtlBucket + 2 * 16 * kLists;
+constexpr int kCtlBucket = 16, kCtlWords = kCtlBucket + 2 * 16 * kLists;
 
 struct DevWorkload {      // device copy of one slo_workload
   uint32_t kind, start_state;
@@ -53,6 +54,7 @@ __global__ void slo_classify_kernel(const slo_knobs* cfg, const DevWorkload* wl,
                                     uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl, uint32_t* lists);
 __global__ void slo_select_kernel(const SimParams p, uint32_t smem_vals);
 size_t group_warp_bytes();   // per-warp shared memory of K1
+size_t cont_warp_bytes();    // per-warp shared memory of K1c
 __global__ void slo_aggregate_kernel(const slo_replica_result* detail, uint32_t n_cfg, uint32_t n_seeds,
                                      slo_config_agg* agg);
 __global__ void slo_aggregate_reduce_kernel(const slo_config_agg* parts, uint32_t n_parts, uint32_t n_cfg,

@@ -109,8 +109,8 @@ struct alignas(16) Group {
 };
 
 // A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
-template <int G>
-__device__ __forceinline__ uint32_t accepted(const Group<G>& R, uint32_t u, uint32_t gp) {
+template <class GR>
+__device__ __forceinline__ uint32_t accepted(const GR& R, uint32_t u, uint32_t gp) {
   const uint32_t g = R.guide[u >> 24];
   uint32_t A = g & 0x7Fu;
   if (g & 0x80u) {
@@ -212,8 +212,8 @@ __device__ __forceinline__ uint32_t spec_steps(const Group<G>* Rw, uint8_t* slot
 }
 
 // (a1) set up a newly acquired replica (group-convergent; other groups do not enter)
-template <int G>
-__device__ __forceinline__ void setup_replica(Group<G>& R, const DevWorkload& W, const slo_knobs& k, uint32_t k0,
+template <int G, class GR>
+__device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const slo_knobs& k, uint32_t k0,
                                               uint32_t k1, uint32_t gamma, uint32_t& gp, int li, uint32_t gmask) {
   gp = 0;
   {
@@ -286,8 +286,8 @@ __device__ __forceinline__ void setup_replica(Group<G>& R, const DevWorkload& W,
 }
 
 // (a2, a3) generate requests [gen, gen + G) for every group with `go` (all lanes execute)
-template <int G>
-__device__ __forceinline__ void generate(Group<G>& R, const DevWorkload* __restrict__ wls, uint32_t wl,
+template <int G, class GR>
+__device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ wls, uint32_t wl,
                                          const uint32_t* __restrict__ tables, uint32_t k0, uint32_t k1, uint32_t gen,
                                          uint32_t N, uint32_t warmup, bool go, int lane, int li) {
   const uint32_t i = gen + (uint32_t)li;
@@ -344,9 +344,9 @@ __device__ __forceinline__ void generate(Group<G>& R, const DevWorkload* __restr
     const DevWorkload& W = wls[wl];
     const uint32_t P = length_of(tables + W.p_off, W.p_ncw, W.p_lo, w.y);
     const uint32_t O = length_of(tables + W.o_off, W.o_ncw, W.o_lo, w.z);
-    R.a[i % Group<G>::RING] = a;
-    R.po[i % Group<G>::RING] = P | (O << 16);
-    R.w3[i % Group<G>::RING] = w.w;
+    R.a[i % GR::RING] = a;
+    R.po[i % GR::RING] = P | (O << 16);
+    R.w3[i % GR::RING] = w.w;
     if (i == warmup) R.a_w = a;
   }
   __syncwarp();
@@ -594,189 +594,281 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 }
 
 // ------------------------------------------------------------------------------------------------
-// continuous (iteration-level, vLLM-style) batching: one replica per warp, lane = slot of
-// the running set R (|R| <= B <= 32).  The server's free instants are iteration ends and, when it idles,
-// the next issue; at each of them the gate's closed form s_j = max(a_j, kappa_{j-C}) (which holds for any
-// service order, since issue is in index order and completions only free slots) gives the queue, a ballot
-// counts it, and the warp runs one prefill or decode iteration.  Per decode iteration every running lane
-// takes its next acceptance draw from a per-lane FIFO of precomputed A values (refilled 4 steps = one SPEC
-// block at a time, pooled: when any lane runs dry, every lane with room refills in the same pass).
+// K1c: continuous (iteration-level, vLLM-style) batching, DESIGN.md §2.12.
+//
+// A warp runs 32/G replicas at once, one per G-lane group with G >= B (lane = one slot of the running set
+// R, |R| <= B).  The server's free instants are iteration ends and, when it idles, the next issue.  The
+// gate's closed form s_j = max(a_j, kappa_{j-C}) holds for any service order (issue is in index order and
+// completions only free slots), so a group keeps s_next = s_{nq} (the next request to admit) and:
+//   * prefill iteration iff |R| < B and s_next <= t: a ballot over the window j = nq + li counts the queue,
+//     the first k = min(B - |R|, queue) requests take the free slots;
+//   * else decode iteration iff |R| > 0: every running lane takes its next acceptance draw, completions at
+//     the iteration end fill kappa;
+//   * else idle until s_next.
+// Random words are consumed from pooled per-lane buffers: a FIFO of up to 8 accepted-prefix values per slot
+// (refilled one SPEC block = 4 decode steps at a time; when any slot runs dry every slot with room refills
+// in the same pass) and a window of the next G decode-iteration noise words per group (ITER blocks; when
+// any group exhausts its window every group shifts its window and refills the consumed part).
 // ------------------------------------------------------------------------------------------------
+template <int G>
+struct alignas(16) CGroup {
+  static constexpr int RING = 4 * G;   // a, po, w3 for [nq, gen), gen < nq + 2G
+  static constexpr int KRING = 64;     // kappa_k for k in [nq - C, ndone): span <= C + B <= 64
+  uint64_t a[RING];
+  uint64_t kap[KRING];
+  uint32_t po[RING];
+  uint32_t w3[RING];
+  uint32_t tm1[16];
+  uint8_t guide[256];
+  uint64_t g[2], rho[2];
+  uint64_t last;
+  uint64_t pstart, pD, pU, pLam, nphase, a_w, alpha0, alpha1;
+  uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, gp;
+  uint32_t k0, k1, wl, pad;
+};
+
+template <int G>
 __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
-  constexpr int RING = Group<32>::RING;
-  Group<32>& R = *reinterpret_cast<Group<32>*>(wsmem);
-  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  using CG = CGroup<G>;
+  constexpr int RING = CG::RING, KRING = CG::KRING;
+  const int g = lane / G, li = lane % G;
+  CG& R = reinterpret_cast<CG*>(wsmem)[g];
+  const uint32_t gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
+  const uint32_t ltg = (1u << li) - 1u;                 // group-relative lanes below this one
   const uint32_t N = p.warmup + p.seg;
   const uint32_t count = p.counts[cls];
   const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
 
+  // group-uniform state (every lane of a group holds the same value)
+  uint32_t r = 0, rowoff = 0, nq = 0, ndone = 0, gen = 0, it = 0, nrun = 0, npre = 0;
+  uint32_t C = 0, B = 0, gamma = 0, noise = 0, k0 = 0, k1 = 0;
+  uint64_t t = 0, s_next = INF64, a_w = 0;
+  bool active = false, exhausted = false, need_s = false, closed = false;
+  // slot state (lane = one slot of the running set)
+  bool run = false;
+  uint32_t mi = 0, rem = 0, steps = 0, q = 0, acnt = 0, nzw = 0, nzc = 0, my_slo = 0;
+  uint64_t origin = 0, abuf = 0, my_sum = 0, my_cmax = 0;
+
   for (;;) {
     __syncwarp();
-    uint32_t idx = 0;
-    if (lane == 0) idx = atomicAdd(p.cursor + cls, 1u);
-    idx = __shfl_sync(FULL, idx, 0);
-    if (idx >= count) break;
-    const uint32_t r = list[idx];
-    const uint32_t ci = r / p.n_seeds;
-    const slo_knobs k = p.cfg[ci];
-    if (!knobs_valid(k, p.n_wl)) {   // (K0 puts invalid records in list 0; kept for safety)
-      if (lane == 0) {
-        p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
-        if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+    // ---- acquire replicas for idle groups
+    bool want = !active && !exhausted;
+    while (__any_sync(FULL, want)) {
+      uint32_t idx = 0;
+      if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
+      idx = gshfl<G>(idx, 0);
+      if (want) {
+        if (idx >= count) {
+          exhausted = true;
+        } else {
+          r = list[idx];
+          const uint32_t ci = r / p.n_seeds;
+          const slo_knobs k = p.cfg[ci];
+          if (!knobs_valid(k, p.n_wl)) {   // (K0 puts invalid records in list 0; kept for safety)
+            if (li == 0) {
+              p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+              if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+            }
+          } else {
+            const DevWorkload& W = p.wl[k.workload];
+            const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+            const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+            k0 = (uint32_t)seed;
+            k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+            gamma = k.spec_on ? k.draft_len : 0u;
+            uint32_t gp;
+            if (li == 0) R.wl = k.workload;
+            setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
+            C = k.conc;
+            B = k.max_num_seqs;
+            closed = W.kind == 3;
+            noise = W.t.noise_step_ppm;
+            rowoff = (r - p.r_base) * N;
+            t = 0;
+            s_next = INF64;
+            a_w = 0;
+            nq = ndone = gen = it = nrun = npre = 0;
+            nzc = G;                                     // noise window empty: filled at the first decode
+            run = false;
+            my_slo = 0;
+            my_sum = 0;
+            my_cmax = 0;
+            need_s = true;
+            active = true;
+          }
+        }
       }
-      continue;
+      want = !active && !exhausted;
     }
-    const DevWorkload& W = p.wl[k.workload];
-    const uint64_t seed = p.seeds[r - ci * p.n_seeds];
-    const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
-    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
-    const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
-    uint32_t gp;
-    if (lane == 0) R.wl = k.workload;
-    setup_replica<32>(R, W, k, k0, k1, gamma, gp, lane, FULL);
-    const uint32_t C = k.conc, B = k.max_num_seqs;
-    const bool closed = W.kind == 3;
-    const uint32_t noise = W.t.noise_step_ppm;
-    const uint64_t alpha0 = R.alpha0, alpha1 = R.alpha1;
-    const uint32_t pre_base = W.t.pre_base_us, pre_tok = W.t.pre_tok_us;
-    const uint32_t rowoff = (r - p.r_base) * N;
+    if (!__any_sync(FULL, active)) break;
+    __syncwarp();   // setup / previous iteration's ring writes before this iteration's reads
 
-    uint64_t t = 0, cmax = 0, a_w = 0;
-    uint32_t nq = 0, ndone = 0, gen = 0, it = 0, nzw = 0;
-    // lane = one slot of the running set
-    bool run = false;
-    uint32_t mi = 0, rem = 0, steps = 0, q = 0, acnt = 0;
-    uint64_t origin = 0, abuf = 0;
-    uint32_t my_slo = 0;
-    uint64_t my_sum = 0;
-
-    while (ndone < N) {
-      __syncwarp();   // ring writes of the previous iteration before this iteration's reads
-      // (a2, a3) keep [nq, nq + 32) generated
-      while (gen < N && gen < nq + 32u) {
-        generate<32>(R, p.wl, k.workload, p.tables, k0, k1, gen, N, p.warmup, true, lane, lane);
-        gen += 32;
+    // ---- s_next = s_{nq} for groups whose nq or gate changed; keep [nq, nq + G) generated
+    if (__any_sync(FULL, need_s)) {
+      bool gn = need_s && gen < N && gen < nq + G;
+      while (__any_sync(FULL, gn)) {
+        generate<G>(R, p.wl, R.wl, p.tables, k0, k1, gen, N, p.warmup, gn, lane, li);
+        if (gn) gen += G;
+        gn = need_s && gen < N && gen < nq + G;
       }
-      // (a4) queue at t: issued (s_j <= t), not yet admitted, j in [nq, min(N, ndone + C))
-      const uint32_t j = nq + (uint32_t)lane;
-      const uint32_t lim = min(N, ndone + C);
+      if (need_s) {
+        s_next = INF64;
+        if (nq < min(N, ndone + C)) {
+          const uint64_t aj = R.a[nq % RING];
+          const uint64_t kj = nq >= C ? R.kap[(nq - C) % KRING] : 0;
+          s_next = aj > kj ? aj : kj;
+        }
+        need_s = false;
+      }
+    }
+    if (active && nrun == 0 && s_next > t) t = s_next;   // idle until the next issue
+    const bool pre = active && nrun < B && s_next <= t;
+    const bool dec = active && !pre && nrun > 0;
+
+    // ---- prefill iteration: admit the first k queued requests into free slots (§2.12)
+    if (__any_sync(FULL, pre)) {
+      const uint32_t j = nq + (uint32_t)li;
       uint64_t sj = INF64;
-      if (j < lim) {
+      if (pre && j < min(N, ndone + C)) {
         const uint64_t aj = R.a[j % RING];
-        const uint64_t kj = j >= C ? R.kap[(j - C) % RING] : 0;
+        const uint64_t kj = j >= C ? R.kap[(j - C) % KRING] : 0;
         sj = aj > kj ? aj : kj;
       }
-      const uint32_t avail = __popc(__ballot_sync(FULL, sj <= t));
-      const uint32_t runmask = __ballot_sync(FULL, run);
-      const uint32_t nrun = __popc(runmask);
-      if (nrun < B && avail > 0) {
-        // ---- prefill iteration: admit the first k queued requests into free slots
-        const uint32_t kk = min(B - nrun, avail);
-        const uint32_t rank = __popc(~runmask & lanemask_lt);
-        const bool adm = !run && rank < kk;
-        const uint64_t s_r = shfl64(sj, (int)(rank & 31u));
-        uint32_t P = 0;
-        if (adm) {
-          const uint32_t i = nq + rank;
-          const uint32_t po = R.po[i % RING];
-          P = po & 0xFFFFu;
-          mi = i;
-          rem = po >> 16;
-          origin = closed ? s_r : R.a[i % RING];
-          steps = 0;
-          q = 0;
-          acnt = 0;
-          abuf = 0;
-          run = true;
-        }
-        if (closed && p.warmup >= nq && p.warmup < nq + kk) a_w = shfl64(sj, (int)((p.warmup - nq) & 31u));
-        const uint32_t maxP = __reduce_max_sync(FULL, P);
+      const uint32_t avail = __popc(gballot<G>(sj <= t, lane));
+      const uint32_t runm = gballot<G>(run, lane);
+      const uint32_t kk = pre ? min(B - nrun, avail) : 0u;
+      const uint32_t rank = __popc(~runm & ltg);
+      const bool adm = pre && !run && rank < kk;
+      const uint64_t s_r = gshfl64<G>(sj, (int)(rank & (G - 1)));
+      uint32_t P = 0;
+      if (adm) {
+        const uint32_t i = nq + rank;
+        const uint32_t po = R.po[i % RING];
+        P = po & 0xFFFFu;
+        mi = i;
+        rem = po >> 16;
+        origin = closed ? s_r : R.a[i % RING];
+        steps = 0;
+        q = 0;
+        acnt = 0;
+        abuf = 0;
+        run = true;
+      }
+      const bool wsrc = pre && closed && p.warmup >= nq && p.warmup < nq + kk;
+      if (__any_sync(FULL, wsrc)) {                      // closed loop: the window starts at s_warmup
+        const uint64_t sw = gshfl64<G>(sj, (int)((p.warmup - nq) & (G - 1)));
+        if (wsrc) a_w = sw;
+      }
+      const uint32_t maxP = gmax<G>(P);
+      if (pre) {
         const uint32_t w3h = R.w3[nq % RING];
         const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
         const uint64_t f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
-        t += f * ((uint64_t)pre_base + (uint64_t)pre_tok * maxP) / 1000000u;
+        t += f * ((uint64_t)R.pre_base + (uint64_t)R.pre_tok * maxP) / 1000000u;
         nq += kk;
-        if (lane == 0) ct.batches += 1;
-      } else if (nrun > 0) {
-        // ---- decode iteration over the running set
-        uint64_t f = 1000000u;
-        if (noise) {
-          if ((it & 31u) == 0) nzw = philox(it + (uint32_t)lane, 3, 0, 0, k0, k1).x;   // ITER blocks, 32 ahead
-          const uint32_t w = __shfl_sync(FULL, nzw, (int)(it & 31u));
-          const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
-          f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+        nrun += kk;
+        ++npre;
+        need_s = true;
+      }
+    }
+
+    // ---- decode iteration over the running set
+    if (__any_sync(FULL, dec)) {
+      uint64_t f = 1000000u;
+      const bool nz = dec && noise != 0;
+      if (__any_sync(FULL, nz && nzc >= (uint32_t)G)) {  // pooled shift-refill of the noise windows
+        const uint32_t src = (uint32_t)li + nzc;
+        const uint32_t sh = __shfl_sync(FULL, nzw, (int)(src & (G - 1)), G);
+        if (nz && nzc > 0) {
+          nzw = src < (uint32_t)G ? sh : philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x;   // ITER block it + li
+          nzc = 0;
         }
-        t += f * (alpha0 + alpha1 * nrun) / 1000000u;
-        uint32_t e = 1;
-        if (gamma > 0) {
-          if (__any_sync(FULL, run && acnt == 0)) {     // pooled refill: every lane with room takes a block
-            if (run && acnt <= 4) {
-              const u32x4 w = philox(mi, 1, q, 0, k0, k1);
-              uint32_t g0 = R.guide[w.x >> 24], g1 = R.guide[w.y >> 24];
-              uint32_t g2 = R.guide[w.z >> 24], g3 = R.guide[w.w >> 24];
-              if ((g0 | g1 | g2 | g3) & 0x80u) {
-                g0 = accepted(R, w.x, gp);
-                g1 = accepted(R, w.y, gp);
-                g2 = accepted(R, w.z, gp);
-                g3 = accepted(R, w.w, gp);
-              }
-              const uint32_t pk = (g0 & 0x7Fu) | ((g1 & 0x7Fu) << 8) | ((g2 & 0x7Fu) << 16) | ((g3 & 0x7Fu) << 24);
-              abuf |= (uint64_t)pk << (8u * acnt);
-              acnt += 4;
-              ++q;
-            }
+      }
+      const uint32_t w = __shfl_sync(FULL, nzw, (int)(nzc & (G - 1)), G);
+      if (nz) {
+        const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
+        f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+        ++nzc;
+      }
+      if (dec) t += f * (R.alpha0 + R.alpha1 * nrun) / 1000000u;
+      const bool sp = dec && run && gamma > 0;
+      uint32_t e = 1;
+      if (__any_sync(FULL, sp && acnt == 0)) {           // pooled refill: every slot with room takes a block
+        if (sp && acnt <= 4) {
+          const u32x4 wb = philox(mi, 1, q, 0, k0, k1);
+          uint32_t g0 = R.guide[wb.x >> 24], g1 = R.guide[wb.y >> 24];
+          uint32_t g2 = R.guide[wb.z >> 24], g3 = R.guide[wb.w >> 24];
+          if ((g0 | g1 | g2 | g3) & 0x80u) {             // a threshold inside one of the buckets (rare)
+            const uint32_t gp = R.gp;
+            g0 = accepted(R, wb.x, gp);
+            g1 = accepted(R, wb.y, gp);
+            g2 = accepted(R, wb.z, gp);
+            g3 = accepted(R, wb.w, gp);
           }
-          const uint32_t A = (uint32_t)abuf & 0xFFu;
-          abuf >>= 8;
-          --acnt;
-          e = min(A + 1u, rem);
+          const uint32_t pk = (g0 & 0x7Fu) | ((g1 & 0x7Fu) << 8) | ((g2 & 0x7Fu) << 16) | ((g3 & 0x7Fu) << 24);
+          abuf |= (uint64_t)pk << (8u * acnt);
+          acnt += 4;
+          ++q;
         }
-        if (run) {
-          rem -= e;
-          ++steps;
-        }
-        const bool fin = run && rem == 0;
-        const uint32_t finmask = __ballot_sync(FULL, fin);
-        const uint32_t nf = __popc(finmask);
-        if (fin) {                                     // (a8) completions at t
+      }
+      if (sp) {
+        const uint32_t A = (uint32_t)abuf & 0xFFu;
+        abuf >>= 8;
+        --acnt;
+        e = min(A + 1u, rem);
+      }
+      if (dec && run) {
+        rem -= e;
+        ++steps;
+      }
+      const bool fin = dec && run && rem == 0;
+      if (__any_sync(FULL, fin)) {
+        const uint32_t nf = __popc(gballot<G>(fin, lane));
+        if (fin) {                                       // (a8) completion at t
           const uint64_t l = t - origin;
           p.lat[rowoff + mi] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
           if (mi >= p.warmup) {
             my_slo += (l <= p.slo_us);
             my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
             my_sum += l;
+            my_cmax = t;
           }
           ct.steps += steps;
           ct.blocks += gamma > 0 ? (steps + 3u) >> 2 : 0u;
           run = false;
         }
-        if (__any_sync(FULL, fin && mi >= p.warmup)) cmax = t;
-        if ((uint32_t)lane < nf) R.kap[(ndone + lane) % RING] = t;
-        ndone += nf;
-        ++it;
-        if (lane == 0) {
-          ct.dsteps += 1;
-          ct.blocks += noise ? 1u : 0u;
+        if (dec && (uint32_t)li < nf) R.kap[(ndone + li) % KRING] = t;
+        if (dec) {
+          ndone += nf;
+          nrun -= nf;
+          if (s_next == INF64 && nq < N) need_s = true;  // completions may have opened the gate for nq
         }
-      } else {
-        t = shfl64(sj, 0);                             // idle until the next issue, s_nq
       }
-      if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u) flush_counters(p, ct);  // rare
+      if (dec) ++it;
     }
-    // ---- replica outputs (p99 and goodput follow in K1b)
-    const uint32_t slo_met = gsum<32>(my_slo & 0x7FFFFFFFu);
-    const uint64_t sum = gsum64<32>(my_sum);
-    const bool sat = __ballot_sync(FULL, (my_slo >> 31) != 0) != 0;
-    if (lane == 0) {
-      const uint64_t a0 = closed ? a_w : R.a_w;
-      const uint64_t Tw = cmax - a0;
-      p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
-      if (p.stats) {
-        unsigned long long* st = (unsigned long long*)p.stats;
-        atomicAdd(st + 0, (unsigned long long)N);
-        atomicAdd(st + 4, (unsigned long long)(N + R.nphase));
-        atomicAdd(st + 5, 1ull);
+
+    // ---- groups that finished their replica: outputs (p99 and goodput follow in K1b)
+    const bool done = active && ndone >= N;
+    if (__any_sync(FULL, done)) {
+      const uint32_t slo_met = gsum<G>(my_slo & 0x7FFFFFFFu);
+      const uint64_t sum = gsum64<G>(my_sum);
+      const uint64_t cm = gmax64<G>(my_cmax);
+      const bool sat = gballot<G>((my_slo >> 31) != 0, lane) != 0;
+      if (done && li == 0) {
+        const uint64_t Tw = cm - (closed ? a_w : R.a_w);
+        p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
+        ct.batches += npre;
+        ct.dsteps += it;
+        ct.blocks += noise ? it : 0u;
+        if (p.stats) {
+          unsigned long long* st = (unsigned long long*)p.stats;
+          atomicAdd(st + 0, (unsigned long long)N);
+          atomicAdd(st + 4, (unsigned long long)(N + R.nphase));
+          atomicAdd(st + 5, 1ull);
+        }
       }
+      if (done) active = false;
+      if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u || ct.blocks >= 0x40000000u) flush_counters(p, ct);
     }
   }
 }
@@ -815,7 +907,9 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel(const SimParam
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
-  run_cont(p, 3, wsmem, lane, ct);
+  run_cont<8>(p, 3, wsmem, lane, ct);
+  run_cont<16>(p, 4, wsmem, lane, ct);
+  run_cont<32>(p, 5, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -827,6 +921,13 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel(const SimParam
       atomicAdd(st + 4, (unsigned long long)blocks);
     }
   }
+}
+
+size_t cont_warp_bytes() {
+  size_t m = 4 * sizeof(CGroup<8>);
+  if (2 * sizeof(CGroup<16>) > m) m = 2 * sizeof(CGroup<16>);
+  if (sizeof(CGroup<32>) > m) m = sizeof(CGroup<32>);
+  return m;
 }
 
 size_t group_warp_bytes() {
@@ -852,9 +953,9 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
   const uint32_t beff = min((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
   const bool spec = k.spec_on && k.draft_len > 0;
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
-  if (wl[k.workload].batching) {      // continuous batching: one replica per warp, ~N*O/beff iterations
+  if (wl[k.workload].batching) {      // continuous batching: lane groups G >= B, ~N*O/beff iterations
     bucket = min(14u, (31u - __clz(beff)) + (spec ? 0u : 2u));
-    return 3u;
+    return k.max_num_seqs <= 8 ? 3u : (k.max_num_seqs <= 16 ? 4u : 5u);
   }
   return need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
 }
