@@ -72,6 +72,12 @@ __device__ __forceinline__ uint64_t gmax64(uint64_t v) {
   return v;
 }
 template <int G>
+__device__ __forceinline__ uint32_t gmin(uint32_t v) {
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) v = min(v, __shfl_xor_sync(FULL, v, m, G));
+  return v;
+}
+template <int G>
 __device__ __forceinline__ uint32_t gsum(uint32_t v) {
 #pragma unroll
   for (int m = G / 2; m >= 1; m >>= 1) v += __shfl_xor_sync(FULL, v, m, G);
@@ -641,12 +647,12 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
 
   // group-uniform state (every lane of a group holds the same value)
   uint32_t r = 0, rowoff = 0, nq = 0, ndone = 0, gen = 0, it = 0, nrun = 0, npre = 0;
-  uint32_t C = 0, B = 0, gamma = 0, noise = 0, k0 = 0, k1 = 0;
+  uint32_t C = 0, B = 0, gamma = 0, noise = 0, k0 = 0, k1 = 0, alpha0 = 0, alpha1 = 0;
   uint64_t t = 0, s_next = INF64, a_w = 0;
   bool active = false, exhausted = false, need_s = false, closed = false;
   // slot state (lane = one slot of the running set)
   bool run = false;
-  uint32_t mi = 0, rem = 0, steps = 0, q = 0, acnt = 0, nzw = 0, nzc = 0, my_slo = 0;
+  uint32_t mi = 0, rem = 0, steps = 0, q = 0, acnt = 0, fw = 0, nzc = 0, my_slo = 0;   // fw: noise window
   uint64_t origin = 0, abuf = 0, my_sum = 0, my_cmax = 0;
 
   for (;;) {
@@ -683,6 +689,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             B = k.max_num_seqs;
             closed = W.kind == 3;
             noise = W.t.noise_step_ppm;
+            alpha0 = (uint32_t)R.alpha0;                 // d(n) = alpha0 + alpha1 n
+            alpha1 = (uint32_t)R.alpha1;
             rowoff = (r - p.r_base) * N;
             t = 0;
             s_next = INF64;
@@ -772,27 +780,31 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       }
     }
 
-    // ---- decode iteration over the running set
+    // ---- decode iterations over the running set, fast-forwarded to the next event.  While no member
+    // finishes and no prefill can start, consecutive decode iterations change nothing but t, the members'
+    // token counts and the random-word cursors, so a group advances K of them at once: lane k holds the
+    // duration of iteration it + k (D_k = floor(f_k d(n) / 10^6), d(n) = alpha0 + alpha1 n), a group scan
+    // gives their end times, and
+    //   K = min(first iteration at whose end a member finishes,
+    //           first iteration at whose end a prefill can start (|R| < B and s_next <= end),
+    //           the iterations whose random words are buffered).
     if (__any_sync(FULL, dec)) {
-      uint64_t f = 1000000u;
       const bool nz = dec && noise != 0;
-      if (__any_sync(FULL, nz && nzc >= (uint32_t)G)) {  // pooled shift-refill of the noise windows
+      if (__any_sync(FULL, nz && nzc > (uint32_t)(G / 2))) {   // pooled shift-refill of the noise windows
         const uint32_t src = (uint32_t)li + nzc;
-        const uint32_t sh = __shfl_sync(FULL, nzw, (int)(src & (G - 1)), G);
+        const uint32_t sh = __shfl_sync(FULL, fw, (int)(src & (G - 1)), G);
         if (nz && nzc > 0) {
-          nzw = src < (uint32_t)G ? sh : philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x;   // ITER block it + li
+          if (src < (uint32_t)G) {
+            fw = sh;
+          } else {                                       // ITER block it + li, word 0 (§2.12)
+            const uint32_t w = philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x;
+            const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
+            fw = (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+          }
           nzc = 0;
         }
       }
-      const uint32_t w = __shfl_sync(FULL, nzw, (int)(nzc & (G - 1)), G);
-      if (nz) {
-        const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
-        f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
-        ++nzc;
-      }
-      if (dec) t += f * (R.alpha0 + R.alpha1 * nrun) / 1000000u;
       const bool sp = dec && run && gamma > 0;
-      uint32_t e = 1;
       if (__any_sync(FULL, sp && acnt == 0)) {           // pooled refill: every slot with room takes a block
         if (sp && acnt <= 4) {
           const u32x4 wb = philox(mi, 1, q, 0, k0, k1);
@@ -811,17 +823,56 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           ++q;
         }
       }
-      if (sp) {
-        const uint32_t A = (uint32_t)abuf & 0xFFu;
-        abuf >>= 8;
-        --acnt;
-        e = min(A + 1u, rem);
-      }
+      // end times of the next iterations: lane k <-> iteration it + k
+      const uint32_t d = alpha0 + alpha1 * nrun;          // < 2^31 (timing values < 2^20, gamma <= 16)
+      const uint32_t fk = __shfl_sync(FULL, fw, (int)(((uint32_t)li + nzc) & (G - 1)), G);
+      const uint32_t Dk = nz ? (uint32_t)(((uint64_t)fk * d) / 1000000u) : d;
+      const uint64_t cum = gscan64<G>((uint64_t)Dk, li);
+      // iterations until each running member finishes (within its buffered draws)
+      uint32_t Sm = 0xFFFFu, av = 0xFFFFu;
       if (dec && run) {
-        rem -= e;
-        ++steps;
+        if (gamma == 0) {
+          Sm = rem;
+        } else {
+          av = acnt;
+          uint32_t c = 0;
+          uint64_t b = abuf;
+          for (uint32_t i = 0; i < acnt; ++i) {
+            c += ((uint32_t)b & 0xFFu) + 1u;
+            b >>= 8;
+            if (c >= rem) {
+              Sm = i + 1;
+              break;
+            }
+          }
+        }
       }
-      const bool fin = dec && run && rem == 0;
+      uint32_t K = min(gmin<G>(Sm), gmin<G>(av));
+      K = min(K, nz ? (uint32_t)G - nzc : (uint32_t)G);
+      const bool open = dec && nrun < B && (uint32_t)li < K && t + cum >= s_next;   // s_next = INF: never
+      const uint32_t om = gballot<G>(open, lane);
+      if (om) K = (uint32_t)__ffs(om);                    // the first such iteration end (lanes < K only)
+      const uint64_t tK = gshfl64<G>(cum, (int)((K - 1u) & (G - 1)));
+      bool fin = false;
+      if (dec) {
+        t += tK;
+        it += K;
+        if (nz) nzc += K;
+        if (run) {
+          steps += K;
+          if (Sm == K) {
+            fin = true;
+          } else if (gamma == 0) {
+            rem -= K;
+          } else {
+            for (uint32_t i = 0; i < K; ++i) {
+              rem -= ((uint32_t)abuf & 0xFFu) + 1u;
+              abuf >>= 8;
+            }
+            acnt -= K;
+          }
+        }
+      }
       if (__any_sync(FULL, fin)) {
         const uint32_t nf = __popc(gballot<G>(fin, lane));
         if (fin) {                                       // (a8) completion at t
@@ -844,7 +895,6 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           if (s_next == INF64 && nq < N) need_s = true;  // completions may have opened the gate for nq
         }
       }
-      if (dec) ++it;
     }
 
     // ---- groups that finished their replica: outputs (p99 and goodput follow in K1b)
