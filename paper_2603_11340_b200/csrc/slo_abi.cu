@@ -314,6 +314,8 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     if (cont_smem > 48 * 1024)
       CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
+    // occupancy is register-bound; give the group rings the whole carveout so smem never binds first
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel, h->warps_per_block * 32,
                                                       cont_smem) != cudaSuccess || cont_bps < 1)
       cont_bps = 1;

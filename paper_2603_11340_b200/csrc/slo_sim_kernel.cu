@@ -829,21 +829,23 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       const uint32_t Dk = nz ? (uint32_t)(((uint64_t)fk * d) / 1000000u) : d;
       const uint64_t cum = gscan64<G>((uint64_t)Dk, li);
       // iterations until each running member finishes (within its buffered draws)
+      // speculative members: byte i of `pre` = tokens emitted by the next i + 1 steps, sum of (A + 1)
+      // (each A <= 16, so 8 prefix sums <= 136 stay inside their bytes: a SWAR prefix sum)
       uint32_t Sm = 0xFFFFu, av = 0xFFFFu;
+      uint64_t pre = abuf + 0x0101010101010101ull;
+      pre += pre << 8;
+      pre += pre << 16;
+      pre += pre << 32;
       if (dec && run) {
         if (gamma == 0) {
           Sm = rem;
         } else {
           av = acnt;
-          uint32_t c = 0;
-          uint64_t b = abuf;
-          for (uint32_t i = 0; i < acnt; ++i) {
-            c += ((uint32_t)b & 0xFFu) + 1u;
-            b >>= 8;
-            if (c >= rem) {
-              Sm = i + 1;
-              break;
-            }
+          if (rem <= 136u) {                             // first step i < acnt with prefix >= rem
+            const uint32_t rr = rem * 0x01010101u;
+            const uint32_t lo = __vcmpgeu4((uint32_t)pre, rr), hi = __vcmpgeu4((uint32_t)(pre >> 32), rr);
+            const uint64_t ge = (((uint64_t)hi << 32) | lo) & (acnt >= 8 ? ~0ull : ((1ull << (8 * acnt)) - 1ull));
+            if (ge) Sm = (uint32_t)(__ffsll((long long)ge) + 7) >> 3;
           }
         }
       }
@@ -865,10 +867,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           } else if (gamma == 0) {
             rem -= K;
           } else {
-            for (uint32_t i = 0; i < K; ++i) {
-              rem -= ((uint32_t)abuf & 0xFFu) + 1u;
-              abuf >>= 8;
-            }
+            rem -= (uint32_t)(pre >> (8 * (K - 1))) & 0xFFu;
+            abuf = K >= 8 ? 0ull : abuf >> (8 * K);
             acnt -= K;
           }
         }
