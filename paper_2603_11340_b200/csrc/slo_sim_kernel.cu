@@ -731,10 +731,16 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
     }
     if (active && nrun == 0 && s_next > t) t = s_next;   // idle until the next issue
     const bool pre = active && nrun < B && s_next <= t;
-    const bool dec = active && !pre && nrun > 0;
 
     // ---- prefill iteration: admit the first k queued requests into free slots (§2.12)
     if (__any_sync(FULL, pre)) {
+      bool gn = pre && gen < N && gen < nq + G;          // the window [nq, nq + G) must be generated
+      while (__any_sync(FULL, gn)) {
+        generate<G>(R, p.wl, R.wl, p.tables, k0, k1, gen, N, p.warmup, gn, lane, li);
+        if (gn) gen += G;
+        gn = pre && gen < N && gen < nq + G;
+      }
+      __syncwarp();
       const uint32_t j = nq + (uint32_t)li;
       uint64_t sj = INF64;
       if (pre && j < min(N, ndone + C)) {
@@ -768,6 +774,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         if (wsrc) a_w = sw;
       }
       const uint32_t maxP = gmax<G>(P);
+      // s_next = s_{nq + k} straight from the window (INF if beyond the gate); k = G: recompute at the top
+      const uint64_t sn = gshfl64<G>(sj, (int)(kk & (G - 1)));
       if (pre) {
         const uint32_t w3h = R.w3[nq % RING];
         const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
@@ -776,9 +784,12 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         nq += kk;
         nrun += kk;
         ++npre;
-        need_s = true;
+        s_next = sn;
+        if (kk == (uint32_t)G) need_s = true;
       }
     }
+    // a group that just prefilled decodes in the same pass unless another prefill is due at once
+    const bool dec = active && !need_s && nrun > 0 && !(nrun < B && s_next <= t);
 
     // ---- decode iterations over the running set, fast-forwarded to the next event.  While no member
     // finishes and no prefill can start, consecutive decode iterations change nothing but t, the members'
