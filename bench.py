@@ -321,26 +321,45 @@ def main():
     value = world * req_per_step * args.steps / t_total
 
     # ---- e2e: the public API on HOST buffers (pinned), H2D + D2H inside the timed region
-    hk = sim.knobs_tensor(cfg.knobs if args.workload != "c4" else sim.unpack_knobs(cands.cpu().numpy()),
-                          device="cpu").pin_memory()
-    hs = sim.seeds_tensor(seeds, device="cpu").pin_memory()
-    hout = dict(p99_us=torch.empty(R, dtype=torch.int32).pin_memory(),
-                goodput=torch.empty(R, dtype=torch.float64).pin_memory())
-    S.run_batch_host(hk, hs, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=hout)
-    e2e_steps = max(1, min(args.steps, 5))
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    if graph is not None:
+        # the climb as a caller runs it (ClimbGraph.run_host): starting candidates + climb state copied in
+        # from pinned host memory, then every step's climb state (the step's result) read back to the host
+        e2e_steps = max(1, args.steps)
+        h_c = graph.init_cands.cpu().pin_memory()
+        h_s = graph.init_state.cpu().pin_memory()
+        h_traj = torch.empty((e2e_steps, h_s.numel()), dtype=torch.uint8).pin_memory()
+        graph.run_host(1, h_c, h_s, h_traj)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        graph.run_host(e2e_steps, h_c, h_s, h_traj)
+        t_e2e = time.perf_counter() - t0
+        h2d = (h_c.numel() + h_s.numel()) / e2e_steps
+        d2h = h_s.numel()
+    else:
+        hk = sim.knobs_tensor(cfg.knobs if args.workload != "c4" else sim.unpack_knobs(cands.cpu().numpy()),
+                              device="cpu").pin_memory()
+        hs = sim.seeds_tensor(seeds, device="cpu").pin_memory()
+        hout = dict(p99_us=torch.empty(R, dtype=torch.int32).pin_memory(),
+                    goodput=torch.empty(R, dtype=torch.float64).pin_memory())
         S.run_batch_host(hk, hs, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=hout)
-    t_e2e = time.perf_counter() - t0
+        e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            S.run_batch_host(hk, hs, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=hout)
+        t_e2e = time.perf_counter() - t0
+        h2d = hk.numel() + hs.numel() * 8
+        d2h = R * 4 + R * 8
     if world > 1:
         te = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         t_e2e = te.item()
     e2e = {"value": world * req_per_step * e2e_steps / t_e2e, "unit": "requests/s",
-           "h2d_bytes_per_step": hk.numel() + hs.numel() * 8,
-           "d2h_bytes_per_step": R * 4 + R * 8}
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if graph is not None:
+        e2e["api"] = "dist.ClimbGraph.run_host: climb trajectory read back every step"
 
     if rank == 0:
         pk = peaks()

@@ -114,6 +114,23 @@ class ClimbGraph:
             self.graph.replay()
         return self.state, self.cands
 
+    def run_host(self, steps: int, h_cands: torch.Tensor, h_state: torch.Tensor, h_traj: torch.Tensor):
+        """End-to-end use from host memory: copy the starting candidates and climb state in (pinned host ->
+        device), replay `steps` climb steps and read every step's climb state back into h_traj[step]
+        (pinned uint8 [steps, 104]) — the trajectory a caller observes.  Synchronous."""
+        if self.graph is None:
+            self.capture()
+        st = self.stream
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            self.cands.copy_(h_cands, non_blocking=True)
+            self.state.copy_(h_state, non_blocking=True)
+            for i in range(steps):
+                self.graph.replay()
+                h_traj[i].copy_(self.state.view(-1), non_blocking=True)
+        st.synchronize()
+        return h_traj
+
 
 def hillclimb(sim, cfg, steps: int, seeds: List[int], n_cand: int = 32, stream=None):
     """Device-resident Alg. 1 over `steps` iterations on this rank's seed slice; returns the final state.

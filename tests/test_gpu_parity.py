@@ -407,3 +407,22 @@ def test_continuous_full_size_sampled(S, orc):
     d = g["detail"]
     assert np.all(d["slo_met"] <= d["n_measured"]) and np.all(d["flags"] & 1 == 0)
     assert int(g["stats"]["requests"]) == cfg.requests
+
+
+def test_climb_run_host_trajectory(S):
+    """The end-to-end climb call (ClimbGraph.run_host, used by bench.py's c4 e2e): starting point copied in
+    from pinned host memory, every step's climb state read back — equal, step by step, to the eager loop."""
+    from paper_2603_11340_b200.dist import ClimbGraph, hillclimb
+    cfg = inputs.config_c4(n_seeds=4, segment_len=300)
+    s = S.Simulator(cfg.workloads, device=0)
+    g = ClimbGraph(s, cfg, cfg.seeds()).capture()
+    steps = 4
+    h_c = g.init_cands.cpu().pin_memory()
+    h_s = g.init_state.cpu().pin_memory()
+    traj = torch.empty((steps, h_s.numel()), dtype=torch.uint8).pin_memory()
+    g.run_host(steps, h_c, h_s, traj)
+    for i in range(steps):
+        st_e, _ = hillclimb(s, cfg, i + 1, cfg.seeds())
+        torch.cuda.synchronize()
+        assert torch.equal(traj[i], st_e.cpu().view(-1)), f"step {i}"
+    s.close()
