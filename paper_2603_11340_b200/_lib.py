@@ -50,7 +50,7 @@ class slo_workload(C.Structure):
 
 class slo_sim_opts(C.Structure):
     _fields_ = [("crn", C.c_uint32), ("warps_per_block", C.c_uint32), ("blocks_per_sm", C.c_uint32),
-                ("scratch_mb", C.c_uint32), ("reserved", C.c_uint32 * 4)]
+                ("scratch_mb", C.c_uint32), ("group_policy", C.c_uint32), ("reserved", C.c_uint32 * 3)]
 
 
 class slo_sim_info(C.Structure):

@@ -27,6 +27,7 @@ struct slo_sim {
   uint32_t n_wl = 0;
   uint32_t crn = 1;
   bool any_cont = false;            // a workload uses continuous batching: launch K1c
+  uint32_t group_policy = 0;        // slo_sim_opts.group_policy
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
   uint32_t* d_ctl = nullptr;        // [136]: list lengths [4], K1 cursors [4], K0 bucket counts/cursors [128]
@@ -126,8 +127,9 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   o.crn = 1;
   if (opts) {
     o = *opts;
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
       if (o.reserved[i]) return fail(nullptr, SLO_E_INVAL, "create: opts.reserved must be 0");
+    if (o.group_policy > 2) return fail(nullptr, SLO_E_INVAL, "create: opts.group_policy must be 0, 1 or 2");
     if (o.crn > 1) return fail(nullptr, SLO_E_INVAL, "create: opts.crn must be 0 or 1");
     if (o.warps_per_block > (uint32_t)slo::kMaxWarpsPerBlock)
       return fail(nullptr, SLO_E_INVAL, "create: warps_per_block > %d", slo::kMaxWarpsPerBlock);
@@ -200,6 +202,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
   if (o.scratch_mb) h->lat_budget = (size_t)o.scratch_mb << 20;
+  h->group_policy = o.group_policy;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel) == cudaSuccess) h->regs = fa.numRegs;
   cudaError_t e;
@@ -331,11 +334,16 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
     CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * slo::kCtlWords, st));
+    // a chunk with fewer replicas than resident warps cannot fill the GPU: K0 then picks wide lane groups
+    // (G >= max(C, B), shorter per-replica chains) instead of narrow ones (G >= min(C, B), more replicas/warp)
+    const uint32_t wide = h->group_policy == 2 ? 1u
+                          : h->group_policy == 1 ? 0u
+                          : (uint64_t)nc <= (uint64_t)bps * h->sm_count * h->warps_per_block ? 1u : 0u;
     slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
-                                                                    h->n_wl, h->d_ctl);
+                                                                    h->n_wl, wide, h->d_ctl);
     CUDA_TRY(h, cudaGetLastError());
     slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc, h->n_wl,
-                                                              h->d_ctl, h->d_lists);
+                                                              wide, h->d_ctl, h->d_lists);
     CUDA_TRY(h, cudaGetLastError());
     uint64_t blocks = (uint64_t)bps * h->sm_count;
     const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);

@@ -49,9 +49,10 @@ struct SimParams {
 __global__ void slo_sim_kernel(const SimParams p);
 __global__ void slo_sim_cont_kernel(const SimParams p);   // K1c: continuous batching
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
-                                          uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl);
+                                          uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t wide,
+                                          uint32_t* ctl);
 __global__ void slo_classify_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds, uint32_t r_base,
-                                    uint32_t n_chunk, uint32_t n_wl, uint32_t* ctl, uint32_t* lists);
+                                    uint32_t n_chunk, uint32_t n_wl, uint32_t wide, uint32_t* ctl, uint32_t* lists);
 __global__ void slo_select_kernel(const SimParams p, uint32_t smem_vals);
 size_t group_warp_bytes();   // per-warp shared memory of K1
 size_t cont_warp_bytes();    // per-warp shared memory of K1c

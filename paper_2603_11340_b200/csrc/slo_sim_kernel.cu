@@ -99,9 +99,10 @@ __device__ __forceinline__ uint64_t gsum64(uint64_t v) {
 // ------------------------------------------------------------------------------------------------
 template <int G>
 struct alignas(16) Group {
-  static constexpr int RING = 4 * G;  // holds [h - C, gen) with gen <= h + 3G
+  static constexpr int RING = 4 * G;  // a, po, w3 for [h, gen) with gen <= h + 3G
+  static constexpr int KRING = 4 * G > 64 ? 4 * G : 64;   // kappa for [h - C, h + b): C + b <= 64
   uint64_t a[RING];                   // arrival time of request j at a[j % RING]
-  uint64_t kap[RING];                 // kappa_k (k-th completion, ascending) at kap[k % RING]
+  uint64_t kap[KRING];                // kappa_k (k-th completion, ascending) at kap[k % KRING]
   uint32_t po[RING];                  // P | (O << 16)
   uint32_t w3[RING];                  // noise word
   uint32_t tm1[16];                   // T_a - 1, a = 1..gp
@@ -486,13 +487,15 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     uint64_t sj = INF64;
     if (active && (uint32_t)li < C && j < N) {
       const uint64_t aj = R.a[j % RING];
-      const uint64_t kj = j >= C ? R.kap[(j - C) % RING] : 0;
+      const uint64_t kj = j >= C ? R.kap[(j - C) % Group<G>::KRING] : 0;
       sj = aj > kj ? aj : kj;
     }
     // ---- (a5) formation instant and batch size
     const uint64_t sh = gshfl64<G>(sj, 0);
     uint64_t t_form = t_idle > sh ? t_idle : sh;
-    const uint64_t sl = gshfl64<G>(sj, (int)(B - 1) & (G - 1));    // INF if B > C or beyond N
+    // s_{h+B-1}: INF if B > C (the queue never holds B) or beyond N; B <= C implies B <= G (K0: G >= min(C, B))
+    const uint64_t slB = gshfl64<G>(sj, (int)(B - 1) & (G - 1));
+    const uint64_t sl = B > C ? INF64 : slB;
     if (mw > 0) {                                                 // (mw is group-uniform, not warp-uniform)
       const uint64_t dl = sh + mw;
       const uint64_t x = dl < sl ? dl : sl;
@@ -541,7 +544,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const uint32_t summin = incl - Sk + (b - (uint32_t)li) * Sk;
     const uint64_t cum = R.alpha0 * Sk + R.alpha1 * summin;
     const uint64_t c = t0 + (f * cum) / 1000000u;
-    if (member) R.kap[(h + li) % RING] = c;
+    if (member) R.kap[(h + li) % Group<G>::KRING] = c;
     const int lastm = (int)(b > 0 ? b - 1 : 0);
     const uint64_t tend = gshfl64<G>(c, lastm);
     const uint32_t maxS = gshfl<G>(Sk, lastm);
@@ -1005,13 +1008,17 @@ size_t group_warp_bytes() {
 // and a speculative batch costs ~3x a plain one.  bucket = floor(log2(beff^2)) (+3 ~ 2 log2 3 if not
 // speculative), so bucket 0 = most expensive; invalid records (no work) go last.
 __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWorkload* __restrict__ wl, uint32_t n_wl,
-                                               uint32_t& bucket) {
+                                               uint32_t wide, uint32_t& bucket) {
   if (!knobs_valid(k, n_wl)) {
     bucket = 15;
     return 0;
   }
-  const uint32_t need = max((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
+  // static batching needs G >= min(C, B) lanes: a batch has b <= min(C, B) members, the issue window
+  // only matters for them, and s_{h+B-1} is needed only when B <= C.  Narrow groups pack more replicas
+  // per warp (throughput); a launch too small to fill the GPU (`wide`) takes G >= max(C, B) instead, which
+  // shortens each replica's dependency chain (latency)
   const uint32_t beff = min((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
+  const uint32_t need = wide ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : beff;
   const bool spec = k.spec_on && k.draft_len > 0;
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
   if (wl[k.workload].batching) {      // continuous batching: lane groups G >= B, ~N*O/beff iterations
@@ -1023,17 +1030,17 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
 
 __global__ void slo_classify_count_kernel(const slo_knobs* __restrict__ cfg, const DevWorkload* __restrict__ wl,
                                           uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk, uint32_t n_wl,
-                                          uint32_t* __restrict__ ctl) {
+                                          uint32_t wide, uint32_t* __restrict__ ctl) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_chunk) return;
   uint32_t bucket;
-  const uint32_t cls = work_class(cfg[(r_base + t) / n_seeds], wl, n_wl, bucket);
+  const uint32_t cls = work_class(cfg[(r_base + t) / n_seeds], wl, n_wl, wide, bucket);
   atomicAdd(ctl + kCtlBucket + cls * 16 + bucket, 1u);     // per (class, bucket) counts
 }
 
 __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, const DevWorkload* __restrict__ wl,
                                     uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk, uint32_t n_wl,
-                                    uint32_t* __restrict__ ctl, uint32_t* __restrict__ lists) {
+                                    uint32_t wide, uint32_t* __restrict__ ctl, uint32_t* __restrict__ lists) {
   __shared__ uint32_t off[16 * kLists];
   if (threadIdx.x < kLists) {                      // exclusive offsets of the buckets inside each list
     uint32_t acc = 0;
@@ -1048,7 +1055,7 @@ __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, const Dev
   if (t >= n_chunk) return;
   const uint32_t r = r_base + t;
   uint32_t bucket;
-  const uint32_t cls = work_class(cfg[r / n_seeds], wl, n_wl, bucket);
+  const uint32_t cls = work_class(cfg[r / n_seeds], wl, n_wl, wide, bucket);
   const uint32_t pos = off[cls * 16 + bucket] + atomicAdd(ctl + kCtlBucket + 16 * kLists + cls * 16 + bucket, 1u);
   lists[(size_t)cls * n_chunk + pos] = r;
 }

@@ -105,7 +105,7 @@ class Simulator:
     """One libslosim handle on one CUDA device."""
 
     def __init__(self, workloads: Sequence[Dict], device: Optional[int] = None, crn: int = 1,
-                 warps_per_block: int = 0, blocks_per_sm: int = 0, scratch_mb: int = 0):
+                 warps_per_block: int = 0, blocks_per_sm: int = 0, scratch_mb: int = 0, group_policy: int = 0):
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
@@ -133,6 +133,7 @@ class Simulator:
         opts = _lib.slo_sim_opts()
         opts.crn, opts.warps_per_block, opts.blocks_per_sm = crn, warps_per_block, blocks_per_sm
         opts.scratch_mb = scratch_mb
+        opts.group_policy = group_policy
         h = C.c_void_p()
         check(lib().slo_sim_create(self.device, arr, n, C.byref(opts), C.byref(h)))
         self.h = h

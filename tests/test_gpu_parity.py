@@ -75,10 +75,12 @@ def _wls():
             inputs.preset_ll(rate=40.0, stream_id=7), inputs.preset_closed(stream_id=3)]
 
 
+@pytest.mark.parametrize("policy", [1, 2], ids=["narrow", "wide"])
 @pytest.mark.parametrize("block", range(6))
-def test_random_small_configs(S, orc, block):
+def test_random_small_configs(S, orc, block, policy):
     """Random valid knob records over every workload kind, lengths spanning several 32-request windows
-    and a ragged tail, warmup on/off — every latency and output bit-exact, plus the work counters."""
+    and a ragged tail, warmup on/off — every latency and output bit-exact, plus the work counters; in both
+    lane-group policies (narrow G >= min(C, B), the throughput default; wide G >= max(C, B))."""
     rng = random.Random(500 + block)
     wls = _wls()
     ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)]
@@ -89,9 +91,11 @@ def test_random_small_configs(S, orc, block):
     ks[4] = inputs.knobs(conc=24, max_num_seqs=6, draft_len=4, spec_on=1, workload=5)       # closed loop, G = 32
     ks[5] = inputs.knobs(conc=8, max_num_seqs=8, workload=5, max_wait_us=30_000)           # closed loop, G = 8
     seeds = inputs.seeds(3, 77 * block)
+    ks[6] = inputs.knobs(conc=32, max_num_seqs=8, draft_len=3, spec_on=1, workload=4)     # C + B = 40 > 4G
+    ks[7] = inputs.knobs(conc=30, max_num_seqs=2, max_wait_us=20_000, workload=4)
     N = rng.choice([37, 333, 1000, 1234])
     warmup = rng.choice([0, 0, 17, 100])
-    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup)
+    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup, group_policy=policy)
     tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
     for ci, k in enumerate(ks):
         for si, sd in enumerate(seeds):
@@ -102,7 +106,8 @@ def test_random_small_configs(S, orc, block):
         assert int(g["stats"][f]) == tot[f], f
 
 
-def test_edge_cases(S, orc):
+@pytest.mark.parametrize("policy", [1, 2], ids=["narrow", "wide"])
+def test_edge_cases(S, orc, policy):
     """Degenerate sizes and values: one request, N < 32, invalid records, saturating SLO, zero noise."""
     wls = [inputs.preset_ll(), inputs.workload(kind=0, rate=1000.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0))]
     ks = [inputs.knobs(conc=8, max_num_seqs=16), inputs.knobs(conc=0), inputs.knobs(max_num_seqs=33),
@@ -111,7 +116,7 @@ def test_edge_cases(S, orc):
                                                                           draft_len=3, spec_on=1)]
     seeds = inputs.seeds(2, 900)
     for N, warm in ((1, 0), (1, 5), (31, 0), (32, 1), (33, 0), (65, 64)):
-        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm)
+        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm, group_policy=policy)
         for ci, k in enumerate(ks):
             for si, sd in enumerate(seeds):
                 r = ci * len(seeds) + si
@@ -268,6 +273,9 @@ def test_launch_shapes_agree(S, orc):
     for wpb, bps in ((1, 1), (8, 0), (2, 3)):
         g = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=True, warps_per_block=wpb, blocks_per_sm=bps)
         assert np.array_equal(g["lat"], base["lat"]) and np.array_equal(g["gp"], base["gp"])
+    for pol in (1, 2):                                              # narrow / wide lane groups
+        g = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=True, group_policy=pol)
+        assert np.array_equal(g["lat"], base["lat"]) and g["detail"].tobytes() == base["detail"].tobytes()
     # latency-row scratch split into many launch chunks (1 MiB -> 524 replicas per chunk of 63 x 4 = 252... )
     base_nl = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=False)
     g = _run_gpu(S, wls, cfg.knobs, cfg.seeds(), 500, latencies=False, scratch_mb=1)
