@@ -223,9 +223,12 @@ def config_c3(n_seeds=256, segment_len=10_000) -> Config:
     return Config("C3", [preset_ll()], ks, n_seeds, segment_len)
 
 
-def config_c5(n_seeds=16, segment_len=2000, limit=None) -> Config:
-    """C5: STRESS grid 25 C x 25 B x 8 gamma x 5 alpha x 40 rate levels (2..80 req/s) = 10^6 configs."""
+def config_c5(n_seeds=16, segment_len=2000, limit=None, stride=1) -> Config:
+    """C5: STRESS grid 25 C x 25 B x 8 gamma x 5 alpha x 40 rate levels (2..80 req/s) = 10^6 configs.
+    `stride` keeps every stride-th config of the full grid (a sample spanning every knob), `limit` the first
+    `limit` configs after striding."""
     ks = []
+    idx = -1
     gam = (0, 1, 2, 3, 4, 6, 8, 12)
     alph = (0.3, 0.45, 0.6, 0.75, 0.9)
     rates = [2.0 + i * (78.0 / 39.0) for i in range(40)]
@@ -234,6 +237,9 @@ def config_c5(n_seeds=16, segment_len=2000, limit=None) -> Config:
             for g in gam:
                 for a in alph:
                     for r in rates:
+                        idx += 1
+                        if idx % stride:
+                            continue
                         ks.append(knobs(conc=c, max_num_seqs=b, draft_len=g, spec_on=1 if g else 0,
                                         accept_q16=q16(a), rate_scale_q8=max(1, int(round(r / 10.0 * 256)))))
                         if limit is not None and len(ks) >= limit:
