@@ -1021,9 +1021,11 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
   const uint32_t need = wide ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : beff;
   const bool spec = k.spec_on && k.draft_len > 0;
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
-  if (wl[k.workload].batching) {      // continuous batching: lane groups G >= B, ~N*O/beff iterations
+  if (wl[k.workload].batching) {      // continuous batching, ~N*O/beff iterations: lane groups G >= min(C, B)
+    // (at most min(C, B) requests run at once and a prefill admits at most that many; `wide`: G >= B)
     bucket = min(14u, (31u - __clz(beff)) + (spec ? 0u : 2u));
-    return k.max_num_seqs <= 8 ? 3u : (k.max_num_seqs <= 16 ? 4u : 5u);
+    const uint32_t cneed = wide ? (uint32_t)k.max_num_seqs : beff;
+    return cneed <= 8 ? 3u : (cneed <= 16 ? 4u : 5u);
   }
   return need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
 }

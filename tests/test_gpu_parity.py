@@ -354,8 +354,9 @@ def _wls_cont():
             c(inputs.workload(kind=0, rate=200.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0), stream_id=5))]
 
 
+@pytest.mark.parametrize("policy", [1, 2], ids=["narrow", "wide"])
 @pytest.mark.parametrize("block", range(6))
-def test_continuous_random_configs(S, orc, block):
+def test_continuous_random_configs(S, orc, block, policy):
     """Continuous batching: random knob records over every arrival kind (incl. the closed loop), noise on
     and off, speculation, several 32-request windows, ragged tails and warmup — every latency, p50/p95/p99,
     goodput and the work counters bit-exact against the oracle's iteration-level event loop."""
@@ -369,10 +370,12 @@ def test_continuous_random_configs(S, orc, block):
     ks[4] = inputs.knobs(conc=24, max_num_seqs=6, draft_len=4, spec_on=1, workload=5)       # closed loop
     ks[5] = inputs.knobs(conc=32, max_num_seqs=32, workload=7, draft_len=5, spec_on=1)      # no noise, overload
     ks[6] = inputs.knobs(conc=8, max_num_seqs=8, workload=6)                                # static, same launch
+    ks[7] = inputs.knobs(conc=3, max_num_seqs=32, workload=4, draft_len=6, spec_on=1)      # G >= min(C, B) = 3
+    ks[8] = inputs.knobs(conc=32, max_num_seqs=5, workload=5)                              # C + B > 4G
     seeds = inputs.seeds(3, 31 * block)
     N = rng.choice([37, 333, 1000, 1234])
     warmup = rng.choice([0, 0, 17, 100])
-    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup)
+    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup, group_policy=policy)
     tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
     for ci, k in enumerate(ks):
         for si, sd in enumerate(seeds):
