@@ -29,10 +29,10 @@ __all__ = ["Simulator", "pack_knobs", "knobs_tensor", "seeds_tensor", "neighbors
 # ------------------------------------------------------------------------------------------------
 def pack_knobs(knobs: Sequence[Dict]) -> np.ndarray:
     arr = np.zeros(len(knobs), KNOB_DTYPE)
+    for f in ("conc", "max_num_seqs", "draft_len", "spec_on", "draft_width", "workload", "rate_scale_q8",
+              "accept_q16", "max_wait_us"):
+        arr[f] = np.fromiter((k[f] for k in knobs), dtype=np.int64, count=len(knobs))
     for i, k in enumerate(knobs):
-        for f in ("conc", "max_num_seqs", "draft_len", "spec_on", "draft_width", "workload", "rate_scale_q8",
-                  "accept_q16", "max_wait_us"):
-            arr[i][f] = k[f]
         if "reserved" in k:
             arr[i]["reserved"] = k["reserved"]
     return arr
