@@ -178,6 +178,9 @@ def main():
     ap.add_argument("--warps-per-block", type=int, default=0, help="launch shape override (0 = library default)")
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--eager-climb", action="store_true", help="c4: host loop instead of the CUDA-graph step")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 aggregate exchange: p2p = K2x/K2w through CUDA IPC peer windows (NEXT-4), "
+                         "nccl = K2 + all_gather_into_tensor + K2b/K3 (also the fallback when p2p cannot map)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -269,12 +272,27 @@ def main():
     if any(w.get("batching", 0) for w in cfg.workloads):
         launches_per_step += 1                                          # K1c (continuous batching)
 
+    # N > 1: the aggregate exchange through the peers' windows (K2x/K2w, NEXT-4), NCCL as the fallback
+    xchg, exchange_desc = None, None
+    if world > 1:
+        exchange_desc = "nccl all_gather_into_tensor"
+        if args.exchange == "p2p":
+            try:
+                from paper_2603_11340_b200.dist import PeerExchange
+                if args.workload != "c4":
+                    xchg = PeerExchange(S, n_cfg)
+                exchange_desc = "p2p: K2x pushes into CUDA IPC peer windows, K2w waits on epoch flags"
+            except Exception as e:                                      # noqa: BLE001
+                exchange_desc = f"nccl all_gather_into_tensor (p2p unavailable: {str(e)[:120]})"
+                args.exchange = "nccl"
+        # (K2x + K2w replace K2 + K2b: the same launch count)
     graph = None
-    if args.workload == "c4" and not args.eager_climb and (world == 1 or dist.get_backend() == "nccl"):
+    if args.workload == "c4" and not args.eager_climb and (world == 1 or dist.get_backend() == "nccl"
+                                                          or args.exchange == "p2p"):
         from paper_2603_11340_b200.dist import ClimbGraph
-        graph = ClimbGraph(S, cfg, seeds, n_cand=n_cfg).capture()      # NEXT-4: one graph per climb step
+        graph = ClimbGraph(S, cfg, seeds, n_cand=n_cfg, exchange=args.exchange).capture()   # one graph per step
         out = graph.out                                                 # (replayed on the current stream)
-        launches_per_step = 6                                           # K0 x2, K1, K1b, K2, K3
+        launches_per_step = 6 + (1 if graph.xchg is not None else 0)    # K0 x2, K1, K1b, K2 (K2x+K2w), K3
 
     def step(i=None):
         if graph is not None:
@@ -290,6 +308,11 @@ def main():
         S.run_batch(cands, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out, stream=stream)
         if i is not None:
             k1_end[i].record(stream)
+        if xchg is not None:                                         # K2x + K2w: pooled over ranks
+            xchg.pooled(out["detail"], n_seeds_local, pooled, stream=stream)
+            if i is not None:
+                st_end[i].record(stream)
+            return
         S.aggregate(out["detail"], n_cfg, n_seeds_local, out=agg, stream=stream)
         if world > 1:
             if dist.get_backend() == "nccl":
@@ -388,6 +411,13 @@ def main():
     if graph is not None:
         e2e["api"] = "dist.ClimbGraph.run_host: climb trajectory read back every step"
 
+    x_err = 0
+    if world > 1:
+        xo = xchg if xchg is not None else (graph.xchg if graph is not None else None)
+        x_err = xo.error() if xo is not None else 0
+        te = torch.tensor([x_err], dtype=torch.int64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        x_err = int(te.item())
     if rank == 0:
         pk = peaks()
         blocks = int(stats["philox_blocks"])
@@ -409,6 +439,7 @@ def main():
                        "requests_per_step_per_gpu": req_per_step, "preset": "STRESS" if args.workload.startswith("c5") else "LL",
                        "l2": "flushed between timed steps (256 MiB write, untimed); inputs are < 1 MB",
                        "parallelism": f"dp{world} over replicas ({'seed-sharded climb' if args.workload == 'c4' else 'weak: full grid, per-rank seed block'})",
+                       "exchange": exchange_desc,
                        "launch": {"blocks_per_sm": info["blocks_per_sm"], "warps_per_block": info["warps_per_block"],
                                   "regs_per_thread": info["regs_per_thread"]}},
             "replica_segments_per_s": world * R * args.steps / t_total,
@@ -425,6 +456,7 @@ def main():
                          "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
                                  "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)"},
             "gpu_launches": launches_per_step * args.steps,
+            **({"exchange_error": x_err} if world > 1 else {}),
             "e2e": e2e,
             "clocks": clk,
         }
@@ -434,6 +466,11 @@ def main():
                                     "sample": f"{reps} replicas ({reqs} requests) of {args.workload.upper()} in "
                                               f"seed-major order, {dt:.1f} s on {cores} worker processes"}
         print(json.dumps(line))
+    if world > 1:
+        dist.barrier()                         # no rank still reads a peer window
+        for xo in (xchg, graph.xchg if graph is not None else None):
+            if xo is not None:
+                xo.close()
     S.close()
     if world > 1:
         dist.destroy_process_group()

@@ -227,6 +227,34 @@ slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_scor
                               uint32_t n_parts, slo_climb_state* d_state, int64_t* d_scores,
                               void* stream);
 
+/* ---- Peer exchange of the per-config aggregates (SV §8(f) NEXT-4) ----------------------
+ * The one exchange of the method — pooling the per-config aggregates over ranks before the score and the
+ * argmax (Eq. 1 pooled over seeds, R17; Alg. 1) — done by the aggregation kernel itself: every
+ * rank's K2x pushes its aggregates straight into every peer's exchange window over NVLink (CUDA IPC
+ * peer pointers, one process per GPU), then publishes an epoch flag; K2w waits for all flags and sums the
+ * parts in rank order (integer sums: bit-identical to the NCCL all-gather + slo_aggregate_reduce path).
+ * Windows are double-buffered by epoch parity, so a rank can never overwrite a part a peer has not read.
+ * Usage: slo_exchange_create on every rank -> all-gather the 64-byte handles (any transport, e.g. a
+ * torch.distributed group) -> slo_exchange_open -> slo_aggregate_exchange per step (stream-ordered, graph-
+ * capturable; all ranks must call it the same number of times).  A rank that waits > ~1 s for a peer gives
+ * up (results undefined) and latches an error readable with slo_exchange_error. */
+#define SLO_EXCHANGE_MAX_RANKS 16u
+#define SLO_EXCHANGE_HANDLE_BYTES 64u
+typedef struct slo_exchange slo_exchange;
+/* Allocate this rank's window for n_cfg aggregates among `world` ranks (2..16) on h's device and write its
+ * CUDA IPC handle (64 B) to h_handle_out.  Errors: SLO_E_INVAL, SLO_E_RANGE, SLO_E_NOMEM, SLO_E_CUDA. */
+slo_status slo_exchange_create(slo_sim* h, uint32_t world, uint32_t rank, uint32_t n_cfg, slo_exchange** out,
+                               void* h_handle_out);
+/* Map the peers' windows: h_handles = world x 64 B in rank order (this rank's own entry is ignored). */
+slo_status slo_exchange_open(slo_exchange* x, const void* h_handles);
+/* K2x + K2w: d_pooled[c] = sum over ranks r of (sum over seeds s of rank r's d_detail[c * n_seeds_r + s]),
+ * n_seeds = this rank's seed count.  d_pooled (n_cfg records) feeds slo_hillclimb_step with n_parts = 1. */
+slo_status slo_aggregate_exchange(slo_sim* h, slo_exchange* x, const slo_replica_result* d_detail,
+                                  uint32_t n_seeds, slo_config_agg* d_pooled, void* stream);
+/* Synchronising read of the latched error word (0 = ok, 1 = a wait for a peer timed out). */
+slo_status slo_exchange_error(slo_exchange* x, uint32_t* h_err);
+slo_status slo_exchange_destroy(slo_exchange* x);
+
 const char* slo_status_string(slo_status s);
 const char* slo_last_error(const slo_sim* h); /* detail of the last failing call on h (NULL h: global) */
 

@@ -505,4 +505,110 @@ slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_scor
   return SLO_OK;
 }
 
-}  // extern "C"
+// ---- peer exchange (NEXT-4) ----------------------------------------------------------------------
+struct slo_exchange {
+  slo_sim* h = nullptr;
+  uint32_t world = 0, rank = 0, n_cfg = 0;
+  char* window = nullptr;          // this rank's window (exported)
+  size_t bytes = 0;
+  slo::XState* st = nullptr;       // rank-local epoch / counters / error
+  char** d_peers = nullptr;        // device copy of the window base of every rank
+  char* h_peers[slo::kXMaxRanks] = {};
+  bool opened = false;
+};
+
+slo_status slo_exchange_create(slo_sim* h, uint32_t world, uint32_t rank, uint32_t n_cfg, slo_exchange** out,
+                               void* h_handle_out) {
+  if (!h || !out || !h_handle_out || n_cfg == 0 || rank >= world) return fail(h, SLO_E_INVAL, "exchange_create: bad arguments");
+  if (world < 2 || world > slo::kXMaxRanks) return fail(h, SLO_E_RANGE, "exchange_create: world must be in [2, %u]", slo::kXMaxRanks);
+  *out = nullptr;
+  DeviceGuard g(h->device);
+  slo_exchange* x = new (std::nothrow) slo_exchange();
+  if (!x) return fail(h, SLO_E_NOMEM, "exchange_create: host allocation");
+  x->h = h;
+  x->world = world;
+  x->rank = rank;
+  x->n_cfg = n_cfg;
+  x->bytes = slo::kXHeader + (size_t)2 * world * n_cfg * sizeof(slo_config_agg);
+  cudaError_t e;
+  if ((e = cudaMalloc(&x->window, x->bytes)) != cudaSuccess || (e = cudaMalloc(&x->st, sizeof(slo::XState))) != cudaSuccess ||
+      (e = cudaMalloc(&x->d_peers, sizeof(char*) * slo::kXMaxRanks)) != cudaSuccess) {
+    slo_exchange_destroy(x);
+    return fail(h, SLO_E_NOMEM, "exchange_create: cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  cudaIpcMemHandle_t hd;
+  if ((e = cudaMemset(x->window, 0, x->bytes)) != cudaSuccess || (e = cudaMemset(x->st, 0, sizeof(slo::XState))) != cudaSuccess ||
+      (e = cudaIpcGetMemHandle(&hd, x->window)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    slo_exchange_destroy(x);
+    return fail(h, SLO_E_CUDA, "exchange_create: %s", cudaGetErrorString(e));
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == SLO_EXCHANGE_HANDLE_BYTES, "IPC handle size");
+  memcpy(h_handle_out, &hd, sizeof hd);
+  *out = x;
+  return SLO_OK;
+}
+
+slo_status slo_exchange_open(slo_exchange* x, const void* h_handles) {
+  if (!x || !h_handles || x->opened) return fail(x ? x->h : nullptr, SLO_E_INVAL, "exchange_open: bad arguments");
+  DeviceGuard g(x->h->device);
+  const char* hb = static_cast<const char*>(h_handles);
+  for (uint32_t r = 0; r < x->world; ++r) {
+    if (r == x->rank) {
+      x->h_peers[r] = x->window;
+      continue;
+    }
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, hb + (size_t)r * SLO_EXCHANGE_HANDLE_BYTES, sizeof hd);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(x->h, SLO_E_CUDA, "exchange_open: rank %u: %s", r, cudaGetErrorString(e));
+    x->h_peers[r] = static_cast<char*>(p);
+  }
+  CUDA_TRY(x->h, cudaMemcpy(x->d_peers, x->h_peers, sizeof(char*) * slo::kXMaxRanks, cudaMemcpyHostToDevice));
+  x->opened = true;
+  return SLO_OK;
+}
+
+slo_status slo_aggregate_exchange(slo_sim* h, slo_exchange* x, const slo_replica_result* d_detail, uint32_t n_seeds,
+                                  slo_config_agg* d_pooled, void* stream) {
+  if (!h || !x || !x->opened || x->h != h || !d_detail || !d_pooled || n_seeds == 0)
+    return fail(h, SLO_E_INVAL, "aggregate_exchange: bad arguments (exchange opened on this handle?)");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned threads = 256, warps = threads / 32;
+  const unsigned pblocks = (unsigned)((x->n_cfg + warps - 1) / warps);
+  slo::slo_aggregate_push_kernel<<<pblocks, threads, 0, st>>>(d_detail, x->n_cfg, n_seeds, x->d_peers, x->world,
+                                                              x->rank, x->st);
+  CUDA_TRY(h, cudaGetLastError());
+  unsigned wblocks = (unsigned)((x->n_cfg + threads - 1) / threads);
+  if (wblocks > (unsigned)h->sm_count) wblocks = (unsigned)h->sm_count;
+  slo::slo_exchange_wait_kernel<<<wblocks, threads, 0, st>>>(x->window, x->n_cfg, x->world, x->st, d_pooled);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+slo_status slo_exchange_error(slo_exchange* x, uint32_t* h_err) {
+  if (!x || !h_err) return fail(nullptr, SLO_E_INVAL, "exchange_error: null");
+  DeviceGuard g(x->h->device);
+  slo::XState s;
+  CUDA_TRY(x->h, cudaMemcpy(&s, x->st, sizeof s, cudaMemcpyDeviceToHost));
+  *h_err = s.error;
+  return SLO_OK;
+}
+
+slo_status slo_exchange_destroy(slo_exchange* x) {
+  if (!x) return SLO_OK;
+  {
+    DeviceGuard g(x->h->device);
+    cudaDeviceSynchronize();
+    for (uint32_t r = 0; r < x->world && x->opened; ++r)
+      if (r != x->rank && x->h_peers[r]) cudaIpcCloseMemHandle(x->h_peers[r]);
+    if (x->window) cudaFree(x->window);
+    if (x->st) cudaFree(x->st);
+    if (x->d_peers) cudaFree(x->d_peers);
+  }
+  delete x;
+  return SLO_OK;
+}
+
+}  // extern "C\"

@@ -50,6 +50,101 @@ __global__ void slo_aggregate_reduce_kernel(const slo_config_agg* __restrict__ p
 }
 
 // ------------------------------------------------------------------------------------------------
+// NEXT-4 peer exchange: K2x aggregates and pushes into every rank's window, K2w waits and sums
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ slo_config_agg* inbox(char* base, uint32_t par, uint32_t world, uint32_t src,
+                                                 uint32_t n_cfg) {
+  return reinterpret_cast<slo_config_agg*>(base + kXHeader) + ((size_t)par * world + src) * n_cfg;
+}
+__device__ __forceinline__ unsigned long long* xflag(char* base, uint32_t par, uint32_t src) {
+  return reinterpret_cast<unsigned long long*>(base) + par * kXMaxRanks + src;
+}
+
+// one warp per config: the K2 sums, stored into slot [parity][rank] of every rank's window (P2P stores over
+// NVLink for the peers); the last block to finish publishes flag[parity][rank] = epoch in every window
+__global__ void slo_aggregate_push_kernel(const slo_replica_result* __restrict__ detail, uint32_t n_cfg,
+                                          uint32_t n_seeds, char* const* __restrict__ peers, uint32_t world,
+                                          uint32_t rank, XState* st) {
+  const unsigned long long e = *(volatile unsigned long long*)&st->epoch + 1ull;
+  const uint32_t par = (uint32_t)(e & 1ull);
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp < n_cfg) {
+    uint64_t sp = 0, sm = 0, sw = 0;
+    uint32_t fl = 0;
+    const slo_replica_result* d = detail + (size_t)warp * n_seeds;
+    for (uint32_t s = lane; s < n_seeds; s += 32) {
+      const slo_replica_result x = d[s];
+      sp += x.p99_us;
+      sm += x.slo_met;
+      sw += x.window_us;
+      fl |= x.flags;
+    }
+    sp = warp_sum64(sp);
+    sm = warp_sum64(sm);
+    sw = warp_sum64(sw);
+    fl = __reduce_or_sync(FULL, fl);
+    const slo_config_agg a{sp, sm, sw, n_seeds, fl};
+    if ((uint32_t)lane < world) inbox(peers[lane], par, world, rank, n_cfg)[warp] = a;   // lane r -> rank r
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(&st->arrive_push, 1u) == gridDim.x - 1) {       // every block's stores are fenced
+      st->arrive_push = 0;
+      __threadfence_system();
+      for (uint32_t r = 0; r < world; ++r) {
+        unsigned long long* f = xflag(peers[r], par, rank);
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+      }
+    }
+  }
+}
+
+// every block waits for all ranks' flags of this epoch (acquire), then sums its configs over ranks in rank
+// order; the last block to finish advances the local epoch
+__global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uint32_t world, XState* st,
+                                         slo_config_agg* __restrict__ out) {
+  const unsigned long long e = *(volatile unsigned long long*)&st->epoch + 1ull;
+  const uint32_t par = (uint32_t)(e & 1ull);
+  char* base = const_cast<char*>(window);
+  if (threadIdx.x < world) {
+    const unsigned long long* f = xflag(base, par, threadIdx.x);
+    for (uint32_t spins = 0;; ++spins) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v == e) break;
+      if (spins > (1u << 24)) {                                  // ~1 s: a peer never arrived
+        atomicOr(&st->error, 1u);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cfg; c += gridDim.x * blockDim.x) {
+    slo_config_agg a{0, 0, 0, 0, 0};
+    for (uint32_t r = 0; r < world; ++r) {
+      const slo_config_agg x = inbox(base, par, world, r, n_cfg)[c];
+      a.sum_p99_us += x.sum_p99_us;
+      a.sum_slo_met += x.sum_slo_met;
+      a.sum_window_us += x.sum_window_us;
+      a.n_seeds += x.n_seeds;
+      a.flags |= x.flags;
+    }
+    out[c] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&st->arrive_wait, 1u) == gridDim.x - 1) {       // every block has read the epoch
+      st->arrive_wait = 0;
+      *(volatile unsigned long long*)&st->epoch = e;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // neighbours (host + device)
 // ------------------------------------------------------------------------------------------------
 __host__ __device__ static inline int32_t dim_get(const slo_knobs& k, int d) {

@@ -64,6 +64,18 @@ __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs
                                  const slo_config_agg* aggs, uint32_t n_parts, slo_climb_state* state,
                                  int64_t* scores);
 
+// peer exchange (NEXT-4): window = [flags 2 x kXMaxRanks u64][inbox 2 parities x world x n_cfg slo_config_agg]
+constexpr uint32_t kXMaxRanks = 16;
+constexpr size_t kXHeader = 2 * kXMaxRanks * sizeof(uint64_t);
+struct XState {                 // rank-local (not shared)
+  unsigned long long epoch;     // completed exchanges
+  unsigned int arrive_push, arrive_wait, error, pad;
+};
+__global__ void slo_aggregate_push_kernel(const slo_replica_result* detail, uint32_t n_cfg, uint32_t n_seeds,
+                                          char* const* peers, uint32_t world, uint32_t rank, XState* st);
+__global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uint32_t world, XState* st,
+                                         slo_config_agg* out);
+
 // host+device neighbour generation
 __host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& K, slo_knobs* out, uint32_t cap);
 

@@ -59,12 +59,43 @@ def max_over_ranks(x: float, device=None) -> float:
     return float(t.item())
 
 
+class PeerExchange:
+    """NEXT-4: the aggregate exchange done by the aggregation kernel itself over NVLink peer memory.
+
+    Every rank's K2x writes its per-config sums straight into every peer's window (CUDA IPC peer pointers)
+    and publishes an epoch flag; K2w waits for all flags and sums the parts in rank order — the same integers
+    as all-gather + K2b, with no NCCL call and no host round trip, so it can live inside the climb's CUDA
+    graph.  Handles are swapped once through the process group (any backend)."""
+
+    def __init__(self, sim, n_cfg: int, group=None):
+        rank, w = world()
+        if w < 2:
+            raise ValueError("PeerExchange needs world_size >= 2")
+        self.sim, self.n_cfg = sim, n_cfg
+        self.x, handle = sim.exchange_create(w, rank, n_cfg)
+        handles: List[bytes] = [b""] * w
+        dist.all_gather_object(handles, handle, group=group)
+        sim.exchange_open(self.x, b"".join(handles))
+        dist.barrier(group=group)                 # every window is mapped before anyone pushes
+
+    def pooled(self, detail: torch.Tensor, n_seeds: int, out: torch.Tensor, stream=None) -> torch.Tensor:
+        return self.sim.aggregate_exchange(self.x, detail, n_seeds, out, stream=stream)
+
+    def error(self) -> int:
+        return self.sim.exchange_error(self.x)
+
+    def close(self):
+        if self.x is not None:
+            self.sim.exchange_destroy(self.x)
+            self.x = None
+
+
 class ClimbGraph:
     """Alg. 1 with the whole step — K0/K1/K1b simulate, K2 aggregate, all-gather (N > 1), K3 climb — captured
     once in a CUDA graph and replayed (SV §8(f) NEXT-4): no host round trip between steps.  The candidate
     list and the climb state live in device buffers that the step rewrites in place."""
 
-    def __init__(self, sim, cfg, seeds: List[int], n_cand: int = 32, sp=None):
+    def __init__(self, sim, cfg, seeds: List[int], n_cand: int = 32, sp=None, exchange: str = "nccl"):
         from . import sim as S
         self.sim, self.cfg = sim, cfg
         self.space = cfg.extra["space"]
@@ -81,6 +112,8 @@ class ClimbGraph:
         _, self.w = world()
         self.parts = (torch.empty((self.w * n_cand, 32), dtype=torch.uint8, device=self.cands.device)
                       if self.w > 1 else self.agg)
+        # N > 1: "nccl" = K2 + NCCL all-gather + K3 summing the parts; "p2p" = PeerExchange (K2x + K2w)
+        self.xchg = PeerExchange(sim, n_cand) if (self.w > 1 and exchange == "p2p") else None
         self.stream = torch.cuda.Stream(device=self.cands.device)
         self.graph = None
 
@@ -88,6 +121,10 @@ class ClimbGraph:
         c = self.cfg
         self.sim.run_batch(self.cands, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out,
                            stream=self.stream)
+        if self.xchg is not None:
+            self.xchg.pooled(self.out["detail"], self.n_seeds, self.agg, stream=self.stream)
+            self.sim.hillclimb_step(self.space, self.sp, self.cands, self.agg, 1, self.state, stream=self.stream)
+            return
         self.sim.aggregate(self.out["detail"], self.n_cand, self.n_seeds, out=self.agg, stream=self.stream)
         if self.w > 1:
             dist.all_gather_into_tensor(self.parts, self.agg)

@@ -226,6 +226,32 @@ class Simulator:
                                          _stream_ptr(stream)), self.h)
         return out
 
+    # ---- NEXT-4 peer exchange (include/slo_sim.h: slo_exchange_*) -------------------------------
+    def exchange_create(self, world: int, rank: int, n_cfg: int):
+        """This rank's exchange window; returns (opaque handle, 64-byte CUDA IPC handle as bytes)."""
+        x = C.c_void_p()
+        hbuf = (C.c_uint8 * _lib.EXCHANGE_HANDLE_BYTES)()
+        check(lib().slo_exchange_create(self.h, world, rank, n_cfg, C.byref(x), hbuf), self.h)
+        return x, bytes(hbuf)
+
+    def exchange_open(self, x, handles: bytes) -> None:
+        buf = (C.c_uint8 * len(handles)).from_buffer_copy(handles)
+        check(lib().slo_exchange_open(x, buf), self.h)
+
+    def aggregate_exchange(self, x, detail: torch.Tensor, n_seeds: int, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """K2x + K2w: per-config aggregates pooled over all ranks, pushed through the peers' windows."""
+        check(lib().slo_aggregate_exchange(self.h, x, detail.data_ptr(), n_seeds, out.data_ptr(),
+                                           _stream_ptr(stream)), self.h)
+        return out
+
+    def exchange_error(self, x) -> int:
+        e = C.c_uint32(0)
+        check(lib().slo_exchange_error(x, C.byref(e)), self.h)
+        return e.value
+
+    def exchange_destroy(self, x) -> None:
+        lib().slo_exchange_destroy(x)
+
     def climb_state(self, K0: Dict) -> torch.Tensor:
         st = np.zeros(1, CLIMB_DTYPE)
         k = pack_knobs([K0])[0]
