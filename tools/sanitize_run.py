@@ -13,6 +13,12 @@ wls += [inputs.continuous(w) for w in wls] + [inputs.continuous(inputs.preset_cl
 ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)] + [inputs.knobs(conc=0)]
 ks += [inputs.knobs(max_num_seqs=b, conc=c, workload=w, draft_len=4, spec_on=1) for b, c, w in
        ((4, 12, 4), (12, 3, 5), (32, 32, 6), (8, 8, 8))]
+for pol in (1, 2):   # narrow (G >= min(C, B)) and wide (G >= max(C, B)) lane groups
+    sp = sim.Simulator(wls, device=0, group_policy=pol)
+    sp.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(inputs.seeds(3)), 150, warmup_len=10, latencies=True,
+                 stats=True)
+    torch.cuda.synchronize()
+    sp.close()
 s = sim.Simulator(wls, device=0)
 out = s.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(inputs.seeds(3)), 150, warmup_len=10, latencies=True,
                   stats=True)
