@@ -438,3 +438,20 @@ def test_climb_run_host_trajectory(S):
         torch.cuda.synchronize()
         assert torch.equal(traj[i], st_e.cpu().view(-1)), f"step {i}"
     s.close()
+
+
+def test_continuous_launch_shapes_and_chunks_agree(S):
+    """Continuous batching: the result does not depend on warps per block, blocks per SM, the lane-group
+    policy or on splitting the launch into latency-row chunks."""
+    cfg = inputs.config_c2_cont(n_seeds=6, segment_len=700)
+    ks = cfg.knobs[::7]
+    base = _run_gpu(S, cfg.workloads, ks, cfg.seeds(), 700, latencies=True)
+    for kw in (dict(warps_per_block=1, blocks_per_sm=1), dict(warps_per_block=8), dict(group_policy=1),
+               dict(group_policy=2)):
+        g = _run_gpu(S, cfg.workloads, ks, cfg.seeds(), 700, latencies=True, **kw)
+        assert np.array_equal(g["lat"], base["lat"]) and g["detail"].tobytes() == base["detail"].tobytes(), kw
+        assert g["stats"].tobytes() == base["stats"].tobytes(), kw
+    a = _run_gpu(S, cfg.workloads, ks, cfg.seeds(), 700, latencies=False)
+    b = _run_gpu(S, cfg.workloads, ks, cfg.seeds(), 700, latencies=False, scratch_mb=1)   # 1.19 MiB of rows: 2 chunks
+    assert np.array_equal(a["p99"], b["p99"]) and a["detail"].tobytes() == b["detail"].tobytes()
+    assert a["stats"].tobytes() == b["stats"].tobytes()
