@@ -129,7 +129,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     o = *opts;
     for (int i = 0; i < 3; ++i)
       if (o.reserved[i]) return fail(nullptr, SLO_E_INVAL, "create: opts.reserved must be 0");
-    if (o.group_policy > 2) return fail(nullptr, SLO_E_INVAL, "create: opts.group_policy must be 0, 1 or 2");
+    if (o.group_policy > 3) return fail(nullptr, SLO_E_INVAL, "create: opts.group_policy must be 0..3");
     if (o.crn > 1) return fail(nullptr, SLO_E_INVAL, "create: opts.crn must be 0 or 1");
     if (o.warps_per_block > (uint32_t)slo::kMaxWarpsPerBlock)
       return fail(nullptr, SLO_E_INVAL, "create: warps_per_block > %d", slo::kMaxWarpsPerBlock);
@@ -337,8 +337,11 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     // narrow lane groups (G >= min(C, B), up to four replicas per warp) only pay when they still leave every
     // resident warp slot busy: a chunk of fewer than 4 x (resident warps) replicas takes wide groups
     // (G >= max(C, B): more warps, shorter per-replica chains)
-    const uint32_t wide = h->group_policy == 2 ? 1u
+    // and a chunk of at most one replica per SM runs every replica on a whole warp (latency)
+    const uint32_t wide = h->group_policy == 3 ? 2u
+                          : h->group_policy == 2 ? 1u
                           : h->group_policy == 1 ? 0u
+                          : nc <= (uint32_t)h->sm_count ? 2u
                           : (uint64_t)nc < 4ull * bps * h->sm_count * h->warps_per_block ? 1u : 0u;
     slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
                                                                     h->n_wl, wide, h->d_ctl);

@@ -1018,7 +1018,9 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
   // per warp (throughput); a launch too small to fill the GPU (`wide`) takes G >= max(C, B) instead, which
   // shortens each replica's dependency chain (latency)
   const uint32_t beff = min((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
-  const uint32_t need = wide ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : beff;
+  // (wide == 2: a launch of at most one replica per SM — a lone replica's chain is shortest with the whole
+  // warp, G = 32: a generation pass yields 32 requests)
+  const uint32_t need = wide == 2 ? 32u : wide ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : beff;
   const bool spec = k.spec_on && k.draft_len > 0;
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
   if (wl[k.workload].batching) {      // continuous batching, ~N*O/beff iterations: lane groups G >= min(C, B)

@@ -75,7 +75,7 @@ def _wls():
             inputs.preset_ll(rate=40.0, stream_id=7), inputs.preset_closed(stream_id=3)]
 
 
-@pytest.mark.parametrize("policy", [1, 2], ids=["narrow", "wide"])
+@pytest.mark.parametrize("policy", [1, 2, 3], ids=["narrow", "wide", "warp"])
 @pytest.mark.parametrize("block", range(6))
 def test_random_small_configs(S, orc, block, policy):
     """Random valid knob records over every workload kind, lengths spanning several 32-request windows
