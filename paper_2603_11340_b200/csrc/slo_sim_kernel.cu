@@ -1,12 +1,14 @@
 // slo_sim_kernel.cu — the simulation kernels of libslosim.
 //
-//  K0 slo_classify_kernel : sorts replicas into three work lists by the lane-group size G in {8, 16, 32}
-//                           that fits their client window (G >= max(C, B)).
+//  K0 slo_classify_kernel : sorts replicas into work lists by lane-group size G in {8, 16, 32} (static:
+//                           G >= min(C, B) narrow / max(C, B) wide / 32; continuous: G >= min(C, B) or B).
 //  K1 slo_sim_kernel      : persistent; a warp runs 32/G replicas at once, one per G-lane group, with every
 //                           collective (ballot, shuffle, scan, sort) scoped to the group. Per-group shared
-//                           memory holds rings of arrival times a_j and sorted completion times kappa_k,
-//                           packed (P, O), noise words, acceptance thresholds and the warp-uniform
-//                           arrival-process state. Every request's latency goes to an HBM scratch row.
+//                           memory holds rings of arrival times a_j, completion times kappa_k, packed (P, O),
+//                           decode step counts S_j, noise words, acceptance thresholds and the arrival-process
+//                           state. Every request's latency goes to an HBM scratch row.
+//  K1c slo_sim_cont_kernel: the same for continuous (iteration-level) batching, decode iterations
+//                           fast-forwarded to the next event.
 //  K1b slo_select_kernel  : per replica, stages the measured latencies in shared memory and takes the
 //                           exact nearest-rank p99 by an 8-bit radix select; writes p99 and goodput.
 //
@@ -14,7 +16,8 @@
 // checked bit-exactly against the oracle):
 //   s_j = max(a_j, kappa_{j-C});  t_form = max(t_idle, s_h[, min(s_h + max_wait, s_{h+B-1})]);
 //   b = min(B, #{j in [h, h+C) : s_j <= t_form});
-//   Cum_m = alpha0 S_m + alpha1 sum_{m'} min(S_m', S_m); completion order = order of S_m.
+//   Cum_m = alpha0 S_m + alpha1 sum_{m'} min(S_m', S_m); completion order = order of S_m;
+//   S_m depends on request m's own SPEC stream only, so it is resolved at generation (lane-parallel).
 #include <cstdint>
 
 #include "slo_device.cuh"
@@ -105,6 +108,7 @@ struct alignas(16) Group {
   uint64_t kap[KRING];                // kappa_k (k-th completion, ascending) at kap[k % KRING]
   uint32_t po[RING];                  // P | (O << 16)
   uint32_t w3[RING];                  // noise word
+  uint16_t ss[RING];                  // S_j: decode steps request j needs (its own draws only, §2.6)
   uint32_t tm1[16];                   // T_a - 1, a = 1..gp
   uint8_t guide[256];                 // A at the top of bucket u >> 24, | 0x80 if a threshold is inside
   uint64_t g[2], rho[2];              // scaled mean gaps, floor((2^64-1)/g)
@@ -124,98 +128,6 @@ __device__ __forceinline__ uint32_t accepted(const GR& R, uint32_t u, uint32_t g
     while (A < gp && u <= R.tm1[A]) ++A;
   }
   return A;
-}
-
-// lanes per pending member for u = 1..32 pending members (floor(32/u)) and ceil(2^16 / L), so that
-// slot = (lane * recip) >> 16 = floor(lane / L) for every lane < 32
-__constant__ uint32_t kSegL[33] = {32, 32, 16, 10, 8, 6, 5, 4, 4, 3, 3, 2, 2, 2, 2, 2, 2,
-                                   1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
-__constant__ uint32_t kSegRecip[33] = {2048, 2048, 4096, 6554, 8192, 10923, 13108, 16384, 16384, 21846, 21846,
-                                       32768, 32768, 32768, 32768, 32768, 32768, 65536, 65536, 65536, 65536,
-                                       65536, 65536, 65536, 65536, 65536, 65536, 65536, 65536, 65536, 65536,
-                                       65536, 65536};
-
-// Warp-pooled speculative step counts: every lane holding a speculative batch member
-// (`mine`: member of an active group with gamma > 0) is a pending item, whatever its group.  Each round the
-// u pending members get L = floor(32 / u) consecutive lanes of the whole warp; each lane computes one
-// Philox SPEC block (4 decode steps) of its member, a segmented scan of the block token sums finds the
-// block where the member's cumulative tokens reach O, and that lane resolves the exact step.  Members
-// that finish release their lanes to the others in the next round.  Blocks past a crossing are computed
-// speculatively and discarded (the definition's work is ceil(S/4) blocks per member).  Returns S_m in the
-// member's own lane.
-template <int G>
-__device__ __forceinline__ uint32_t spec_steps(const Group<G>* Rw, uint8_t* slots, uint32_t j, uint32_t O, bool mine,
-                                               int lane, uint32_t lanemask_lt) {
-  uint32_t S = 0, cum = 0, q = 0;
-  bool pending = mine;
-  uint32_t pend = __ballot_sync(FULL, pending);
-  while (pend) {
-    const uint32_t u = __popc(pend);
-    const uint32_t L = kSegL[u];                       // floor(32 / u) lanes per pending member
-    const uint32_t lowmask = FULL >> (32 - L);
-    const uint32_t myslot = __popc(pend & lanemask_lt);
-    slots[pending ? myslot : 32u + (uint32_t)lane] = (uint8_t)lane;   // non-pending lanes: dummy slots
-    __syncwarp();
-    const uint32_t slot = ((uint32_t)lane * kSegRecip[u]) >> 16;
-    const uint32_t off = (uint32_t)lane - slot * L;
-    const bool active = slot < u;
-    const int src = active ? slots[slot] : lane;
-    __syncwarp();
-    const uint32_t mj = __shfl_sync(FULL, j, src);
-    const uint32_t moc = __shfl_sync(FULL, O | (cum << 16), src);   // O, cum < 2^16
-    const uint32_t mq = __shfl_sync(FULL, q, src) + off;            // this lane's SPEC block
-    const uint32_t mO = moc & 0xFFFFu, mcum = moc >> 16;
-    const Group<G>& Rm = Rw[src / G];
-    uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-    if (active) {
-      const u32x4 w = philox(mj, 1, mq, 0, Rm.k0, Rm.k1);
-      const uint32_t g0 = Rm.guide[w.x >> 24], g1 = Rm.guide[w.y >> 24];
-      const uint32_t g2 = Rm.guide[w.z >> 24], g3 = Rm.guide[w.w >> 24];
-      e0 = (g0 & 0x7Fu) + 1;
-      e1 = (g1 & 0x7Fu) + 1;
-      e2 = (g2 & 0x7Fu) + 1;
-      e3 = (g3 & 0x7Fu) + 1;
-      if ((g0 | g1 | g2 | g3) & 0x80u) {               // a threshold inside one of the buckets (rare)
-        const uint32_t gp = Rm.gp;
-        e0 = accepted(Rm, w.x, gp) + 1;
-        e1 = accepted(Rm, w.y, gp) + 1;
-        e2 = accepted(Rm, w.z, gp) + 1;
-        e3 = accepted(Rm, w.w, gp) + 1;
-      }
-    }
-    const uint32_t T = e0 + e1 + e2 + e3;
-    uint32_t P = T;                                    // segmented inclusive scan over the L lanes
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(FULL, P, d);
-      if ((int)off >= d) P += v;                       // off < L, so d <= off stays inside the segment
-    }
-    // the cumulative token count is non-decreasing along a segment, so its crossing lanes are a suffix:
-    // with nc crossing lanes the first one is at segbase + L - nc
-    const bool cross = active && (mcum + P >= mO);
-    const uint32_t cb = __ballot_sync(FULL, cross);
-    const uint32_t up = __shfl_up_sync(FULL, (uint32_t)cross, 1);
-    const uint32_t nprev = off > 0 ? up : 0u;
-    uint32_t give = P;
-    if (cross && !nprev) {                             // first crossing lane: exact step inside the block
-      const uint32_t c = mcum + P - T;                 // tokens before this block
-      give = 4u * mq + 1u + (c + e0 < mO) + (c + e0 + e1 < mO) + (c + e0 + e1 + e2 < mO);
-    }
-    const uint32_t nc = __popc((cb >> ((myslot * L) & 31u)) & lowmask);
-    const int from = (int)(((myslot + 1u) * L) - (nc ? nc : 1u)) & 31;
-    const uint32_t got = __shfl_sync(FULL, give, from);
-    if (pending) {
-      if (nc) {
-        S = got;
-        pending = false;
-      } else {
-        cum += got;
-        q += L;
-      }
-    }
-    pend = __ballot_sync(FULL, pending);
-  }
-  return S;
 }
 
 // (a1) set up a newly acquired replica (group-convergent; other groups do not enter)
@@ -355,6 +267,35 @@ __device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ 
     R.po[i % GR::RING] = P | (O << 16);
     R.w3[i % GR::RING] = w.w;
     if (i == warmup) R.a_w = a;
+    // (a7) S_i = min{s : sum_{j<s} (A(u_{i,j}) + 1) >= O_i}.  With static batches a
+    // member's j counts its steps within its batch and with continuous batching its own decode iterations,
+    // so in both models S_i depends on request i's own SPEC stream only and is resolved here, lane-parallel
+    // over the generated requests, one SPEC block (4 steps) per loop trip.  gp = 0 (no speculation, or
+    // alpha_eff = 0): A = 0 and S = O.
+    uint32_t S = O;
+    const uint32_t gp = R.gp;
+    if (gp > 0) {
+      uint32_t tok = 0;
+      for (uint32_t q = 0;; ++q) {
+        const u32x4 b = philox(i, 1, q, 0, k0, k1);
+        uint32_t g0 = R.guide[b.x >> 24], g1 = R.guide[b.y >> 24];
+        uint32_t g2 = R.guide[b.z >> 24], g3 = R.guide[b.w >> 24];
+        if ((g0 | g1 | g2 | g3) & 0x80u) {           // a threshold inside one of the buckets (rare)
+          g0 = accepted(R, b.x, gp);
+          g1 = accepted(R, b.y, gp);
+          g2 = accepted(R, b.z, gp);
+          g3 = accepted(R, b.w, gp);
+        }
+        const uint32_t c1 = tok + (g0 & 0x7Fu) + 1u, c2 = c1 + (g1 & 0x7Fu) + 1u;
+        const uint32_t c3 = c2 + (g2 & 0x7Fu) + 1u, c4 = c3 + (g3 & 0x7Fu) + 1u;
+        if (c4 >= O) {
+          S = 4u * q + 1u + (c1 < O) + (c2 < O) + (c3 < O);
+          break;
+        }
+        tok = c4;
+      }
+    }
+    R.ss[i % GR::RING] = (uint16_t)S;
   }
   __syncwarp();
 }
@@ -407,10 +348,8 @@ __device__ __forceinline__ void flush_counters(const SimParams& p, Counters& ct)
 // one lane-group mode of K1: groups pull replicas from work list `cls` until it is exhausted
 // ------------------------------------------------------------------------------------------------
 template <int G>
-__device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, uint8_t* slots, int lane,
-                                         Counters& ct) {
+__device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   constexpr int RING = Group<G>::RING;
-  const uint32_t lanemask_lt = (1u << lane) - 1u;
   const int g = lane / G, li = lane % G;
   Group<G>& R = reinterpret_cast<Group<G>*>(wsmem)[g];
   const uint32_t gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
@@ -508,13 +447,8 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const uint32_t po = member ? R.po[j % RING] : 0u;
 
     // ---- (a7) decode: S_m = min{s : sum_{j<s} (A(u_{m,j}) + 1) >= O_m}
-    uint32_t S = po >> 16;
+    const uint32_t S = member ? (uint32_t)R.ss[j % RING] : 0u;      // resolved at generation
     const bool spec = kn.w > 0;
-    if (__any_sync(FULL, member && spec)) {
-      const uint32_t Ss = spec_steps<G>(reinterpret_cast<const Group<G>*>(wsmem), slots, j, po >> 16,
-                                        member && spec, lane, lanemask_lt);
-      if (spec) S = Ss;
-    }
 
     // ---- (a6) prefill with the head's noise factor
     const uint32_t w3h = R.w3[h % RING];
@@ -627,6 +561,7 @@ struct alignas(16) CGroup {
   uint64_t kap[KRING];
   uint32_t po[RING];
   uint32_t w3[RING];
+  uint16_t ss[RING];                   // S_j: decode iterations request j needs (§2.12: its own draws only)
   uint32_t tm1[16];
   uint8_t guide[256];
   uint64_t g[2], rho[2];
@@ -944,11 +879,10 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
-  uint8_t* slots = wsmem + p.warp_bytes - 64;            // spec-decode slot map (last 64 B of the warp area)
   Counters ct{0, 0, 0, 0};
-  run_mode<8>(p, 0, wsmem, slots, lane, ct);
-  run_mode<16>(p, 1, wsmem, slots, lane, ct);
-  run_mode<32>(p, 2, wsmem, slots, lane, ct);
+  run_mode<8>(p, 0, wsmem, lane, ct);
+  run_mode<16>(p, 1, wsmem, lane, ct);
+  run_mode<32>(p, 2, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -998,7 +932,7 @@ size_t group_warp_bytes() {
   size_t m = 4 * sizeof(Group<8>);
   if (2 * sizeof(Group<16>) > m) m = 2 * sizeof(Group<16>);
   if (sizeof(Group<32>) > m) m = sizeof(Group<32>);
-  return m + 64;   // + spec-decode slot map (32 slots + 32 dummies)
+  return m;
 }
 
 // ------------------------------------------------------------------------------------------------
