@@ -548,10 +548,11 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 //   * else decode iteration iff |R| > 0: every running lane takes its next acceptance draw, completions at
 //     the iteration end fill kappa;
 //   * else idle until s_next.
-// Random words are consumed from pooled per-lane buffers: a FIFO of up to 8 accepted-prefix values per slot
-// (refilled one SPEC block = 4 decode steps at a time; when any slot runs dry every slot with room refills
-// in the same pass) and a window of the next G decode-iteration noise words per group (ITER blocks; when
-// any group exhausts its window every group shifts its window and refills the consumed part).
+// A request's decode-iteration count S_i depends on its own SPEC stream only (its j counts its own
+// iterations), so generation resolves it and a slot just counts down; between events the decode iterations
+// are fast-forwarded (K = first completion, first prefill opportunity, or the noise window).  Noise words
+// come from a window of the next G decode iterations per group (ITER blocks; when any group has used half
+// of its window every group shifts its window and draws the consumed part in the same pass).
 // ------------------------------------------------------------------------------------------------
 template <int G>
 struct alignas(16) CGroup {
@@ -590,8 +591,9 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
   bool active = false, exhausted = false, need_s = false, closed = false;
   // slot state (lane = one slot of the running set)
   bool run = false;
-  uint32_t mi = 0, rem = 0, steps = 0, q = 0, acnt = 0, fw = 0, nzc = 0, my_slo = 0;   // fw: noise window
-  uint64_t origin = 0, abuf = 0, my_sum = 0, my_cmax = 0;
+  // sleft: decode iterations the slot's request still runs; stot: its S (counters); fw: noise window
+  uint32_t mi = 0, sleft = 0, stot = 0, fw = 0, nzc = 0, my_slo = 0;
+  uint64_t origin = 0, my_sum = 0, my_cmax = 0;
 
   for (;;) {
     __syncwarp();
@@ -698,12 +700,9 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         const uint32_t po = R.po[i % RING];
         P = po & 0xFFFFu;
         mi = i;
-        rem = po >> 16;
+        stot = R.ss[i % RING];                          // S_i, resolved at generation (§2.12: own draws only)
+        sleft = stot;
         origin = closed ? s_r : R.a[i % RING];
-        steps = 0;
-        q = 0;
-        acnt = 0;
-        abuf = 0;
         run = true;
       }
       const bool wsrc = pre && closed && p.warmup >= nq && p.warmup < nq + kk;
@@ -753,52 +752,13 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           nzc = 0;
         }
       }
-      const bool sp = dec && run && gamma > 0;
-      if (__any_sync(FULL, sp && acnt == 0)) {           // pooled refill: every slot with room takes a block
-        if (sp && acnt <= 4) {
-          const u32x4 wb = philox(mi, 1, q, 0, k0, k1);
-          uint32_t g0 = R.guide[wb.x >> 24], g1 = R.guide[wb.y >> 24];
-          uint32_t g2 = R.guide[wb.z >> 24], g3 = R.guide[wb.w >> 24];
-          if ((g0 | g1 | g2 | g3) & 0x80u) {             // a threshold inside one of the buckets (rare)
-            const uint32_t gp = R.gp;
-            g0 = accepted(R, wb.x, gp);
-            g1 = accepted(R, wb.y, gp);
-            g2 = accepted(R, wb.z, gp);
-            g3 = accepted(R, wb.w, gp);
-          }
-          const uint32_t pk = (g0 & 0x7Fu) | ((g1 & 0x7Fu) << 8) | ((g2 & 0x7Fu) << 16) | ((g3 & 0x7Fu) << 24);
-          abuf |= (uint64_t)pk << (8u * acnt);
-          acnt += 4;
-          ++q;
-        }
-      }
       // end times of the next iterations: lane k <-> iteration it + k
       const uint32_t d = alpha0 + alpha1 * nrun;          // < 2^31 (timing values < 2^20, gamma <= 16)
       const uint32_t fk = __shfl_sync(FULL, fw, (int)(((uint32_t)li + nzc) & (G - 1)), G);
       const uint32_t Dk = nz ? (uint32_t)(((uint64_t)fk * d) / 1000000u) : d;
       const uint64_t cum = gscan64<G>((uint64_t)Dk, li);
-      // iterations until each running member finishes (within its buffered draws)
-      // speculative members: byte i of `pre` = tokens emitted by the next i + 1 steps, sum of (A + 1)
-      // (each A <= 16, so 8 prefix sums <= 136 stay inside their bytes: a SWAR prefix sum)
-      uint32_t Sm = 0xFFFFu, av = 0xFFFFu;
-      uint64_t pre = abuf + 0x0101010101010101ull;
-      pre += pre << 8;
-      pre += pre << 16;
-      pre += pre << 32;
-      if (dec && run) {
-        if (gamma == 0) {
-          Sm = rem;
-        } else {
-          av = acnt;
-          if (rem <= 136u) {                             // first step i < acnt with prefix >= rem
-            const uint32_t rr = rem * 0x01010101u;
-            const uint32_t lo = __vcmpgeu4((uint32_t)pre, rr), hi = __vcmpgeu4((uint32_t)(pre >> 32), rr);
-            const uint64_t ge = (((uint64_t)hi << 32) | lo) & (acnt >= 8 ? ~0ull : ((1ull << (8 * acnt)) - 1ull));
-            if (ge) Sm = (uint32_t)(__ffsll((long long)ge) + 7) >> 3;
-          }
-        }
-      }
-      uint32_t K = min(gmin<G>(Sm), gmin<G>(av));
+      // K = min(first completion, first iteration end at which a prefill can start, the noise window)
+      uint32_t K = gmin<G>(dec && run ? sleft : 0xFFFFu);
       K = min(K, nz ? (uint32_t)G - nzc : (uint32_t)G);
       const bool open = dec && nrun < B && (uint32_t)li < K && t + cum >= s_next;   // s_next = INF: never
       const uint32_t om = gballot<G>(open, lane);
@@ -810,16 +770,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         it += K;
         if (nz) nzc += K;
         if (run) {
-          steps += K;
-          if (Sm == K) {
-            fin = true;
-          } else if (gamma == 0) {
-            rem -= K;
-          } else {
-            rem -= (uint32_t)(pre >> (8 * (K - 1))) & 0xFFu;
-            abuf = K >= 8 ? 0ull : abuf >> (8 * K);
-            acnt -= K;
-          }
+          sleft -= K;
+          fin = sleft == 0;
         }
       }
       if (__any_sync(FULL, fin)) {
@@ -833,8 +785,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             my_sum += l;
             my_cmax = t;
           }
-          ct.steps += steps;
-          ct.blocks += gamma > 0 ? (steps + 3u) >> 2 : 0u;
+          ct.steps += stot;
+          ct.blocks += gamma > 0 ? (stot + 3u) >> 2 : 0u;
           run = false;
         }
         if (dec && (uint32_t)li < nf) R.kap[(ndone + li) % KRING] = t;
