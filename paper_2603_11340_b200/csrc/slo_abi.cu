@@ -79,6 +79,20 @@ struct DeviceGuard {
   }
 };
 
+// bucket guide of a length table: for the 2^24-wide bucket b of u, entry b packs
+// lo_b = #{l : cw[l] <= b 2^24} and hi_b = #{l : cw[l] <= b 2^24 + 2^24 - 1}; the count for any u in the bucket
+// lies in [lo_b, hi_b], so lo_b == hi_b answers at once and otherwise a search over cw[lo_b, hi_b) does
+void append_guide(std::vector<uint32_t>& t, const uint32_t* cw, uint32_t ncw) {
+  uint32_t lo = 0, hi = 0;
+  for (uint32_t b = 0; b < 256; ++b) {
+    const uint32_t umin = b << 24, umax = umin | 0xFFFFFFu;
+    while (lo < ncw && cw[lo] <= umin) ++lo;
+    if (hi < lo) hi = lo;
+    while (hi < ncw && cw[hi] <= umax) ++hi;
+    t.push_back(lo | (hi << 16));
+  }
+}
+
 bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
   if (lo < 1 || (uint64_t)lo + ncw > SLO_MAX_LENGTH) return false;
   if (ncw > 0 && cw == nullptr) return false;
@@ -174,10 +188,14 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     d.p_ncw = x.prompt_ncw;
     d.p_off = (uint32_t)tables.size();
     tables.insert(tables.end(), x.prompt_cw, x.prompt_cw + x.prompt_ncw);
+    d.p_goff = (uint32_t)tables.size();
+    append_guide(tables, x.prompt_cw, x.prompt_ncw);
     d.o_lo = x.output_lo;
     d.o_ncw = x.output_ncw;
     d.o_off = (uint32_t)tables.size();
     tables.insert(tables.end(), x.output_cw, x.output_cw + x.output_ncw);
+    d.o_goff = (uint32_t)tables.size();
+    append_guide(tables, x.output_cw, x.output_ncw);
     d.t = x.timing;
     d.stream_id = x.stream_id;
     d.batching = x.batching;

@@ -74,10 +74,13 @@ __device__ __forceinline__ uint64_t capacity(uint64_t D, uint64_t rho) {
   return x > (1ull << 62) ? (1ull << 62) : x;
 }
 
-// ---- lengths: lo + #{l : cw[l] <= u}, by binary search over the cut points.
-__device__ __forceinline__ uint32_t length_of(const uint32_t* __restrict__ cw, uint32_t ncw, uint32_t lo,
-                                              uint32_t u) {
-  uint32_t base = 0, n = ncw;
+// ---- lengths: lo + #{l : cw[l] <= u}: the bucket guide brackets the count, a binary
+// search over the (usually empty) bracket finishes it
+__device__ __forceinline__ uint32_t length_guided(const uint32_t* __restrict__ tables, uint32_t off, uint32_t goff,
+                                                  uint32_t lo, uint32_t u) {
+  const uint32_t g = __ldg(tables + goff + (u >> 24));
+  uint32_t base = g & 0xFFFFu, n = (g >> 16) - base;
+  const uint32_t* cw = tables + off;
   while (n > 0) {
     const uint32_t half = n >> 1;
     if (__ldg(cw + base + half) <= u) {

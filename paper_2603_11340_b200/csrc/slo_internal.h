@@ -18,8 +18,8 @@ struct DevWorkload {      // device copy of one slo_workload
   uint32_t kind, start_state;
   uint64_t gap_q16[2];
   uint64_t soj[2];
-  uint32_t p_lo, p_ncw, p_off;
-  uint32_t o_lo, o_ncw, o_off;
+  uint32_t p_lo, p_ncw, p_off, p_goff;   // cut points at tables[off], 256-entry bucket guide at tables[goff]
+  uint32_t o_lo, o_ncw, o_off, o_goff;
   slo_timing t;
   uint32_t stream_id, batching;
 };

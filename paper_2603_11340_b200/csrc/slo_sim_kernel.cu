@@ -261,8 +261,8 @@ __device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ 
   if (go && li == 0) R.last = newlast;
   if (valid) {
     const DevWorkload& W = wls[wl];
-    const uint32_t P = length_of(tables + W.p_off, W.p_ncw, W.p_lo, w.y);
-    const uint32_t O = length_of(tables + W.o_off, W.o_ncw, W.o_lo, w.z);
+    const uint32_t P = length_guided(tables, W.p_off, W.p_goff, W.p_lo, w.y);
+    const uint32_t O = length_guided(tables, W.o_off, W.o_goff, W.o_lo, w.z);
     R.a[i % GR::RING] = a;
     R.po[i % GR::RING] = P | (O << 16);
     R.w3[i % GR::RING] = w.w;
