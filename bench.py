@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--warps-per-block", type=int, default=0, help="launch shape override (0 = library default)")
     ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--group-policy", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="lane groups: 0 auto, 1 narrow G>=min(C,B), 2 wide G>=max(C,B), 3 whole warp")
     ap.add_argument("--eager-climb", action="store_true", help="c4: host loop instead of the CUDA-graph step")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 aggregate exchange: p2p = K2x/K2w through CUDA IPC peer windows (NEXT-4), "
@@ -236,7 +238,7 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     S = sim.Simulator(cfg.workloads, device=local, warps_per_block=args.warps_per_block,
-                      blocks_per_sm=args.blocks_per_sm)
+                      blocks_per_sm=args.blocks_per_sm, group_policy=args.group_policy)
     info = S.info()
 
     from paper_2603_11340_b200.dist import seed_block, sweep_seed_offset
