@@ -364,7 +364,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   bool active = false, exhausted = false;
 
   for (;;) {
-    __syncwarp();   // lanes of other groups read this group's record in the pooled decode: order before reuse
+    __syncwarp();   // every lane is past the previous iteration's reads of its group's record
     // ---- acquire replicas for idle groups
     bool want = !active && !exhausted;
     while (__any_sync(FULL, want)) {
@@ -539,8 +539,8 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
 // ------------------------------------------------------------------------------------------------
 // K1c: continuous (iteration-level, vLLM-style) batching, DESIGN.md §2.12.
 //
-// A warp runs 32/G replicas at once, one per G-lane group with G >= B (lane = one slot of the running set
-// R, |R| <= B).  The server's free instants are iteration ends and, when it idles, the next issue.  The
+// A warp runs 32/G replicas at once, one per G-lane group with G >= min(C, B) (lane = one slot of the
+// running set R, |R| <= min(C, B)).  The server's free instants are iteration ends and, when it idles, the next issue.  The
 // gate's closed form s_j = max(a_j, kappa_{j-C}) holds for any service order (issue is in index order and
 // completions only free slots), so a group keeps s_next = s_{nq} (the next request to admit) and:
 //   * prefill iteration iff |R| < B and s_next <= t: a ballot over the window j = nq + li counts the queue,
