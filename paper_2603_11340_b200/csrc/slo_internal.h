@@ -9,8 +9,7 @@ namespace slo {
 constexpr int kMaxWarpsPerBlock = 8;
 constexpr int kDefaultWarpsPerBlock = 4;
 // K0 work lists: static batching by lane-group size G = 8, 16, 32 (>= min(C, B) narrow, >= max(C, B) wide, or
-// 32 for a lone replica; K1), then continuous
-// batching by G = 8, 16, 32 >= B (K1c)
+// 32 for a lone replica; K1), then continuous batching by G = 8, 16, 32 >= min(C, B) (wide: >= B) (K1c)
 constexpr int kLists = 6;
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 constexpr int kCtlBucket = 16, kCtlWords = kCtlBucket + 2 * 16 * kLists;
