@@ -222,6 +222,8 @@ def main():
     import __graft_entry__
     if rank == 0 or world == 1:
         __graft_entry__.build()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)                  # before NCCL: one process per GPU, rank -> its own device
     if world > 1:
         # NCCL over NVLink/NVSwitch in production; SLO_BENCH_BACKEND=gloo lets several ranks share one GPU
         # to exercise this code path on a single-GPU box (never used for a reported number)
@@ -233,8 +235,6 @@ def main():
     from paper_2603_11340_b200 import inputs, sim
     from paper_2603_11340_b200._lib import STATS_DTYPE
 
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     S = sim.Simulator(cfg.workloads, device=local, warps_per_block=args.warps_per_block,
