@@ -425,6 +425,8 @@ def main():
         blocks = int(stats["philox_blocks"])
         peak_gops = 148 * 4 * 32 * pk["sm_max_mhz"] * 1e6 / 1e9      # lane-ops/s at 1 warp-instr/clk/SMSP
         achieved_gops = blocks * OPS_PER_PHILOX_BLOCK / (t_k1 / args.steps) / 1e9
+        # K4: measured Philox4x32-10 throughput of this GPU at full occupancy (untimed, after the run)
+        rng_peak_gops = S.philox_peak() * OPS_PER_PHILOX_BLOCK / 1e9
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -456,7 +458,11 @@ def main():
                                     "slo_sim_run_batch = K0 classify + K1 simulate + K1b p99 select (K1 dominates, "
                                     "see profiles/ launch list)"),
                          "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
-                                 "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)"},
+                                 "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)",
+                         "measured_rng_peak": rng_peak_gops,
+                         "frac_of_measured_rng_peak": achieved_gops / rng_peak_gops,
+                         "measured_rng_peak_note": "K4 slo_philox_peak: Philox blocks/s x 60 of a full-occupancy "
+                                                   "kernel that only draws blocks (the RNG roofline of DESIGN.md §7)"},
             "gpu_launches": launches_per_step * args.steps,
             **({"exchange_error": x_err} if world > 1 else {}),
             "e2e": e2e,

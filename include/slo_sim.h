@@ -256,6 +256,12 @@ slo_status slo_aggregate_exchange(slo_sim* h, slo_exchange* x, const slo_replica
 slo_status slo_exchange_error(slo_exchange* x, uint32_t* h_err);
 slo_status slo_exchange_destroy(slo_exchange* x);
 
+/* K4 (measurement only): the RNG roofline.  Every thread of a full-occupancy grid (sm_count x 8 blocks x
+ * 256 threads) draws `iters` Philox4x32-10 blocks with distinct counters and XOR-folds them
+ * into d_sink[thread] (so nothing is dead code); blocks drawn = sm_count * 2048 * iters.  The caller times
+ * it on `stream` (bench.py reports blocks/s next to the simulator's).  d_sink: >= sm_count * 2048 u32. */
+slo_status slo_philox_peak(slo_sim* h, uint32_t iters, uint32_t* d_sink, void* stream);
+
 const char* slo_status_string(slo_status s);
 const char* slo_last_error(const slo_sim* h); /* detail of the last failing call on h (NULL h: global) */
 

@@ -609,6 +609,14 @@ slo_status slo_aggregate_exchange(slo_sim* h, slo_exchange* x, const slo_replica
   return SLO_OK;
 }
 
+slo_status slo_philox_peak(slo_sim* h, uint32_t iters, uint32_t* d_sink, void* stream) {
+  if (!h || !d_sink || iters == 0) return fail(h, SLO_E_INVAL, "philox_peak: bad arguments");
+  DeviceGuard g(h->device);
+  slo::slo_philox_peak_kernel<<<(unsigned)h->sm_count * 8u, 256, 0, (cudaStream_t)stream>>>(iters, d_sink);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
 slo_status slo_exchange_error(slo_exchange* x, uint32_t* h_err) {
   if (!x || !h_err) return fail(nullptr, SLO_E_INVAL, "exchange_error: null");
   DeviceGuard g(x->h->device);

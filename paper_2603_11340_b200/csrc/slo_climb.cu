@@ -145,6 +145,22 @@ __global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uin
 }
 
 // ------------------------------------------------------------------------------------------------
+// K4: Philox4x32-10 throughput at full occupancy (the RNG roofline of DESIGN.md §7), keyed per thread,
+// counters (iteration, 1, thread, 0) like the SPEC stream; the XOR fold keeps every block live
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) slo_philox_peak_kernel(uint32_t iters, uint32_t* __restrict__ sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t k0 = 0x5EED0000u ^ tid, k1 = 0x9E3779B9u * (tid + 1u);
+  uint32_t acc = 0;
+#pragma unroll 1
+  for (uint32_t q = 0; q < iters; ++q) {
+    const u32x4 w = philox(q, 1, tid, 0, k0, k1);
+    acc ^= w.x ^ w.y ^ w.z ^ w.w;
+  }
+  sink[tid] = acc;
+}
+
+// ------------------------------------------------------------------------------------------------
 // neighbours (host + device)
 // ------------------------------------------------------------------------------------------------
 __host__ __device__ static inline int32_t dim_get(const slo_knobs& k, int d) {

@@ -76,6 +76,8 @@ __global__ void slo_aggregate_push_kernel(const slo_replica_result* detail, uint
 __global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uint32_t world, XState* st,
                                          slo_config_agg* out);
 
+__global__ void slo_philox_peak_kernel(uint32_t iters, uint32_t* sink);   // K4: RNG roofline
+
 // host+device neighbour generation
 __host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& K, slo_knobs* out, uint32_t cap);
 

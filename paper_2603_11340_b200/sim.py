@@ -244,6 +244,22 @@ class Simulator:
                                            _stream_ptr(stream)), self.h)
         return out
 
+    def philox_peak(self, iters: int = 2048, repeats: int = 3) -> float:
+        """K4: measured Philox4x32-10 blocks/s at full occupancy (the RNG roofline)."""
+        sm = self.info()["sm_count"]
+        sink = torch.empty(sm * 2048, dtype=torch.int32, device=torch.device("cuda", self.device))
+        st = torch.cuda.current_stream()
+        check(lib().slo_philox_peak(self.h, iters, sink.data_ptr(), _stream_ptr(st)), self.h)   # warm-up
+        best = 0.0
+        for _ in range(repeats):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            check(lib().slo_philox_peak(self.h, iters, sink.data_ptr(), _stream_ptr(st)), self.h)
+            e1.record(st)
+            e1.synchronize()
+            best = max(best, sm * 2048 * iters / (e0.elapsed_time(e1) / 1000.0))
+        return best
+
     def exchange_error(self, x) -> int:
         e = C.c_uint32(0)
         check(lib().slo_exchange_error(x, C.byref(e)), self.h)
