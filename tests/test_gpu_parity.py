@@ -455,3 +455,19 @@ def test_continuous_launch_shapes_and_chunks_agree(S):
     b = _run_gpu(S, cfg.workloads, ks, cfg.seeds(), 700, latencies=False, scratch_mb=1)   # 1.19 MiB of rows: 2 chunks
     assert np.array_equal(a["p99"], b["p99"]) and a["detail"].tobytes() == b["detail"].tobytes()
     assert a["stats"].tobytes() == b["stats"].tobytes()
+
+
+def test_philox_peak_kernel_is_deterministic(S):
+    """K4 (measurement only): positive throughput, and the XOR-folded blocks are the same on every run (every
+    block is computed, nothing is elided)."""
+    s = S.Simulator([inputs.preset_ll()], device=0)
+    from paper_2603_11340_b200._lib import lib
+    sm = s.info()["sm_count"]
+    a = torch.zeros(sm * 2048, dtype=torch.int32, device="cuda")
+    b = torch.ones(sm * 2048, dtype=torch.int32, device="cuda")
+    assert lib().slo_philox_peak(s.h, 16, a.data_ptr(), None) == 0
+    assert lib().slo_philox_peak(s.h, 16, b.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and int((a != 0).sum()) > sm * 2000
+    assert s.philox_peak(iters=256, repeats=1) > 1e10
+    s.close()
