@@ -116,9 +116,8 @@ typedef struct {
   uint32_t scratch_mb;          /* latency-row scratch per launch chunk in MiB; 0 = default (4096). A run */
                                 /* whose rows exceed it is split into chunks of replicas (same results)  */
   uint32_t group_policy;        /* static-batching lane groups (results never depend on it): 0 auto      */
-                                /* (whole warp for <= 1 replica per SM, wide G >= max(C,B) while narrow   */
-                                /* groups would leave warp slots idle, else narrow G >= min(C,B)),        */
-                                /* 1 narrow, 2 wide, 3 whole warp (G = 32); other values SLO_E_INVAL      */
+                                /* (whole warp for <= 1 replica per SM, else narrow G >= min(C,B)),       */
+                                /* 1 narrow, 2 wide G >= max(C,B), 3 whole warp (G = 32); else INVAL      */
   uint32_t reserved[3];         /* must be 0                                                              */
 } slo_sim_opts;
 

@@ -354,15 +354,13 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
     CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * slo::kCtlWords, st));
-    // narrow lane groups (G >= min(C, B), up to four replicas per warp) only pay when they still leave every
-    // resident warp slot busy: a chunk of fewer than 4 x (resident warps) replicas takes wide groups
-    // (G >= max(C, B): more warps, shorter per-replica chains)
-    // and a chunk of at most one replica per SM runs every replica on a whole warp (latency)
+    // lane groups: narrow (G >= min(C, B), up to four replicas per warp) by default — measured best from
+    // 512-replica climb steps (one 8-GPU rank of C4) up to the full sweeps; a chunk of at most one replica per
+    // SM runs each replica on a whole warp (C1: shortest chain); wide (G >= max(C, B)) only when forced
     const uint32_t wide = h->group_policy == 3 ? 2u
                           : h->group_policy == 2 ? 1u
                           : h->group_policy == 1 ? 0u
-                          : nc <= (uint32_t)h->sm_count ? 2u
-                          : (uint64_t)nc < 4ull * bps * h->sm_count * h->warps_per_block ? 1u : 0u;
+                          : nc <= (uint32_t)h->sm_count ? 2u : 0u;
     slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
                                                                     h->n_wl, wide, h->d_ctl);
     CUDA_TRY(h, cudaGetLastError());
