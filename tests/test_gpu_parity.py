@@ -471,3 +471,25 @@ def test_philox_peak_kernel_is_deterministic(S):
     assert torch.equal(a, b) and int((a != 0).sum()) > sm * 2000
     assert s.philox_peak(iters=256, repeats=1) > 1e10
     s.close()
+
+
+def test_maximum_segment_and_saturated_latencies(S, orc):
+    """The largest replica the ABI allows (warmup + segment = SLO_MAX_REQUESTS = 2^22 requests), static and
+    continuous, one of them overloaded so far past the knee that latencies pass 2^32 - 1 us (stored
+    saturated, flags bit 1): p99, SLO count, window, latency sum, flags and goodput bit-exact."""
+    N = 1 << 22
+    wls = [inputs.preset_ll(rate=10.0), inputs.continuous(inputs.preset_ll(rate=10.0)),
+           inputs.preset_ll(rate=2000.0)]
+    ks = [inputs.knobs(conc=8, max_num_seqs=16), inputs.knobs(conc=6, max_num_seqs=4, workload=1, draft_len=4,
+                                                               spec_on=1),
+          inputs.knobs(conc=32, max_num_seqs=2, workload=2)]                        # ~20x overload
+    seeds = inputs.seeds(1, 4242)
+    g = _run_gpu(S, wls, ks, seeds, N - 100, warmup=100, latencies=False)
+    for ci, k in enumerate(ks):
+        ref = _compare_replica(orc, g, ci, wls, k, seeds[0], N - 100, 100, 1_200_000, check_lat=False)
+        if ci == 2:
+            assert ref["flags"] & 2 and int(g["detail"][2]["flags"]) & 2
+    # the ABI refuses one request more
+    from paper_2603_11340_b200._lib import SloError
+    with pytest.raises(SloError):
+        _run_gpu(S, wls, ks[:1], seeds, N - 99, warmup=100, latencies=False)
