@@ -9,8 +9,9 @@
 //                           state. Every request's latency goes to an HBM scratch row.
 //  K1c slo_sim_cont_kernel: the same for continuous (iteration-level) batching, decode iterations
 //                           fast-forwarded to the next event.
-//  K1b slo_select_kernel  : per replica, stages the measured latencies in shared memory and takes the
-//                           exact nearest-rank p99 by an 8-bit radix select; writes p99 and goodput.
+//  K1b slo_select_kernel  : per replica, the exact nearest-rank p99 (p50, p95) of the measured latencies by
+//                           an 8-bit radix select over the row (L2-resident; shared-memory staging is kept for
+//                           callers passing smem_vals > 0); writes p99 and goodput.
 //
 // The event loop is replaced by the closed forms of DESIGN.md §2.6 (equal to the event definition;
 // checked bit-exactly against the oracle):
