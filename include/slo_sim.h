@@ -236,7 +236,7 @@ slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_scor
  * Windows are double-buffered by epoch parity, so a rank can never overwrite a part a peer has not read.
  * Usage: slo_exchange_create on every rank -> all-gather the 64-byte handles (any transport, e.g. a
  * torch.distributed group) -> slo_exchange_open -> slo_aggregate_exchange per step (stream-ordered, graph-
- * capturable; all ranks must call it the same number of times).  A rank that waits > ~1 s for a peer gives
+ * capturable; all ranks must call it the same number of times).  A rank that waits > 30 s for a peer gives
  * up (results undefined) and latches an error readable with slo_exchange_error. */
 #define SLO_EXCHANGE_MAX_RANKS 16u
 #define SLO_EXCHANGE_HANDLE_BYTES 64u

@@ -110,15 +110,18 @@ __global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uin
   char* base = const_cast<char*>(window);
   if (threadIdx.x < world) {
     const unsigned long long* f = xflag(base, par, threadIdx.x);
-    for (uint32_t spins = 0;; ++spins) {
-      unsigned long long v;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v, now;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
       if (v == e) break;
-      if (spins > (1u << 24)) {                                  // ~1 s: a peer never arrived
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 30000000000ull) {                           // 30 s: a peer never arrived
         atomicOr(&st->error, 1u);
         break;
       }
-      __nanosleep(64);
+      __nanosleep(256);
     }
   }
   __syncthreads();
