@@ -65,6 +65,17 @@ def test_create_rejects_bad_arguments(L):
     w.arr.mean_gap_q16[0] = (1 << 64) - 1   # Poisson needs a finite gap
     assert lib.slo_sim_create(0, C.byref(w), 1, None, C.byref(h)) == -1
     w.arr.mean_gap_q16[0] = inputs.mean_gap_q16(10.0)
+    w.batching = 2                     # 0 static, 1 continuous
+    assert lib.slo_sim_create(0, C.byref(w), 1, None, C.byref(h)) == -1
+    assert b"batching" in lib.slo_last_error(None)
+    w.batching = 1
+    opts = L.slo_sim_opts()
+    opts.crn = 1
+    opts.group_policy = 4              # 0..3
+    assert lib.slo_sim_create(0, C.byref(w), 1, C.byref(opts), C.byref(h)) == -1
+    opts.group_policy = 0
+    opts.reserved[0] = 1
+    assert lib.slo_sim_create(0, C.byref(w), 1, C.byref(opts), C.byref(h)) == -1
     # a valid workload on a machine without a GPU: no device
     import torch
     if not torch.cuda.is_available():
@@ -73,6 +84,13 @@ def test_create_rejects_bad_arguments(L):
 
 def test_null_handle_calls(L):
     lib = L.lib()
+    x = C.c_void_p()
+    hb = (C.c_uint8 * 64)()
+    assert lib.slo_exchange_create(None, 2, 0, 32, C.byref(x), hb) == -1
+    assert lib.slo_exchange_open(None, hb) == -1
+    assert lib.slo_aggregate_exchange(None, None, None, 1, None, None) == -1
+    assert lib.slo_exchange_destroy(None) == 0
+    assert lib.slo_philox_peak(None, 1, None, None) == -1
     assert lib.slo_sim_run_batch(None, None, 1, None, 1, 1, 0, 1, None, None, None, None, None, None) == -1
     assert lib.slo_aggregate(None, None, 1, 1, None, None) == -1
     assert lib.slo_sim_destroy(None) == 0
