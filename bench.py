@@ -413,6 +413,17 @@ def main():
     if graph is not None:
         e2e["api"] = "dist.ClimbGraph.run_host: climb trajectory read back every step"
 
+    # K5 (supplementary, untimed): the Pareto front of this step's per-config aggregates
+    pareto = None
+    if args.workload != "c4":
+        src = pooled if world > 1 else S.aggregate(out["detail"], n_cfg, n_seeds_local)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        S.pareto_front(src, count=True)
+        e0.record(stream)
+        _, cnt = S.pareto_front(src, count=True)
+        e1.record(stream)
+        e1.synchronize()
+        pareto = {"configs": n_cfg, "on_front": int(cnt.item()), "ms": e0.elapsed_time(e1)}
     x_err = 0
     if world > 1:
         xo = xchg if xchg is not None else (graph.xchg if graph is not None else None)
@@ -465,6 +476,7 @@ def main():
                                                    "kernel that only draws blocks (the RNG roofline of DESIGN.md §7)"},
             "gpu_launches": launches_per_step * args.steps,
             **({"exchange_error": x_err} if world > 1 else {}),
+            **({"pareto": pareto} if pareto is not None else {}),
             "e2e": e2e,
             "clocks": clk,
         }

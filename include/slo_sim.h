@@ -255,6 +255,16 @@ slo_status slo_aggregate_exchange(slo_sim* h, slo_exchange* x, const slo_replica
 slo_status slo_exchange_error(slo_exchange* x, uint32_t* h_err);
 slo_status slo_exchange_destroy(slo_exchange* x);
 
+/* K5: the Pareto front of a sweep ("the resulting Pareto front").
+ * For each of n_cfg aggregates (slo_aggregate output, device), d_on_front[c] = 1 iff config c is valid (no
+ * invalid seed, n_seeds > 0) and no valid config dominates it on (minimise floor(sum_p99 / n_seeds) us,
+ * maximise floor(sum_slo_met * 10^12 / sum_window) micro-rps) — dominate = no worse in both, better in one;
+ * equal points do not dominate each other.  *d_count (nullable, device) = number of front configs.
+ * O(n log n) on the device (two radix sorts and two scans; scratch owned by the handle).
+ * Errors: SLO_E_INVAL (null pointers, n_cfg == 0), SLO_E_NOMEM, SLO_E_CUDA. */
+slo_status slo_pareto_front(slo_sim* h, const slo_config_agg* d_agg, uint32_t n_cfg, uint8_t* d_on_front,
+                            uint32_t* d_count, void* stream);
+
 /* K4 (measurement only): the RNG roofline.  Every thread of a full-occupancy grid (sm_count x 8 blocks x
  * 256 threads) draws `iters` Philox4x32-10 blocks with distinct counters and XOR-folds them
  * into d_sink[thread] (so nothing is dead code); blocks drawn = sm_count * 2048 * iters.  The caller times

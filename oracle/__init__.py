@@ -13,7 +13,8 @@ Pins (tests/test_oracle_*.py):
     simulator on small random traces, the Lindley recursion at B = 1 (textbook special case),
     Pollaczek-Khinchine M/D/1 mean wait (statistical), conservation / gate / FCFS invariants;
   * p99 / goodput — SPEC nearest-rank examples (S:123-128) and S:135-136;
-  * score / neighbours / move — S:73-75, S:201-202, S:210, S:278-280 (oracle/climb.py).
+  * score / neighbours / move — S:73-75, S:201-202, S:210, S:278-280 (oracle/climb.py);
+  * Pareto front — the O(n^2) definition (oracle/pareto.py): hand example, floors, front properties.
 Parity unpinned: absolute paper simulator values (calibration unpublished).
 """
 from __future__ import annotations

@@ -22,7 +22,8 @@ STATUS = {0: "ok", -1: "SLO_E_INVAL", -2: "SLO_E_NOMEM", -3: "SLO_E_CUDA", -4: "
 EXPORTS = ("slo_sim_create", "slo_sim_destroy", "slo_sim_get_info", "slo_sim_run", "slo_sim_run_batch",
            "slo_sim_run_batch_host", "slo_aggregate", "slo_aggregate_reduce", "slo_neighbors",
            "slo_hillclimb_step", "slo_exchange_create", "slo_exchange_open", "slo_aggregate_exchange",
-           "slo_exchange_error", "slo_exchange_destroy", "slo_philox_peak", "slo_status_string", "slo_last_error")
+           "slo_exchange_error", "slo_exchange_destroy", "slo_philox_peak", "slo_pareto_front", "slo_status_string",
+           "slo_last_error")
 EXCHANGE_HANDLE_BYTES = 64
 
 
@@ -136,6 +137,7 @@ def lib():
         L.slo_exchange_error.argtypes = [vp, C.POINTER(C.c_uint32)]
         L.slo_exchange_destroy.argtypes = [vp]
         L.slo_philox_peak.argtypes = [vp, C.c_uint32, vp, vp]
+        L.slo_pareto_front.argtypes = [vp, vp, C.c_uint32, vp, vp, vp]
         L.slo_status_string.argtypes = [C.c_int32]
         L.slo_status_string.restype = C.c_char_p
         L.slo_last_error.argtypes = [vp]

@@ -39,6 +39,8 @@ struct slo_sim {
   slo_replica_result* d_part = nullptr;
   size_t part_cap = 0;
   size_t lat_budget = (size_t)4 << 30;  // bytes of latency rows per launch chunk
+  char* d_pareto = nullptr;         // K5 scratch (grow-only)
+  size_t pareto_cap = 0;
   // host-entry scratch
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -252,6 +254,7 @@ slo_status slo_sim_destroy(slo_sim* h) {
     if (h->d_lat) cudaFree(h->d_lat);
     if (h->d_part) cudaFree(h->d_part);
     if (h->d_scratch) cudaFree(h->d_scratch);
+    if (h->d_pareto) cudaFree(h->d_pareto);
   }
   delete h;
   return SLO_OK;
@@ -606,6 +609,20 @@ slo_status slo_aggregate_exchange(slo_sim* h, slo_exchange* x, const slo_replica
   if (wblocks > (unsigned)h->sm_count) wblocks = (unsigned)h->sm_count;
   slo::slo_exchange_wait_kernel<<<wblocks, threads, 0, st>>>(x->window, x->n_cfg, x->world, x->st, d_pooled);
   CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+slo_status slo_pareto_front(slo_sim* h, const slo_config_agg* d_agg, uint32_t n_cfg, uint8_t* d_on_front,
+                            uint32_t* d_count, void* stream) {
+  if (!h || !d_agg || !d_on_front || n_cfg == 0) return fail(h, SLO_E_INVAL, "pareto_front: bad arguments");
+  if (n_cfg >= (1u << 30)) return fail(h, SLO_E_RANGE, "pareto_front: n_cfg >= 2^30");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t cub_bytes = 0;
+  const size_t need = slo::pareto_scratch_bytes(n_cfg, &cub_bytes);
+  slo_status s;
+  if ((s = ensure(h, h->d_pareto, h->pareto_cap, need, st)) != SLO_OK) return s;
+  CUDA_TRY(h, slo::pareto_launch(d_agg, n_cfg, d_on_front, d_count, h->d_pareto, cub_bytes, st));
   return SLO_OK;
 }
 

@@ -77,6 +77,10 @@ __global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uin
                                          slo_config_agg* out);
 
 __global__ void slo_philox_peak_kernel(uint32_t iters, uint32_t* sink);   // K4: RNG roofline
+// K5 Pareto front (slo_pareto.cu): scratch bytes for n configs (cub temp part returned separately), launch
+size_t pareto_scratch_bytes(uint32_t n, size_t* cub_bytes_out);
+cudaError_t pareto_launch(const slo_config_agg* agg, uint32_t n, uint8_t* front, uint32_t* count, void* scratch,
+                          size_t cub_bytes, cudaStream_t st);
 
 // host+device neighbour generation
 __host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& K, slo_knobs* out, uint32_t cap);

@@ -244,6 +244,15 @@ class Simulator:
                                            _stream_ptr(stream)), self.h)
         return out
 
+    def pareto_front(self, agg: torch.Tensor, count: bool = False, stream=None):
+        """K5: uint8 [n_cfg] on-front flags of the per-config aggregates (min mean p99, max goodput)."""
+        n = agg.shape[0]
+        front = torch.empty(n, dtype=torch.uint8, device=agg.device)
+        cnt = torch.zeros(1, dtype=torch.int32, device=agg.device) if count else None
+        check(lib().slo_pareto_front(self.h, agg.data_ptr(), n, front.data_ptr(), _ptr(cnt), _stream_ptr(stream)),
+              self.h)
+        return (front, cnt) if count else front
+
     def philox_peak(self, iters: int = 2048, repeats: int = 3) -> float:
         """K4: measured Philox4x32-10 blocks/s at full occupancy (the RNG roofline)."""
         sm = self.info()["sm_count"]

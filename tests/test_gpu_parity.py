@@ -493,3 +493,35 @@ def test_maximum_segment_and_saturated_latencies(S, orc):
     from paper_2603_11340_b200._lib import SloError
     with pytest.raises(SloError):
         _run_gpu(S, wls, ks[:1], seeds, N - 99, warmup=100, latencies=False)
+
+
+def test_pareto_front_matches_oracle(S):
+    """K5: the device's O(n log n) front equals the oracle's
+    O(n^2) definition on random aggregates with many ties, invalid records and saturated goodput, and on the
+    aggregates of a real C2-grid sweep."""
+    from oracle import pareto
+    from paper_2603_11340_b200._lib import AGG_DTYPE
+    s = S.Simulator([inputs.preset_ll()], device=0)
+    rng = np.random.default_rng(8)
+    for n in (1, 2, 37, 1000, 3000):
+        a = np.zeros(n, AGG_DTYPE)
+        a["n_seeds"] = rng.integers(0, 5, n)
+        a["sum_p99_us"] = rng.integers(0, 6, n) * 100_000 * a["n_seeds"]
+        a["sum_window_us"] = rng.integers(1, 4, n) * 10**6
+        a["sum_slo_met"] = rng.integers(0, 8, n)
+        a["flags"] = (rng.random(n) < 0.05).astype(np.uint32)
+        a[0]["sum_slo_met"], a[0]["sum_window_us"] = 2**63, 1                  # goodput saturates u64
+        dev = torch.from_numpy(a.view(np.uint8).reshape(n, 32).copy()).cuda()
+        f, cnt = s.pareto_front(dev, count=True)
+        torch.cuda.synchronize()
+        rows = [dict(zip(AGG_DTYPE.names, (int(v) for v in r))) for r in a]
+        ref = pareto.pareto_front(rows)
+        assert f.cpu().numpy().astype(bool).tolist() == ref and int(cnt.item()) == sum(ref), n
+    cfg = inputs.config_c2(n_seeds=4, segment_len=500)
+    out = s.run_batch(S.knobs_tensor(cfg.knobs), S.seeds_tensor(cfg.seeds()), 500)
+    agg = s.aggregate(out["detail"], len(cfg.knobs), 4)
+    f = s.pareto_front(agg)
+    torch.cuda.synchronize()
+    rows = [dict(zip(AGG_DTYPE.names, (int(v) for v in r))) for r in S.unpack(agg, AGG_DTYPE)]
+    assert f.cpu().numpy().astype(bool).tolist() == pareto.pareto_front(rows)
+    s.close()
