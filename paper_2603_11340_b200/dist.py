@@ -114,6 +114,8 @@ class ClimbGraph:
                       if self.w > 1 else self.agg)
         # N > 1: "nccl" = K2 + NCCL all-gather + K3 summing the parts; "p2p" = PeerExchange (K2x + K2w)
         self.xchg = PeerExchange(sim, n_cand) if (self.w > 1 and exchange == "p2p") else None
+        self.evaluated = torch.empty_like(self.cands)          # the step's candidates (K3 rewrites cands)
+        self.scores = torch.empty(n_cand, dtype=torch.int64, device=self.cands.device)
         self.stream = torch.cuda.Stream(device=self.cands.device)
         self.graph = None
 
@@ -121,14 +123,17 @@ class ClimbGraph:
         c = self.cfg
         self.sim.run_batch(self.cands, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out,
                            stream=self.stream)
+        self.evaluated.copy_(self.cands)
         if self.xchg is not None:
             self.xchg.pooled(self.out["detail"], self.n_seeds, self.agg, stream=self.stream)
-            self.sim.hillclimb_step(self.space, self.sp, self.cands, self.agg, 1, self.state, stream=self.stream)
+            self.sim.hillclimb_step(self.space, self.sp, self.cands, self.agg, 1, self.state, scores=self.scores,
+                                    stream=self.stream)
             return
         self.sim.aggregate(self.out["detail"], self.n_cand, self.n_seeds, out=self.agg, stream=self.stream)
         if self.w > 1:
             dist.all_gather_into_tensor(self.parts, self.agg)
-        self.sim.hillclimb_step(self.space, self.sp, self.cands, self.parts, self.w, self.state, stream=self.stream)
+        self.sim.hillclimb_step(self.space, self.sp, self.cands, self.parts, self.w, self.state, scores=self.scores,
+                                stream=self.stream)
 
     def capture(self):
         """Warm up (allocates the library's scratch), restore the initial state, capture one step."""
@@ -150,6 +155,47 @@ class ClimbGraph:
         for _ in range(steps):
             self.graph.replay()
         return self.state, self.cands
+
+    def trajectory(self, steps: int, path=None) -> List[dict]:
+        """Run `steps` climb steps from the current device state and return (and, with `path`, write as JSON
+        lines — SPEC S:257/S:300 TuningTrajectory) one record per step: the evaluated candidates and their
+        Eq. (3) scores, the argmax, whether K moved, the next K, the best-so-far and the EMA p99."""
+        import json
+        import numpy as np
+        from . import sim as S
+        from ._lib import CLIMB_DTYPE, KNOB_DTYPE
+        if self.graph is None:
+            self.capture()
+        nb = self.state.numel()
+        h_st = torch.empty((steps, nb), dtype=torch.uint8).pin_memory()
+        h_ev = torch.empty((steps,) + tuple(self.evaluated.shape), dtype=torch.uint8).pin_memory()
+        h_sc = torch.empty((steps, self.n_cand), dtype=torch.int64).pin_memory()
+        st = self.stream
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for i in range(steps):
+                self.graph.replay()
+                h_st[i].copy_(self.state.view(-1), non_blocking=True)
+                h_ev[i].copy_(self.evaluated, non_blocking=True)
+                h_sc[i].copy_(self.scores, non_blocking=True)
+        st.synchronize()
+        recs = []
+        for i in range(steps):
+            s = h_st[i].numpy().view(CLIMB_DTYPE)[0]
+            ks = S.unpack_knobs(h_ev[i].numpy().view(KNOB_DTYPE))
+            sc = h_sc[i].numpy().tolist()
+            valid = [j for j, k in enumerate(ks) if k["conc"] > 0]
+            recs.append({"step": int(s["step"]), "current": ks[0],
+                         "candidates": [ks[j] for j in valid], "scores_micro": [sc[j] for j in valid],
+                         "argmax": int(s["argmax"]), "moved": bool(s["moved"]),
+                         "next": S.unpack_knobs(np.array([s["K"]]))[0],
+                         "best": S.unpack_knobs(np.array([s["K_best"]]))[0], "best_score_micro": int(s["S_best_micro"]),
+                         "ema_p99_us": int(s["ema_p99_us"]) if int(s["has_ema"]) else None})
+        if path is not None:
+            with open(path, "w") as fh:
+                for r in recs:
+                    fh.write(json.dumps(r) + "\n")
+        return recs
 
     def run_host(self, steps: int, h_cands: torch.Tensor, h_state: torch.Tensor, h_traj: torch.Tensor):
         """End-to-end use from host memory: copy the starting candidates and climb state in (pinned host ->

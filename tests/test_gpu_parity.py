@@ -525,3 +525,26 @@ def test_pareto_front_matches_oracle(S):
     rows = [dict(zip(AGG_DTYPE.names, (int(v) for v in r))) for r in S.unpack(agg, AGG_DTYPE)]
     assert f.cpu().numpy().astype(bool).tolist() == pareto.pareto_front(rows)
     s.close()
+
+
+def test_climb_trajectory_jsonl(S, orc, tmp_path):
+    """ClimbGraph.trajectory (SPEC S:257/S:300 TuningTrajectory as JSON lines): every step's evaluated
+    candidates and scores equal oracle/climb.py's Eq. (3) on oracle replicas, and its move, argmax and next K
+    equal the oracle's Alg. 1 step."""
+    import json
+    from oracle import climb
+    from paper_2603_11340_b200.dist import ClimbGraph
+    cfg = inputs.config_c4(n_seeds=3, segment_len=300)
+    s = S.Simulator(cfg.workloads, device=0)
+    g = ClimbGraph(s, cfg, cfg.seeds()).capture()
+    recs = g.trajectory(3, path=tmp_path / "traj.jsonl")
+    lines = [json.loads(l) for l in open(tmp_path / "traj.jsonl")]
+    assert lines == json.loads(json.dumps(recs)) and len(lines) == 3
+    state = climb.initial_state(cfg.knobs[0])
+    for r in lines:
+        cands = r["candidates"]
+        aggs = [climb.aggregate([orc.run(cfg.workloads, k, sd, 300) for sd in cfg.seeds()]) for k in cands]
+        state, moved, am, scores = climb.step(state, cands, aggs, cfg.extra["score"])
+        assert r["scores_micro"] == scores and r["moved"] == moved and r["argmax"] == am
+        assert r["next"] == state["K"] and r["best"] == state["K_best"]
+    s.close()
