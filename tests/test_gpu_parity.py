@@ -548,3 +548,38 @@ def test_climb_trajectory_jsonl(S, orc, tmp_path):
         assert r["scores_micro"] == scores and r["moved"] == moved and r["argmax"] == am
         assert r["next"] == state["K"] and r["best"] == state["K_best"]
     s.close()
+
+
+def test_pareto_front_properties_at_scale(S):
+    """K5 on a 62,500-config sweep (the C5s grid, 2 seeds): properties that hold at any size — the front
+    sorted by mean p99 has strictly increasing goodput, and every valid config off the front is dominated
+    by a config on it (vectorised check of the definition against the front)."""
+    from oracle import pareto
+    from paper_2603_11340_b200._lib import AGG_DTYPE
+    cfg = inputs.config_c5(stride=16, n_seeds=2, segment_len=400)
+    s = S.Simulator(cfg.workloads, device=0)
+    out = s.run_batch(S.knobs_tensor(cfg.knobs), S.seeds_tensor(cfg.seeds()), 400)
+    agg = s.aggregate(out["detail"], len(cfg.knobs), 2)
+    f = s.pareto_front(agg).cpu().numpy().astype(bool)
+    a = S.unpack(agg, AGG_DTYPE)
+    n = a["n_seeds"].astype(object)
+    valid = (a["n_seeds"] > 0) & ((a["flags"] & 1) == 0) & (a["sum_window_us"] > 0)
+    p = np.array([int(x) // int(k) if k else 0 for x, k in zip(a["sum_p99_us"], n)], dtype=np.int64)
+    g = np.array([int(m) * 10**12 // int(w) if w else 0 for m, w in zip(a["sum_slo_met"], a["sum_window_us"])],
+                 dtype=np.float64)                 # < 2^53 here (goodput < 10^3 rps)
+    assert f.sum() > 0 and not (f & ~valid).any()
+    fp, fg = p[f], g[f]
+    order = np.lexsort((-fg, fp))
+    up, ug = fp[order], fg[order]
+    keep = np.r_[True, (up[1:] != up[:-1]) | (ug[1:] != ug[:-1])]
+    assert np.all(np.diff(up[keep]) > 0) and np.all(np.diff(ug[keep]) > 0)
+    off = np.where(valid & ~f)[0]
+    for chunk in np.array_split(off, max(1, len(off) // 4096)):
+        dom = ((fp[None, :] <= p[chunk, None]) & (fg[None, :] >= g[chunk, None]) &
+               ((fp[None, :] < p[chunk, None]) | (fg[None, :] > g[chunk, None]))).any(axis=1)
+        assert dom.all()
+    # and the first 600 configs against the definition itself
+    rows = [dict(zip(AGG_DTYPE.names, (int(v) for v in r))) for r in a[:600]]
+    sub = s.pareto_front(agg[:600].contiguous()).cpu().numpy().astype(bool).tolist()
+    assert sub == pareto.pareto_front(rows)
+    s.close()
