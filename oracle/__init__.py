@@ -105,6 +105,15 @@ def lib():
         L.orc_run.argtypes = [C.POINTER(Workload), C.c_uint32, C.POINTER(Knobs), C.c_uint64, C.c_uint32,
                               C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Result),
                               C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
+        L.orc_run_stop.argtypes = [C.POINTER(Workload), C.c_uint32, C.POINTER(Knobs), C.c_uint64, C.c_uint32,
+                                   C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Result),
+                                   C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
+        L.orc_run_trace_stop.argtypes = [C.POINTER(Timing), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                         C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32,
+                                         C.c_uint32, C.c_uint32, C.POINTER(Result), C.POINTER(C.c_uint32),
+                                         C.POINTER(Req), C.POINTER(Counters)]
         L.orc_run_trace.argtypes = [C.POINTER(Timing), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
@@ -215,17 +224,19 @@ def _pack(res: Result, cnt: Counters, lat, trace) -> Dict:
 
 
 def run(workloads: Sequence[Dict], knobs: Dict, seed: int, segment_len: int, warmup_len: int = 0,
-        slo_us: int = 1_200_000, crn: int = 1, latencies: bool = False, trace: bool = False) -> Dict:
-    """One replica in Philox mode."""
+        slo_us: int = 1_200_000, crn: int = 1, latencies: bool = False, trace: bool = False,
+        stop_n_min: int = 0, stop_t_min_us: int = 0) -> Dict:
+    """One replica in Philox mode (with a segment stop rule, §2.14)."""
     ws = _WorkloadSet(workloads)
     k = make_knobs(knobs)
     N = segment_len + warmup_len
     res, cnt = Result(), Counters()
     lat = np.zeros(N, np.uint32) if latencies else None
     tr = (Req * N)() if trace else None
-    rc = lib().orc_run(ws.arr, ws.n, C.byref(k), seed, crn, segment_len, warmup_len, slo_us, C.byref(res),
-                       lat.ctypes.data_as(C.POINTER(C.c_uint32)) if lat is not None else None,
-                       tr, C.byref(cnt))
+    rc = lib().orc_run_stop(ws.arr, ws.n, C.byref(k), seed, crn, segment_len, warmup_len, slo_us, stop_n_min,
+                            stop_t_min_us, C.byref(res),
+                            lat.ctypes.data_as(C.POINTER(C.c_uint32)) if lat is not None else None,
+                            tr, C.byref(cnt))
     if rc != 0:
         raise ValueError(f"orc_run failed: {rc}")
     return _pack(res, cnt, lat, tr)
@@ -234,7 +245,7 @@ def run(workloads: Sequence[Dict], knobs: Dict, seed: int, segment_len: int, war
 def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_us: int,
               a: Sequence[int], P: Sequence[int], O: Sequence[int], f: Optional[Sequence[int]] = None,
               A: Optional[Sequence[Sequence[int]]] = None, warmup_len: int = 0, slo_us: int = 1_200_000,
-              issue_origin: int = 0, continuous: int = 0) -> Dict:
+              issue_origin: int = 0, continuous: int = 0, stop_n_min: int = 0, stop_t_min_us: int = 0) -> Dict:
     """Trace mode: explicit requests (a, P, O), per-request noise factor f (ppm) and accepted-prefix draws."""
     n = len(a)
     tm = Timing(**timing)
@@ -253,11 +264,9 @@ def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_u
     res, cnt = Result(), Counters()
     lat = np.zeros(n, np.uint32)
     tr = (Req * n)()
-    rc = lib().orc_run_trace(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, issue_origin, continuous, n, a_,
-                             P_, O_, f_,
-                             off_, val_,
-                             warmup_len, slo_us, C.byref(res), lat.ctypes.data_as(C.POINTER(C.c_uint32)), tr,
-                             C.byref(cnt))
+    rc = lib().orc_run_trace_stop(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, issue_origin, continuous, n,
+                                  a_, P_, O_, f_, off_, val_, warmup_len, slo_us, stop_n_min, stop_t_min_us,
+                                  C.byref(res), lat.ctypes.data_as(C.POINTER(C.c_uint32)), tr, C.byref(cnt))
     if rc != 0:
         raise ValueError(f"orc_run_trace failed: {rc}")
     return _pack(res, cnt, lat, tr)

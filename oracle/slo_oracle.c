@@ -255,14 +255,78 @@ static uint64_t step_cost(const orc_timing* tm, uint32_t gamma, uint64_t n) {
          (uint64_t)tm->ver_tok_us * (uint64_t)(gamma + 1) * n;
 }
 
+static int cmp_u64(const void* x, const void* y) {
+  uint64_t a = *(const uint64_t*)x, b = *(const uint64_t*)y;
+  return (a > b) - (a < b);
+}
+
 static int cmp_u32(const void* x, const void* y) {
   uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
   return (a > b) - (a < b);
 }
 
+/* DESIGN.md §2.8 (+ §2.14 stop rule) — replica outputs from the completion times c[] of all N requests.
+ * Without a stop rule every measured request (i >= warmup) counts.  With one (n_min, t_min), the segment
+ * ends at t* = the k-th smallest measured completion time for the smallest k >= max(n_min, 1) with
+ * c_(k) - t0 >= t_min (t0 = origin of request `warmup`); only requests with c <= t* count and every request
+ * completing after t* stores the sentinel latency U32MAX; if no k qualifies, every measured request counts
+ * and flags bit 2 is set (the source ran out first). */
+static void outputs(uint32_t N, uint32_t warmup, uint32_t slo_us, const uint64_t* c, const uint64_t* origin,
+                    const orc_stop* stop, orc_result* res, uint32_t* lat) {
+  const uint32_t nm = N - warmup;
+  const uint64_t t0 = origin[warmup];
+  uint64_t tstar = U64MAX;
+  uint32_t flags = 0;
+  if (stop && (stop->n_min || stop->t_min_us)) {
+    uint64_t* cm = (uint64_t*)malloc((size_t)nm * sizeof(uint64_t));
+    if (!cm) abort();
+    memcpy(cm, c + warmup, (size_t)nm * sizeof(uint64_t));
+    qsort(cm, nm, sizeof(uint64_t), cmp_u64);
+    const uint32_t need = stop->n_min > 0 ? stop->n_min : 1u;
+    int found = 0;
+    for (uint32_t k = need; k <= nm; ++k) {
+      if (cm[k - 1] >= t0 + stop->t_min_us) {
+        tstar = cm[k - 1];
+        found = 1;
+        break;
+      }
+    }
+    if (!found) flags |= 4u;
+    free(cm);
+  }
+  uint32_t n = 0, slo_met = 0;
+  uint64_t sum = 0, cmax = 0;
+  uint32_t* sorted = (uint32_t*)malloc((size_t)nm * sizeof(uint32_t));
+  if (!sorted) abort();
+  for (uint32_t i = 0; i < N; ++i) {
+    const uint64_t l = c[i] - origin[i];
+    const int inc = c[i] <= tstar;
+    lat[i] = !inc ? U32MAX : (l > U32MAX ? U32MAX : (uint32_t)l);
+    if (i >= warmup && inc) {
+      if (l > U32MAX) flags |= 2u;
+      if (l <= slo_us) ++slo_met;
+      sum += l;
+      if (c[i] > cmax) cmax = c[i];
+      sorted[n++] = lat[i];
+    }
+  }
+  qsort(sorted, n, sizeof(uint32_t), cmp_u32);
+  res->p99_us = sorted[(uint32_t)((99ull * n + 99ull) / 100ull) - 1]; /* nearest rank, ceil(0.99 n) */
+  res->p50_us = sorted[(uint32_t)((50ull * n + 99ull) / 100ull) - 1]; /* ceil(0.50 n) */
+  res->p95_us = sorted[(uint32_t)((95ull * n + 99ull) / 100ull) - 1]; /* ceil(0.95 n) */
+  res->slo_met = slo_met;
+  res->n_measured = n;
+  res->flags = flags;
+  const uint64_t T = cmax - t0;
+  res->window_us = T < 1 ? 1 : T;
+  res->sum_latency_us = sum;
+  res->goodput = (double)((uint64_t)slo_met * 1000000ull) / (double)res->window_us;
+  free(sorted);
+}
+
 static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t mw, uint32_t issue_origin,
                     uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
-                    const uint32_t* f, adraw* ad, uint32_t warmup, uint32_t slo_us,
+                    const uint32_t* f, adraw* ad, uint32_t warmup, uint32_t slo_us, const orc_stop* stop,
                     orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
   uint64_t* s = (uint64_t*)calloc(N, sizeof(uint64_t));
   uint64_t* form = (uint64_t*)calloc(N, sizeof(uint64_t));
@@ -360,35 +424,7 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
 
   /* outputs; latency from arrival (open loop, R2) or from issue (closed loop, §2.11) */
   const uint64_t* origin = issue_origin ? s : a;
-  uint32_t n = N - warmup;
-  uint32_t slo_met = 0, flags = 0;
-  uint64_t sum = 0, cmax = 0;
-  for (uint32_t i = 0; i < N; ++i) {
-    uint64_t l = c[i] - origin[i];
-    lat[i] = l > U32MAX ? U32MAX : (uint32_t)l;
-    if (i >= warmup) {
-      if (l > U32MAX) flags |= 2u;
-      if (l <= slo_us) ++slo_met;
-      sum += l;
-      if (c[i] > cmax) cmax = c[i];
-    }
-  }
-  uint32_t* sorted = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
-  if (!sorted) abort();
-  memcpy(sorted, lat + warmup, (size_t)n * sizeof(uint32_t));
-  qsort(sorted, n, sizeof(uint32_t), cmp_u32);
-  uint32_t r = (uint32_t)((99ull * n + 99ull) / 100ull); /* nearest rank, ceil(0.99 n) */
-  res->p99_us = sorted[r - 1];
-  res->p50_us = sorted[(uint32_t)((50ull * n + 99ull) / 100ull) - 1];   /* ceil(0.50 n) */
-  res->p95_us = sorted[(uint32_t)((95ull * n + 99ull) / 100ull) - 1];   /* ceil(0.95 n) */
-  res->slo_met = slo_met;
-  res->n_measured = n;
-  res->flags = flags;
-  uint64_t T = cmax - origin[warmup];
-  res->window_us = T < 1 ? 1 : T;
-  res->sum_latency_us = sum;
-  res->goodput = (double)((uint64_t)slo_met * 1000000ull) / (double)res->window_us;
-
+  outputs(N, warmup, slo_us, c, origin, stop, res, lat);
   if (latencies) memcpy(latencies, lat, (size_t)N * sizeof(uint32_t));
   if (trace) {
     for (uint32_t i = 0; i < N; ++i) {
@@ -408,7 +444,6 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
     cnt->member_steps = member_steps;
     cnt->philox_blocks = spec_blocks; /* caller adds REQ and PHASE blocks */
   }
-  free(sorted);
   free(s); free(form); free(c); free(steps); free(batch_of); free(pend); free(rem); free(lat);
   return ad->bad ? -2 : 0;
 }
@@ -434,7 +469,8 @@ static uint64_t iter_noise(const itnoise* nz, uint64_t it) {
 static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t issue_origin,
                          uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
                          const uint32_t* f, adraw* ad, const itnoise* nz, uint32_t warmup, uint32_t slo_us,
-                         orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+                         const orc_stop* stop, orc_result* res, uint32_t* latencies, orc_req* trace,
+                         orc_counters* cnt) {
   uint64_t* s = (uint64_t*)calloc(N, sizeof(uint64_t));
   uint64_t* form = (uint64_t*)calloc(N, sizeof(uint64_t));   /* admission (prefill start) */
   uint64_t* c = (uint64_t*)calloc(N, sizeof(uint64_t));
@@ -527,33 +563,7 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
   }
 
   const uint64_t* origin = issue_origin ? s : a;
-  uint32_t n = N - warmup;
-  uint32_t slo_met = 0, flags = 0;
-  uint64_t sum = 0, cmax = 0;
-  for (uint32_t i = 0; i < N; ++i) {
-    uint64_t l = c[i] - origin[i];
-    lat[i] = l > U32MAX ? U32MAX : (uint32_t)l;
-    if (i >= warmup) {
-      if (l > U32MAX) flags |= 2u;
-      if (l <= slo_us) ++slo_met;
-      sum += l;
-      if (c[i] > cmax) cmax = c[i];
-    }
-  }
-  uint32_t* sorted = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
-  if (!sorted) abort();
-  memcpy(sorted, lat + warmup, (size_t)n * sizeof(uint32_t));
-  qsort(sorted, n, sizeof(uint32_t), cmp_u32);
-  res->p99_us = sorted[(uint32_t)((99ull * n + 99ull) / 100ull) - 1];
-  res->p50_us = sorted[(uint32_t)((50ull * n + 99ull) / 100ull) - 1];
-  res->p95_us = sorted[(uint32_t)((95ull * n + 99ull) / 100ull) - 1];
-  res->slo_met = slo_met;
-  res->n_measured = n;
-  res->flags = flags;
-  uint64_t T = cmax - origin[warmup];
-  res->window_us = T < 1 ? 1 : T;
-  res->sum_latency_us = sum;
-  res->goodput = (double)((uint64_t)slo_met * 1000000ull) / (double)res->window_us;
+  outputs(N, warmup, slo_us, c, origin, stop, res, lat);
   if (latencies) memcpy(latencies, lat, (size_t)N * sizeof(uint32_t));
   if (trace) {
     for (uint32_t i = 0; i < N; ++i) {
@@ -573,7 +583,6 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
     cnt->member_steps = member_steps;
     cnt->philox_blocks = spec_blocks + ((nz->philox && nz->step_ppm) ? decode_iters : 0);
   }
-  free(sorted);
   free(s); free(form); free(c); free(steps); free(batch_of); free(rem); free(run); free(fin); free(lat);
   return ad->bad ? -2 : 0;
 }
@@ -588,6 +597,13 @@ static void invalid_result(orc_result* res) {
 int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
             uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
             orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  return orc_run_stop(wl, n_wl, k, seed, crn, segment_len, warmup_len, slo_us, 0, 0, res, latencies, trace, cnt);
+}
+
+int orc_run_stop(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
+                 uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us, uint32_t stop_n_min,
+                 uint32_t stop_t_min_us, orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  const orc_stop stop = {stop_n_min, stop_t_min_us};
   if (!wl || !k || !res || segment_len == 0 || n_wl == 0) return -1;
   if ((uint64_t)segment_len + warmup_len > ORC_MAX_N) return -1;
   if (slo_us == U32MAX) return -1;
@@ -619,10 +635,10 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
   if (W->batching == 1) {
     itnoise nz = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, W->timing.noise_step_ppm};
     rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, W->arr.kind == 3, N, a, P, O, f, &ad, &nz,
-                       warmup_len, slo_us, res, latencies, trace, cnt);
+                       warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   } else {
     rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, W->arr.kind == 3, N, a, P, O, f, &ad,
-                  warmup_len, slo_us, res, latencies, trace, cnt);
+                  warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   }
   if (cnt) cnt->philox_blocks += N + (W->arr.kind == 1 ? (uint64_t)phases : 0);
   free(a); free(P); free(O); free(w3); free(f);
@@ -635,6 +651,17 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  return orc_run_trace_stop(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, continuous, n, a, P, O, f,
+                            A_off, A_val, warmup_len, slo_us, 0, 0, res, latencies, trace, cnt);
+}
+
+int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
+                       uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
+                       const uint64_t* a, const uint32_t* P,
+                       const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
+                       uint32_t warmup_len, uint32_t slo_us, uint32_t stop_n_min, uint32_t stop_t_min_us,
+                       orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+  const orc_stop stop = {stop_n_min, stop_t_min_us};
   if (!tm || !a || !P || !O || !f || !res || n == 0 || warmup_len >= n) return -1;
   if (conc < 1 || max_num_seqs < 1) return -1;
   if (gamma_eff > 0 && (!A_off || !A_val)) return -1;
@@ -647,8 +674,8 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
   if (continuous) {
     itnoise nz = {0, 0, 0, 0};
     return simulate_cont(tm, conc, max_num_seqs, gamma_eff, issue_origin, n, a, P, O, f, &ad, &nz, warmup_len,
-                         slo_us, res, latencies, trace, cnt);
+                         slo_us, &stop, res, latencies, trace, cnt);
   }
   return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, warmup_len,
-                  slo_us, res, latencies, trace, cnt);
+                  slo_us, &stop, res, latencies, trace, cnt);
 }

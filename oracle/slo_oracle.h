@@ -85,6 +85,15 @@ int orc_run(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t 
             uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
             orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);
 
+/* DESIGN.md §2.14 segment stop rule: at least n_min measured completions and t_min_us since t0 (0, 0 = off). */
+typedef struct {
+  uint32_t n_min, t_min_us;
+} orc_stop;
+
+int orc_run_stop(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
+                 uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us, uint32_t stop_n_min,
+                 uint32_t stop_t_min_us, orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);
+
 /* Trace mode: explicit arrivals a[n], lengths P[n], O[n], per-request noise factor f[n] (ppm, used when
  * the request heads a batch / a prefill), and per-request accepted-prefix draws A_val[A_off[i] + j] for
  * decode step j of request i (A_off has n+1 entries).  gamma_eff is given directly.  With `continuous`
@@ -95,6 +104,13 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);
+
+int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
+                       uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
+                       const uint64_t* a, const uint32_t* P, const uint32_t* O, const uint32_t* f,
+                       const uint32_t* A_off, const uint32_t* A_val, uint32_t warmup_len, uint32_t slo_us,
+                       uint32_t stop_n_min, uint32_t stop_t_min_us, orc_result* res, uint32_t* latencies,
+                       orc_req* trace, orc_counters* cnt);
 
 #ifdef __cplusplus
 }
