@@ -534,3 +534,62 @@ def test_continuous_invariants(orc):
             cur += d
             assert cur <= k["max_num_seqs"]
         assert r["slo_met"] <= r["n_measured"]
+
+
+# NEXT-3: the paper's segment stop rule ("minimum duration and minimum number of completions"),
+# DESIGN.md §2.14
+def _stop_trace(orc, n_min, t_min):
+    tm = dict(pre_base_us=100, pre_tok_us=0, dec_base_us=10, dec_seq_us=0, dr_base_us=0, dr_seq_us=0,
+              ver_base_us=0, ver_seq_us=0, ver_tok_us=0, noise_step_ppm=0)
+    # C = B = 1, five one-token requests waiting at t = 0: served back to back, 110 us each
+    return orc.run_trace(tm, 1, 1, 0, 0, [0] * 5, [1] * 5, [1] * 5, warmup_len=1, slo_us=250,
+                         stop_n_min=n_min, stop_t_min_us=t_min)
+
+
+def test_stop_rule_hand_trace(orc):
+    """Completions 110, 220, 330, 440, 550 us; request 0 is warmup, t0 = a_1 = 0."""
+    U = 0xFFFFFFFF
+    r = _stop_trace(orc, 2, 300)          # k >= 2 and c >= 300: t* = 330 -> requests 1, 2
+    assert list(r["latencies"]) == [110, 220, 330, U, U]
+    assert (r["n_measured"], r["p99_us"], r["slo_met"], r["window_us"], r["flags"]) == (2, 330, 1, 330, 0)
+    r = _stop_trace(orc, 3, 0)            # the third measured completion: t* = 440
+    assert (r["n_measured"], r["window_us"], list(r["latencies"])[-1]) == (3, 440, U)
+    r = _stop_trace(orc, 1, 500)          # the first completion at or after 500 us: t* = 550, all four
+    assert (r["n_measured"], r["window_us"], r["flags"]) == (4, 550, 0)
+    r = _stop_trace(orc, 5, 0)            # only four measured requests: the source runs out, flag bit 2
+    assert (r["n_measured"], r["window_us"], r["flags"]) == (4, 550, 4)
+    r0 = _stop_trace(orc, 0, 0)           # off: the fixed-count segment of R15
+    assert (r0["n_measured"], r0["window_us"], r0["flags"]) == (4, 550, 0)
+
+
+@pytest.mark.parametrize("cont", [0, 1])
+def test_stop_rule_properties(orc, cont):
+    """Philox mode, static and continuous batching: off and "all of the segment" reproduce the fixed-count
+    outputs; the counted set is a prefix of the completion order that grows with n_min and t_min; the counted
+    requests keep their latencies and the rest store the sentinel."""
+    rng = random.Random(11 + cont)
+    for _ in range(12):
+        w = inputs.preset_ll(rate=rng.choice([5.0, 10.0, 40.0]))
+        if cont:
+            w = inputs.continuous(w)
+        k = inputs.random_knobs(rng, max_wait=not cont)
+        k["workload"] = 0
+        seg, warm = rng.choice([(300, 0), (500, 40)])
+        seed = rng.randrange(1 << 30)
+        base = orc.run([w], k, seed, seg, warmup_len=warm, latencies=True, trace=True)
+        full = orc.run([w], k, seed, seg, warmup_len=warm, latencies=True, stop_n_min=seg)
+        for f in ("p99_us", "slo_met", "n_measured", "window_us", "sum_latency_us", "flags", "goodput"):
+            assert full[f] == base[f], f
+        c = base["trace"]["c"]
+        cm = np.sort(c[warm:])
+        t0 = int(base["trace"]["s" if w["arrivals"]["kind"] == 3 else "a"][warm])
+        for n_min, t_min in ((1, 0), (seg // 4, 0), (seg // 2, 10**6), (1, 5 * 10**6), (seg // 3, 2 * 10**6)):
+            r = orc.run([w], k, seed, seg, warmup_len=warm, latencies=True, stop_n_min=n_min, stop_t_min_us=t_min)
+            ok = [i for i in range(n_min, seg + 1) if cm[i - 1] >= t0 + t_min]
+            tstar = int(cm[ok[0] - 1]) if ok else int(cm[-1])
+            inc = c <= tstar
+            assert r["n_measured"] == int(inc[warm:].sum()) >= (n_min if ok else 0)
+            assert (r["flags"] & 4) == (0 if ok else 4)
+            lat = r["latencies"]
+            assert np.array_equal(lat[inc], base["latencies"][inc]) and np.all(lat[~inc] == 0xFFFFFFFF)
+            assert r["window_us"] == max(1, int(c[warm:][inc[warm:]].max()) - t0)
