@@ -92,7 +92,8 @@ typedef struct {
   uint32_t reserved[4];         /* must be 0                                                             */
 } slo_knobs;
 
-/* Per-replica outputs, 32 B. flags: bit0 invalid knobs, bit1 a latency saturated u32. */
+/* Per-replica outputs, 32 B. flags: bit0 invalid knobs, bit1 a latency saturated u32,
+ * bit2 the stop rule (slo_run_args) was not met before the segment's requests ran out. */
 typedef struct {
   uint32_t p99_us, slo_met, n_measured, flags;
   uint64_t window_us, sum_latency_us;
@@ -159,7 +160,13 @@ typedef struct {
   slo_stats* d_stats;           /* or NULL                                                                */
   uint32_t* d_p50_us;           /* [R] nearest-rank p50 or NULL                             */
   uint32_t* d_p95_us;           /* [R] nearest-rank p95 or NULL                                           */
-  uint32_t reserved[4];         /* must be 0                                                              */
+  /* segment stop rule, both 0 = off (R15's fixed count): the segment ends at
+   * the first measured completion t* with >= stop_min_completions measured completions and
+   * t* - t0 >= stop_min_time_us; only requests completing by t* count (n_measured varies), later ones
+   * store latency UINT32_MAX; flags bit 2 if the segment's requests ran out first.  Work counters then
+   * count what was simulated up to the stop. */
+  uint32_t stop_min_completions, stop_min_time_us;
+  uint32_t reserved[2];         /* must be 0                                                              */
 } slo_run_args;
 slo_status slo_sim_run(slo_sim* h, const slo_run_args* args, void* stream);
 

@@ -224,7 +224,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   if (o.scratch_mb) h->lat_budget = (size_t)o.scratch_mb << 20;
   h->group_policy = o.group_policy;
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel) == cudaSuccess) h->regs = fa.numRegs;
+  if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel_t<false>) == cudaSuccess) h->regs = fa.numRegs;
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
@@ -262,7 +262,7 @@ slo_status slo_sim_destroy(slo_sim* h) {
 
 static int blocks_per_sm_for(slo_sim* h, size_t smem) {
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slo::slo_sim_kernel, h->warps_per_block * 32, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slo::slo_sim_kernel_t<false>, h->warps_per_block * 32, smem) !=
           cudaSuccess ||
       occ < 1)
     occ = 1;
@@ -288,7 +288,8 @@ slo_status slo_sim_get_info(const slo_sim* hc, slo_sim_info* info) {
 static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,
                              uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
                              uint32_t* d_p99, double* d_goodput, slo_replica_result* d_detail, uint32_t* d_lat,
-                             slo_stats* d_stats, uint32_t* d_p50, uint32_t* d_p95, cudaStream_t st) {
+                             slo_stats* d_stats, uint32_t* d_p50, uint32_t* d_p95, cudaStream_t st,
+                             uint32_t stop_n = 0, uint32_t stop_t = 0) {
   const uint32_t n_rep = (uint32_t)((uint64_t)n_configs * n_seeds);
   const uint32_t N = warmup_len + segment_len;
   // replicas per launch chunk: the latency rows of a chunk stay within the budget (a caller-provided
@@ -326,21 +327,31 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   p.seg = segment_len;
   p.slo_us = slo_us;
   p.crn = h->crn;
+  p.stop_n = stop_n;
+  p.stop_t = stop_t;
   p.warp_bytes = (uint32_t)slo::group_warp_bytes();
   const size_t smem = (size_t)p.warp_bytes * h->warps_per_block;
   if (smem > 48 * 1024)
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  {
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
   const int bps = blocks_per_sm_for(h, smem);
   int cont_bps = 1;
   slo::SimParams pc{};
   const size_t cont_smem = slo::cont_warp_bytes() * h->warps_per_block;
   if (h->any_cont) {
     if (cont_smem > 48 * 1024)
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)cont_smem));
+    }
     // occupancy is register-bound; give the group rings the whole carveout so smem never binds first
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel, h->warps_per_block * 32,
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel_t<false>, h->warps_per_block * 32,
                                                       cont_smem) != cudaSuccess || cont_bps < 1)
       cont_bps = 1;
     if (h->blocks_per_sm_opt > 0 && h->blocks_per_sm_opt < cont_bps) cont_bps = h->blocks_per_sm_opt;
@@ -374,7 +385,10 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    slo::slo_sim_kernel<<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+    if (p.stop_n | p.stop_t)
+      slo::slo_sim_kernel_t<true><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+    else
+      slo::slo_sim_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
     CUDA_TRY(h, cudaGetLastError());
     if (h->any_cont) {   // K1c: the continuous-batching list, one replica per warp
       uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;
@@ -382,7 +396,10 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       if (cblocks > cneed) cblocks = cneed;
       pc = p;
       pc.warp_bytes = (uint32_t)slo::cont_warp_bytes();
-      slo::slo_sim_cont_kernel<<<(unsigned)cblocks, h->warps_per_block * 32, cont_smem, st>>>(pc);
+      if (p.stop_n | p.stop_t)
+        slo::slo_sim_cont_kernel_t<true><<<(unsigned)cblocks, h->warps_per_block * 32, cont_smem, st>>>(pc);
+      else
+        slo::slo_sim_cont_kernel_t<false><<<(unsigned)cblocks, h->warps_per_block * 32, cont_smem, st>>>(pc);
       CUDA_TRY(h, cudaGetLastError());
     }
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
@@ -407,14 +424,14 @@ slo_status slo_sim_run(slo_sim* h, const slo_run_args* a, void* stream) {
   if (!h) return fail(nullptr, SLO_E_INVAL, "run: null handle");
   if (!a || !a->d_configs || !a->d_seeds || !a->d_p99_us || !a->d_goodput)
     return fail(h, SLO_E_INVAL, "run: null pointer");
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
     if (a->reserved[i]) return fail(h, SLO_E_INVAL, "run: reserved must be 0");
   slo_status s = check_run_args(h, a->n_configs, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us);
   if (s != SLO_OK) return s;
   DeviceGuard g(h->device);
   return launch_sim(h, a->d_configs, a->n_configs, a->d_seeds, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us,
                     a->d_p99_us, a->d_goodput, a->d_detail, a->d_latencies, a->d_stats, a->d_p50_us, a->d_p95_us,
-                    (cudaStream_t)stream);
+                    (cudaStream_t)stream, a->stop_min_completions, a->stop_min_time_us);
 }
 
 slo_status slo_sim_run_batch(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,

@@ -44,10 +44,11 @@ struct SimParams {
   uint32_t r_base, n_chunk;    // this launch covers replicas [r_base, r_base + n_chunk)
   uint32_t warmup, seg, slo_us, crn;
   uint32_t warp_bytes, pad;
+  uint32_t stop_n, stop_t;     // segment stop rule, 0, 0 = off
 };
 
-__global__ void slo_sim_kernel(const SimParams p);
-__global__ void slo_sim_cont_kernel(const SimParams p);   // K1c: continuous batching
+template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
+template <bool STOP> __global__ void slo_sim_cont_kernel_t(const SimParams p);  // K1c: continuous batching (§2.12)
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
                                           uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t wide,
                                           uint32_t* ctl);

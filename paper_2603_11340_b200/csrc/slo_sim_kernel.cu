@@ -118,6 +118,7 @@ struct alignas(16) Group {
   uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, gp;
   uint32_t k0, k1, wl, pad;
   uint4 knob;                         // C, B, max_wait_us, gamma_eff (kept here, not in registers)
+  uint32_t cnt_meas, cnt_incl, stopped, pad3;   // stop rule (§2.14): measured completions, counted ones, done
 };
 
 // A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
@@ -188,6 +189,8 @@ __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const
     R.gp = gp;
     R.k0 = k0;
     R.k1 = k1;
+    R.cnt_meas = 0;
+    R.stopped = 0;
   }
   __syncwarp(gmask);
   if (gamma > 0) {  // bucket guide for A(u)
@@ -348,7 +351,7 @@ __device__ __forceinline__ void flush_counters(const SimParams& p, Counters& ct)
 // ------------------------------------------------------------------------------------------------
 // one lane-group mode of K1: groups pull replicas from work list `cls` until it is exhausted
 // ------------------------------------------------------------------------------------------------
-template <int G>
+template <int G, bool STOP>
 __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   constexpr int RING = Group<G>::RING;
   const int g = lane / G, li = lane % G;
@@ -394,6 +397,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
             if (li == 0) {
               R.knob = make_uint4(k.conc, k.max_num_seqs, k.max_wait_us, gamma);
               R.wl = k.workload;
+              R.cnt_incl = 0;
             }
             setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
             rowoff = (r - p.r_base) * N;           // < 2^32: a chunk's rows are capped by the scratch budget
@@ -492,12 +496,33 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const bool from_issue = R.kind == 3;
     if (from_issue && member && i == p.warmup) R.a_w = s_orig;     // the goodput window starts at that issue
     const uint64_t l = c - (member ? (from_issue ? s_orig : R.a[i % RING]) : c);
-    if (measured) {
+    // stop rule (§2.14): this batch's measured completions in sorted (= time) order continue the count;
+    // the first one that is the k-th with k >= n_min and ends >= t0 + t_min is t*, and only c <= t* counts
+    bool inc = true;
+    if constexpr (STOP) {                           // compiled into the stop-rule kernels only
+      __syncwarp();                                 // R.a_w of a closed-loop warmup issue written above
+      const uint32_t mm = gballot<G>(measured, lane);
+      const uint32_t before = active ? R.cnt_meas : 0u;
+      const uint32_t kpos = before + __popc(mm & ((1u << li) - 1u)) + 1u;
+      const uint32_t need = p.stop_n ? p.stop_n : 1u;
+      const bool cand = active && !R.stopped && measured && kpos >= need && c >= R.a_w + p.stop_t;
+      const uint32_t cmk = gballot<G>(cand, lane);
+      const uint64_t tstar = gshfl64<G>(c, (int)((cmk ? __ffs(cmk) - 1 : 0) & (G - 1)));
+      inc = cmk == 0 || c <= tstar;
+      const uint32_t ninc = __popc(gballot<G>(measured && inc, lane));
+      __syncwarp();
+      if (active && li == 0) {
+        R.cnt_meas = before + __popc(mm);
+        R.cnt_incl += ninc;
+        if (cmk) R.stopped = 1;
+      }
+    }
+    if (measured && inc) {
       my_slo += (l <= p.slo_us);
       my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
       my_sum += l;
     }
-    if (member) p.lat[rowoff + i] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
+    if (member) p.lat[rowoff + i] = !inc ? 0xFFFFFFFFu : (l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l);
 
     // work counters, lane-local
     ct.steps += Sk;
@@ -510,6 +535,13 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
       t_idle = tend;
       h += b;
     }
+    if constexpr (STOP) {                           // stopped: the rest of the segment is never simulated
+      __syncwarp();
+      if (active && R.stopped) {
+        for (uint32_t j = h + (uint32_t)li; j < N; j += G) p.lat[rowoff + j] = 0xFFFFFFFFu;
+        h = N;
+      }
+    }
 
     // ---- groups that finished their replica: outputs (p99 and goodput follow in K1b)
     const bool fin = active && h >= N;
@@ -520,10 +552,11 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
       // the window ends at the last MEASURED completion (§2.8): all earlier batches ended before this one
       // formed, so it is the largest c among this last batch's measured members (not t_idle, which may be
       // a warmup member's completion when the segment is shorter than the batch)
-      const uint64_t cm = gmax64<G>(measured ? c : 0ull);
+      const uint64_t cm = gmax64<G>(measured && inc ? c : 0ull);
       if (fin && li == 0) {
         const uint64_t Tw = cm - R.a_w;
-        p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
+        const uint32_t fl = (sat ? 2u : 0u) | (STOP && !R.stopped ? 4u : 0u);
+        p.part[r] = slo_replica_result{0, slo_met, STOP ? R.cnt_incl : p.seg, fl, Tw < 1 ? 1 : Tw, sum};
         if (p.stats) {
           unsigned long long* st = (unsigned long long*)p.stats;
           atomicAdd(st + 0, (unsigned long long)N);
@@ -571,9 +604,10 @@ struct alignas(16) CGroup {
   uint64_t pstart, pD, pU, pLam, nphase, a_w, alpha0, alpha1;
   uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, gp;
   uint32_t k0, k1, wl, pad;
+  uint32_t cnt_meas, stopped, pad3[2];          // stop rule (§2.14): measured completions so far, stopped
 };
 
-template <int G>
+template <int G, bool STOP>
 __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   using CG = CGroup<G>;
   constexpr int RING = CG::RING, KRING = CG::KRING;
@@ -796,6 +830,24 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           nrun -= nf;
           if (s_next == INF64 && nq < N) need_s = true;  // completions may have opened the gate for nq
         }
+        if constexpr (STOP) {                            // stop rule (§2.14): completions at t continue the count
+          const uint32_t nfm = __popc(gballot<G>(fin && mi >= p.warmup, lane));
+          const uint32_t before = dec ? R.cnt_meas : 0u;
+          const uint64_t t0 = closed ? a_w : R.a_w;
+          const uint32_t need = p.stop_n ? p.stop_n : 1u;
+          const bool stop_now = dec && !R.stopped && nfm > 0 && before + nfm >= need && t >= t0 + p.stop_t;
+          __syncwarp();
+          if (dec && li == 0) {
+            R.cnt_meas = before + nfm;
+            if (stop_now) R.stopped = 1;
+          }
+          if (stop_now) {                                // t* = t: whatever has not completed never counts
+            if (run) p.lat[rowoff + mi] = 0xFFFFFFFFu;
+            for (uint32_t j = nq + (uint32_t)li; j < N; j += G) p.lat[rowoff + j] = 0xFFFFFFFFu;
+            run = false;
+            ndone = N;
+          }
+        }
       }
     }
 
@@ -808,7 +860,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       const bool sat = gballot<G>((my_slo >> 31) != 0, lane) != 0;
       if (done && li == 0) {
         const uint64_t Tw = cm - (closed ? a_w : R.a_w);
-        p.part[r] = slo_replica_result{0, slo_met, p.seg, sat ? 2u : 0u, Tw < 1 ? 1 : Tw, sum};
+        const uint32_t fl = (sat ? 2u : 0u) | (STOP && !R.stopped ? 4u : 0u);
+        p.part[r] = slo_replica_result{0, slo_met, STOP ? R.cnt_meas : p.seg, fl, Tw < 1 ? 1 : Tw, sum};
         ct.batches += npre;
         ct.dsteps += it;
         ct.blocks += noise ? it : 0u;
@@ -828,14 +881,15 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
 #ifndef SLO_MAXNREG
 #define SLO_MAXNREG 80
 #endif
-__global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
+template <bool STOP>
+__global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel_t(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
-  run_mode<8>(p, 0, wsmem, lane, ct);
-  run_mode<16>(p, 1, wsmem, lane, ct);
-  run_mode<32>(p, 2, wsmem, lane, ct);
+  run_mode<8, STOP>(p, 0, wsmem, lane, ct);
+  run_mode<16, STOP>(p, 1, wsmem, lane, ct);
+  run_mode<32, STOP>(p, 2, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -853,14 +907,15 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel(const SimParams p) {
 #ifndef SLO_CONT_MAXNREG
 #define SLO_CONT_MAXNREG 96
 #endif
-__global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel(const SimParams p) {
+template <bool STOP>
+__global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
-  run_cont<8>(p, 3, wsmem, lane, ct);
-  run_cont<16>(p, 4, wsmem, lane, ct);
-  run_cont<32>(p, 5, wsmem, lane, ct);
+  run_cont<8, STOP>(p, 3, wsmem, lane, ct);
+  run_cont<16, STOP>(p, 4, wsmem, lane, ct);
+  run_cont<32, STOP>(p, 5, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -873,6 +928,13 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel(const SimParam
     }
   }
 }
+
+// K1 / K1c and their stop-rule variants: separate instantiations, so the default path
+// carries none of the stop rule's code
+template __global__ void slo_sim_kernel_t<false>(const SimParams p);
+template __global__ void slo_sim_kernel_t<true>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<true>(const SimParams p);
 
 size_t cont_warp_bytes() {
   size_t m = 4 * sizeof(CGroup<8>);
@@ -960,8 +1022,7 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint
   uint32_t* vals = sv + 256;
   __shared__ uint32_t s_digit, s_kk;
   const uint32_t N = p.warmup + p.seg;
-  const uint32_t n = p.seg;
-  const uint32_t rank = (uint32_t)((99ull * n + 99ull) / 100ull);
+  const uint32_t n = p.seg;                        // row length (stop rule: uncounted entries hold UINT32_MAX)
 
   for (uint32_t t = blockIdx.x; t < p.n_chunk; t += gridDim.x) {
     const uint32_t r = p.r_base + t;
@@ -984,7 +1045,10 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint
     uint32_t res[3];
     const uint32_t nq = (p.p50 || p.p95) ? 3u : 1u;
     for (uint32_t qi = 0; qi < nq; ++qi) {          // p99, then p50 and p95 (nearest rank, ceil(q n))
-    const uint32_t rq = qi == 0 ? rank : (uint32_t)(((qi == 1 ? 50ull : 95ull) * n + 99ull) / 100ull);
+    // nearest rank among the nm counted latencies; the n - nm uncounted ones are UINT32_MAX (the top), so the
+    // rq-th smallest counted value is the (n - rq + 1)-th largest of the row
+    const uint32_t nm = pr.n_measured;
+    const uint32_t rq = (uint32_t)(((qi == 0 ? 99ull : qi == 1 ? 50ull : 95ull) * nm + 99ull) / 100ull);
     uint32_t prefix = 0, kk = n - rq + 1;
     for (int shift = 24; shift >= 0; shift -= 8) {
       hist[threadIdx.x] = 0;

@@ -583,3 +583,41 @@ def test_pareto_front_properties_at_scale(S):
     sub = s.pareto_front(agg[:600].contiguous()).cpu().numpy().astype(bool).tolist()
     assert sub == pareto.pareto_front(rows)
     s.close()
+
+
+@pytest.mark.parametrize("cont", [0, 1], ids=["static", "continuous"])
+def test_stop_rule_matches_oracle(S, orc, cont):
+    """NEXT-3 segment stop rule: with (n_min, t_min) the device stops each
+    replica at t* — the first measured completion that is at least the n_min-th and t_min after t0 — and
+    counts only requests completed by then; every stored latency (sentinels included), p50/p95/p99,
+    n_measured, slo_met, window, sum, flags (bit 2: rule not met) and goodput equal the oracle's."""
+    rng = random.Random(70 + cont)
+    wls = _wls_cont() if cont else _wls()
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(16)]
+    ks[0] = inputs.knobs(conc=8, max_num_seqs=8, draft_len=4, spec_on=1, workload=5)       # closed loop
+    seeds = inputs.seeds(2, 900 + cont)
+    N, warm = 700, 30
+    s = S.Simulator(wls, device=0)
+    for n_min, t_min in ((50, 0), (1, 3_000_000), (300, 20_000_000), (700, 0), (10, 10**9)):
+        out = s.run_batch(S.knobs_tensor(ks), S.seeds_tensor(seeds), N, warmup_len=warm, latencies=True,
+                          percentiles=True, stop_n_min=n_min, stop_t_min_us=t_min)
+        torch.cuda.synchronize()
+        from paper_2603_11340_b200._lib import RESULT_DTYPE
+        lat = out["latencies"].cpu().numpy().view(np.uint32).reshape(-1, N + warm)
+        det = S.unpack(out["detail"], RESULT_DTYPE)
+        p99 = out["p99_us"].cpu().numpy().view(np.uint32)
+        p50 = out["p50_us"].cpu().numpy().view(np.uint32)
+        p95 = out["p95_us"].cpu().numpy().view(np.uint32)
+        gp = out["goodput"].cpu().numpy()
+        for ci, k in enumerate(ks):
+            for si, sd in enumerate(seeds):
+                r = ci * len(seeds) + si
+                ref = orc.run(wls, k, sd, N, warmup_len=warm, latencies=True, stop_n_min=n_min,
+                              stop_t_min_us=t_min)
+                tag = f"stop {(n_min, t_min)} replica {r} knobs {k}"
+                assert np.array_equal(lat[r], ref["latencies"]), tag
+                assert (int(p99[r]), int(p50[r]), int(p95[r])) == (ref["p99_us"], ref["p50_us"], ref["p95_us"]), tag
+                for f in ("slo_met", "n_measured", "window_us", "sum_latency_us", "flags"):
+                    assert int(det[r][f]) == ref[f], (tag, f)
+                assert gp[r] == ref["goodput"], tag
+    s.close()
