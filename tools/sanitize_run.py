@@ -22,6 +22,10 @@ for pol in (1, 2):   # narrow (G >= min(C, B)) and wide (G >= max(C, B)) lane gr
 s = sim.Simulator(wls, device=0)
 out = s.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(inputs.seeds(3)), 150, warmup_len=10, latencies=True,
                   stats=True)
+s.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(inputs.seeds(3)), 150, warmup_len=10, latencies=True,
+            percentiles=True, stop_n_min=40, stop_t_min_us=500_000)                # stop-rule kernels (§2.14)
+agg0 = s.aggregate(out["detail"], len(ks), 3)
+s.pareto_front(agg0, count=True)                                                    # K5
 agg = s.aggregate(out["detail"], len(ks), 3)
 red = s.aggregate_reduce(torch.cat([agg, agg]), 2, len(ks))
 cfg = inputs.config_c4(n_seeds=2, segment_len=100)
