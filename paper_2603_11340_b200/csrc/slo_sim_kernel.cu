@@ -627,7 +627,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
   // slot state (lane = one slot of the running set)
   bool run = false;
   // sleft: decode iterations the slot's request still runs; stot: its S (counters); fw: noise window
-  uint32_t mi = 0, sleft = 0, stot = 0, fw = 0, nzc = 0, my_slo = 0;
+  uint32_t mi = 0, sleft = 0, stot = 0, fw = 0, fw2 = 0, nzc = 0, my_slo = 0;
   uint64_t origin = 0, my_sum = 0, my_cmax = 0;
 
   for (;;) {
@@ -671,7 +671,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             s_next = INF64;
             a_w = 0;
             nq = ndone = gen = it = nrun = npre = 0;
-            nzc = G;                                     // noise window empty: filled at the first decode
+            nzc = 2 * G;                                 // noise window empty: filled at the first decode
             run = false;
             my_slo = 0;
             my_sum = 0;
@@ -766,39 +766,56 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
     // ---- decode iterations over the running set, fast-forwarded to the next event.  While no member
     // finishes and no prefill can start, consecutive decode iterations change nothing but t, the members'
     // token counts and the random-word cursors, so a group advances K of them at once: lane k holds the
-    // duration of iteration it + k (D_k = floor(f_k d(n) / 10^6), d(n) = alpha0 + alpha1 n), a group scan
-    // gives their end times, and
+    // durations of iterations it + 2k and it + 2k + 1 (D = floor(f d(n) / 10^6), d(n) = alpha0 + alpha1 n),
+    // a group scan gives their end times (up to 2G iterations per pass), and
     //   K = min(first iteration at whose end a member finishes,
     //           first iteration at whose end a prefill can start (|R| < B and s_next <= end),
     //           the iterations whose random words are buffered).
     if (__any_sync(FULL, dec)) {
       const bool nz = dec && noise != 0;
-      if (__any_sync(FULL, nz && nzc > (uint32_t)(G / 2))) {   // pooled shift-refill of the noise windows
-        const uint32_t src = (uint32_t)li + nzc;
-        const uint32_t sh = __shfl_sync(FULL, fw, (int)(src & (G - 1)), G);
+      // noise window of 2G decode iterations: lane li holds positions li (fw) and G + li (fw2) after nzc used
+      if (__any_sync(FULL, nz && nzc > (uint32_t)G)) {       // pooled shift-refill once half of it is used
+        const uint32_t sA = (uint32_t)li + nzc, sB = (uint32_t)(G + li) + nzc;   // old positions of the new ones
+        const uint32_t a0 = __shfl_sync(FULL, fw, (int)(sA & (G - 1)), G);
+        const uint32_t b0 = __shfl_sync(FULL, fw2, (int)(sA & (G - 1)), G);
+        const uint32_t b1 = __shfl_sync(FULL, fw2, (int)(sB & (G - 1)), G);
         if (nz && nzc > 0) {
-          if (src < (uint32_t)G) {
-            fw = sh;
+          if (sA < (uint32_t)(2 * G)) {
+            fw = sA < (uint32_t)G ? a0 : b0;
           } else {                                       // ITER block it + li, word 0 (§2.12)
             const uint32_t w = philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x;
             const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
             fw = (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
           }
+          if (sB < (uint32_t)(2 * G)) {
+            fw2 = b1;
+          } else {                                       // ITER block it + G + li
+            const uint32_t w = philox(it + (uint32_t)(G + li), 3, 0, 0, k0, k1).x;
+            const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
+            fw2 = (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+          }
           nzc = 0;
         }
       }
-      // end times of the next iterations: lane k <-> iteration it + k
+      // end times of the next 2G iterations: lane k <-> iterations it + 2k and it + 2k + 1
       const uint32_t d = alpha0 + alpha1 * nrun;          // < 2^31 (timing values < 2^20, gamma <= 16)
-      const uint32_t fk = __shfl_sync(FULL, fw, (int)(((uint32_t)li + nzc) & (G - 1)), G);
-      const uint32_t Dk = nz ? (uint32_t)(((uint64_t)fk * d) / 1000000u) : d;
-      const uint64_t cum = gscan64<G>((uint64_t)Dk, li);
+      const uint32_t p0 = nzc + 2u * (uint32_t)li, p1 = p0 + 1u;
+      const uint32_t x0 = __shfl_sync(FULL, fw, (int)(p0 & (G - 1)), G), y0 = __shfl_sync(FULL, fw2, (int)(p0 & (G - 1)), G);
+      const uint32_t x1 = __shfl_sync(FULL, fw, (int)(p1 & (G - 1)), G), y1 = __shfl_sync(FULL, fw2, (int)(p1 & (G - 1)), G);
+      const uint32_t f0 = p0 < (uint32_t)G ? x0 : y0, f1 = p1 < (uint32_t)G ? x1 : y1;
+      const uint32_t D0 = nz ? (uint32_t)(((uint64_t)f0 * d) / 1000000u) : d;
+      const uint32_t D1 = nz ? (uint32_t)(((uint64_t)f1 * d) / 1000000u) : d;
+      const uint64_t end1 = gscan64<G>((uint64_t)D0 + D1, li);   // end of iteration 2k + 1
+      const uint64_t end0 = end1 - D1;                            // end of iteration 2k
       // K = min(first completion, first iteration end at which a prefill can start, the noise window)
       uint32_t K = gmin<G>(dec && run ? sleft : 0xFFFFu);
-      K = min(K, nz ? (uint32_t)G - nzc : (uint32_t)G);
-      const bool open = dec && nrun < B && (uint32_t)li < K && t + cum >= s_next;   // s_next = INF: never
-      const uint32_t om = gballot<G>(open, lane);
-      if (om) K = (uint32_t)__ffs(om);                    // the first such iteration end (lanes < K only)
-      const uint64_t tK = gshfl64<G>(cum, (int)((K - 1u) & (G - 1)));
+      K = min(K, nz ? (uint32_t)(2 * G) - nzc : (uint32_t)(2 * G));
+      const bool canpre = dec && nrun < B;                          // s_next = INF: never
+      const uint32_t m0 = gballot<G>(canpre && 2u * (uint32_t)li < K && t + end0 >= s_next, lane);
+      const uint32_t m1 = gballot<G>(canpre && 2u * (uint32_t)li + 1u < K && t + end1 >= s_next, lane);
+      const uint32_t i0 = m0 ? 2u * (uint32_t)(__ffs(m0) - 1) : 0xFFFFu, i1 = m1 ? 2u * (uint32_t)(__ffs(m1) - 1) + 1u : 0xFFFFu;
+      if (m0 | m1) K = min(i0, i1) + 1u;                  // the first such iteration end
+      const uint64_t tK = gshfl64<G>(((K - 1u) & 1u) ? end1 : end0, (int)(((K - 1u) >> 1) & (G - 1)));
       bool fin = false;
       if (dec) {
         t += tK;
