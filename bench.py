@@ -444,6 +444,25 @@ def main():
                 traffic = json.load(fh).get(args.workload)
         except Exception:
             pass
+        # BASELINE's "% SM issue / HBM peak": issue-slot utilisation of the dominant kernel from its committed
+        # ncu summary, and the HBM share of this run (ncu bytes per step over the live kernel time)
+        issue_util = None
+        try:
+            import glob
+            pat = "r01_k1c_v*_c2c_ncu.json" if args.workload == "c2c" else "r01_k1_v*_c2_ncu.json"
+            fs = sorted(glob.glob(os.path.join(ROOT, "profiles", pat)),
+                        key=lambda f: int(f.rsplit("_v", 1)[1].split("_")[0]))
+            if fs:
+                with open(fs[-1]) as fh:
+                    m = json.load(fh)["metrics"]
+                issue_util = {"pct_of_peak": float(m["sm__inst_issued.avg.pct_of_peak_sustained_active"][0]),
+                              "source": os.path.relpath(fs[-1], ROOT)}
+        except Exception:
+            issue_util = None
+        hbm = None
+        if traffic:
+            gbs = traffic / (t_k1 / args.steps) / 1e9
+            hbm = {"gb_per_s": gbs, "peak_gb_per_s": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
         line = {
             "metric": "simulated requests/s", "value": value, "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps,
@@ -464,6 +483,7 @@ def main():
                                       "decode_steps": int(stats["decode_steps"])},
             "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
                          "frac": achieved_gops / peak_gops, "traffic": traffic,
+                         "issue_util_ncu": issue_util, "hbm": hbm,
                          "kernel": ("slo_sim_run_batch = K0 classify + K1c continuous-batching simulate + K1b p99 "
                                     "select (K1c dominates)" if args.workload == "c2c" else
                                     "slo_sim_run_batch = K0 classify + K1 simulate + K1b p99 select (K1 dominates, "
