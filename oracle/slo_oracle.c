@@ -168,7 +168,8 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
                    scaled_gap(W->arr.mean_gap_q16[1], k->rate_scale_q8)};
   uint32_t kind = W->arr.kind;
   /* per-state rate rho_s = floor((2^64 - 1) / g_s), 0 for a state without arrivals */
-  uint64_t rho[2] = {g[0] == U64MAX ? 0 : U64MAX / g[0], g[1] == U64MAX ? 0 : U64MAX / g[1]};
+  uint64_t rho[2] = {g[0] == U64MAX || g[0] == 0 ? 0 : U64MAX / g[0], g[1] == U64MAX || g[1] == 0 ? 0 : U64MAX / g[1]};
+  /* (g = 0 only for kind 4, a zero mean think time; rho is used by kinds 1 and 2) */
 
   /* bursty phase state (kinds 1, 2) */
   uint32_t p = 0;
@@ -190,7 +191,8 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
     uint32_t w[4];
     block(k0, k1, i, 0, 0, w);
     uint64_t E = orc_exp_q32(w[0]);
-    if (kind == 3) {           /* closed loop, zero think time: every request is waiting from t = 0 */
+    if (kind >= 3) {           /* closed loop (3: zero think time, 4: exponential think time):
+                                  a_i = 0; kind 4's issue instants come from the think draws in simulate() */
       a[i] = 0;
     } else if (kind == 0) {
       uint64_t gap = (uint64_t)(((u128)E * g[0]) >> 48);
@@ -253,6 +255,21 @@ static uint64_t step_cost(const orc_timing* tm, uint32_t gamma, uint64_t n) {
   return (uint64_t)gamma * ((uint64_t)tm->dr_base_us + (uint64_t)tm->dr_seq_us * n) +
          (uint64_t)tm->ver_base_us + (uint64_t)tm->ver_seq_us * n +
          (uint64_t)tm->ver_tok_us * (uint64_t)(gamma + 1) * n;
+}
+
+/* DESIGN.md §2.11 kind 4 — closed loop with exponential think time: the k-th completion (k = 0, 1, ...)
+ * starts user chain q = k + C (if q < N), which becomes ready at c + Z_k, Z_k = floor(E_q(w0) * g / 2^48)
+ * with w0 from the THINK block (k, 4, 0) and g the scaled mean think time (Q48.16 us). */
+typedef struct {
+  int on;
+  uint32_t k0, k1;
+  uint64_t g;
+} thinkdraw;
+
+static uint64_t think_time(const thinkdraw* th, uint32_t k) {
+  uint32_t w[4];
+  block(th->k0, th->k1, k, 4, 0, w);
+  return (uint64_t)(((u128)orc_exp_q32(w[0]) * th->g) >> 48);
 }
 
 static int cmp_u64(const void* x, const void* y) {
@@ -326,8 +343,8 @@ static void outputs(uint32_t N, uint32_t warmup, uint32_t slo_us, const uint64_t
 
 static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t mw, uint32_t issue_origin,
                     uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
-                    const uint32_t* f, adraw* ad, uint32_t warmup, uint32_t slo_us, const orc_stop* stop,
-                    orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
+                    const uint32_t* f, adraw* ad, const thinkdraw* th, uint32_t warmup, uint32_t slo_us,
+                    const orc_stop* stop, orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
   uint64_t* s = (uint64_t*)calloc(N, sizeof(uint64_t));
   uint64_t* form = (uint64_t*)calloc(N, sizeof(uint64_t));
   uint64_t* c = (uint64_t*)calloc(N, sizeof(uint64_t));
@@ -336,16 +353,29 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
   uint32_t* pend = (uint32_t*)calloc(B, sizeof(uint32_t));
   uint32_t* rem = (uint32_t*)calloc(B, sizeof(uint32_t));
   uint32_t* lat = (uint32_t*)calloc(N, sizeof(uint32_t));
-  if (!s || !form || !c || !steps || !batch_of || !pend || !rem || !lat) abort();
+  /* kind 4: ordinal of each request's completion, and the ready user chains (ready time, chain id) */
+  uint32_t* kord = (uint32_t*)calloc(N, sizeof(uint32_t));
+  uint64_t* rdy_t = (uint64_t*)calloc(C, sizeof(uint64_t));
+  uint32_t* rdy_q = (uint32_t*)calloc(C, sizeof(uint32_t));
+  uint32_t* order = (uint32_t*)calloc(B, sizeof(uint32_t));
+  if (!s || !form || !c || !steps || !batch_of || !pend || !rem || !lat || !kord || !rdy_t || !rdy_q || !order) abort();
 
-  uint32_t na = 0, ni = 0, nb = 0, inflight = 0, ndone = 0, npend = 0, nbatches = 0;
+  uint32_t na = 0, ni = 0, nb = 0, inflight = 0, ndone = 0, npend = 0, nbatches = 0, nrdy = 0, nord = 0;
   int busy = 0;
-  uint64_t decode_steps = 0, member_steps = 0, spec_blocks = 0;
+  uint64_t decode_steps = 0, member_steps = 0, spec_blocks = 0, think_blocks = 0;
+  if (th->on) /* the first C chains are ready at t = 0 */
+    for (uint32_t q = 0; q < C && q < N; ++q) {
+      rdy_t[nrdy] = 0;
+      rdy_q[nrdy++] = q;
+    }
 
   while (ndone < N) {
-    /* next event instant: an arrival, a completion, or a max_wait deadline of an idle server */
+    /* next event instant: an arrival (kind 4: a chain's think ends), a completion, or a max_wait deadline of
+     * an idle server */
     uint64_t t = U64MAX;
-    if (na < N && a[na] < t) t = a[na];
+    if (!th->on && na < N && a[na] < t) t = a[na];
+    for (uint32_t q = 0; q < nrdy; ++q)
+      if (rdy_t[q] < t) t = rdy_t[q];
     for (uint32_t q = 0; q < npend; ++q)
       if (c[pend[q]] < t) t = c[pend[q]];
     if (!busy && nb < ni && mw > 0 && s[nb] + mw < t) t = s[nb] + mw;
@@ -356,6 +386,11 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
       if (c[pend[q]] == t) {
         --inflight;
         ++ndone;
+        if (th->on && kord[pend[q]] + C < N) { /* kind 4: the user thinks, then chain k + C is ready */
+          rdy_t[nrdy] = t + think_time(th, kord[pend[q]]);
+          rdy_q[nrdy++] = kord[pend[q]] + C;
+          ++think_blocks;
+        }
         pend[q] = pend[npend - 1];
         --npend;
       } else {
@@ -363,8 +398,22 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
       }
     }
     if (busy && npend == 0) busy = 0;
-    /* (2) arrivals at t, in index order */
-    while (na < N && a[na] == t) ++na;
+    /* (2) arrivals at t, in index order (kind 4: the chains ready at t, in chain order, arrive and issue at
+     * once; request index = issue order) */
+    if (th->on) {
+      for (;;) {
+        uint32_t best = U32MAX;
+        for (uint32_t q = 0; q < nrdy; ++q)
+          if (rdy_t[q] == t && (best == U32MAX || rdy_q[q] < rdy_q[best])) best = q;
+        if (best == U32MAX) break;
+        rdy_t[best] = rdy_t[nrdy - 1];
+        rdy_q[best] = rdy_q[nrdy - 1];
+        --nrdy;
+        ++na;
+      }
+    } else {
+      while (na < N && a[na] == t) ++na;
+    }
     /* (3) issues at t, in index order, while fewer than C are in flight */
     while (ni < na && inflight < C) {
       s[ni] = t;
@@ -408,6 +457,15 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
           ++j;
         }
         decode_steps += j;
+        /* completion ordinals (kind 4 think draws): in time order, i.e. by step count, then request index */
+        for (uint32_t m = 0; m < b; ++m) order[m] = h + m;
+        for (uint32_t x = 1; x < b; ++x)
+          for (uint32_t y = x; y > 0 && steps[order[y]] < steps[order[y - 1]]; --y) {
+            uint32_t tmp = order[y];
+            order[y] = order[y - 1];
+            order[y - 1] = tmp;
+          }
+        for (uint32_t m = 0; m < b; ++m) kord[order[m]] = nord++;
         for (uint32_t m = h; m < h + b; ++m) {
           form[m] = t;
           batch_of[m] = nbatches;
@@ -442,9 +500,10 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
     cnt->batches = nbatches;
     cnt->decode_steps = decode_steps;
     cnt->member_steps = member_steps;
-    cnt->philox_blocks = spec_blocks; /* caller adds REQ and PHASE blocks */
+    cnt->philox_blocks = spec_blocks + think_blocks; /* caller adds REQ and PHASE blocks */
   }
   free(s); free(form); free(c); free(steps); free(batch_of); free(pend); free(rem); free(lat);
+  free(kord); free(rdy_t); free(rdy_q); free(order);
   return ad->bad ? -2 : 0;
 }
 
@@ -632,12 +691,23 @@ int orc_run_stop(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint
   uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
   adraw ad = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, T, NULL, NULL, 0};
   int rc;
+  const int closed = W->arr.kind == 3 || W->arr.kind == 4;
+  const thinkdraw th = {W->arr.kind == 4, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey,
+                        scaled_gap(W->arr.mean_gap_q16[0], k->rate_scale_q8)};
+  if (th.on && W->arr.mean_gap_q16[0] == U64MAX) { /* kind 4 needs a finite mean think time */
+    free(a); free(P); free(O); free(w3); free(f);
+    return -1;
+  }
   if (W->batching == 1) {
+    if (th.on) { /* kind 4 is defined for static batching only */
+      free(a); free(P); free(O); free(w3); free(f);
+      return -1;
+    }
     itnoise nz = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, W->timing.noise_step_ppm};
-    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, W->arr.kind == 3, N, a, P, O, f, &ad, &nz,
+    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, closed, N, a, P, O, f, &ad, &nz,
                        warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   } else {
-    rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, W->arr.kind == 3, N, a, P, O, f, &ad,
+    rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, closed, N, a, P, O, f, &ad, &th,
                   warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   }
   if (cnt) cnt->philox_blocks += N + (W->arr.kind == 1 ? (uint64_t)phases : 0);
@@ -671,11 +741,12 @@ int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seq
     if (O[i] < 1) return -1;
   if (cnt) memset(cnt, 0, sizeof(*cnt));
   adraw ad = {0, 0, 0, NULL, A_off, A_val, 0};
+  const thinkdraw th = {0, 0, 0, 0};
   if (continuous) {
     itnoise nz = {0, 0, 0, 0};
     return simulate_cont(tm, conc, max_num_seqs, gamma_eff, issue_origin, n, a, P, O, f, &ad, &nz, warmup_len,
                          slo_us, &stop, res, latencies, trace, cnt);
   }
-  return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, warmup_len,
+  return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, &th, warmup_len,
                   slo_us, &stop, res, latencies, trace, cnt);
 }
