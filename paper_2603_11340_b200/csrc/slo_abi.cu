@@ -27,10 +27,11 @@ struct slo_sim {
   uint32_t n_wl = 0;
   uint32_t crn = 1;
   bool any_cont = false;            // a workload uses continuous batching: launch K1c
+  bool any_think = false;           // a workload is a closed loop with think time: launch K1t
   uint32_t group_policy = 0;        // slo_sim_opts.group_policy
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
-  uint32_t* d_ctl = nullptr;        // [136]: list lengths [4], K1 cursors [4], K0 bucket counts/cursors [128]
+  uint32_t* d_ctl = nullptr;        // [slo::kCtlWords]: list lengths, K1 cursors, K0 bucket counts/cursors
   // run scratch (grow-only): work lists, latency rows, per-replica partial results
   uint32_t* d_lists = nullptr;
   size_t lists_cap = 0;
@@ -156,7 +157,11 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   for (uint32_t w = 0; w < n_wl; ++w) {
     const slo_workload& x = wl[w];
     const uint64_t NOA = ~0ull;
-    if (x.arr.kind > 3 || x.arr.start_state > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: bad arrival kind", w);
+    if (x.arr.kind > 4 || x.arr.start_state > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: bad arrival kind", w);
+    if (x.arr.kind == 4 && x.arr.mean_gap_q16[0] == NOA)
+      return fail(nullptr, SLO_E_INVAL, "workload %u: think time needs a finite mean (mean_gap_q16[0])", w);
+    if (x.arr.kind == 4 && x.batching == 1)
+      return fail(nullptr, SLO_E_UNSUPPORTED, "workload %u: think time (kind 4) with continuous batching", w);
     for (int s = 0; s < 2; ++s)
       if (x.arr.mean_gap_q16[s] != NOA && x.arr.mean_gap_q16[s] > (1ull << 48))
         return fail(nullptr, SLO_E_INVAL, "workload %u: mean_gap_q16 > 2^48", w);
@@ -218,6 +223,7 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   h->sm_count = prop.multiProcessorCount;
   h->n_wl = n_wl;
   for (uint32_t w = 0; w < n_wl; ++w) h->any_cont |= wl[w].batching == 1;
+  for (uint32_t w = 0; w < n_wl; ++w) h->any_think |= wl[w].arr.kind == 4;
   h->crn = o.crn;
   if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
@@ -335,6 +341,12 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   {
     CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (h->any_think) {
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_think_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_think_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    }
   }
   const int bps = blocks_per_sm_for(h, smem);
   int cont_bps = 1;
@@ -390,6 +402,13 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     else
       slo::slo_sim_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
     CUDA_TRY(h, cudaGetLastError());
+    if (h->any_think) {  // K1t: closed loops with think time (same group layout and grid as K1)
+      if (p.stop_n | p.stop_t)
+        slo::slo_sim_think_kernel_t<true><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+      else
+        slo::slo_sim_think_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+      CUDA_TRY(h, cudaGetLastError());
+    }
     if (h->any_cont) {   // K1c: the continuous-batching list, one replica per warp
       uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;
       const uint64_t cneed = ((uint64_t)nc + h->warps_per_block - 1) / h->warps_per_block;

@@ -9,10 +9,11 @@ namespace slo {
 constexpr int kMaxWarpsPerBlock = 8;
 constexpr int kDefaultWarpsPerBlock = 4;
 // K0 work lists: static batching by lane-group size G = 8, 16, 32 (>= min(C, B) narrow, >= max(C, B) wide, or
-// 32 for a lone replica; K1), then continuous batching by G = 8, 16, 32 >= min(C, B) (wide: >= B) (K1c)
-constexpr int kLists = 6;
+// 32 for a lone replica; K1), then continuous batching by G = 8, 16, 32 >= min(C, B) (wide: >= B) (K1c), then
+// closed loops with think time (kind 4) by G = 8, 16, 32 >= max(C, B) (K1t)
+constexpr int kLists = 9;
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
-constexpr int kCtlBucket = 16, kCtlWords = kCtlBucket + 2 * 16 * kLists;
+constexpr int kCtlBucket = 32, kCtlWords = kCtlBucket + 2 * 16 * kLists;
 
 struct DevWorkload {      // device copy of one slo_workload
   uint32_t kind, start_state;
@@ -49,6 +50,7 @@ struct SimParams {
 
 template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
 template <bool STOP> __global__ void slo_sim_cont_kernel_t(const SimParams p);  // K1c: continuous batching (§2.12)
+template <bool STOP> __global__ void slo_sim_think_kernel_t(const SimParams p); // K1t: think-time closed loop (§2.11)
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
                                           uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t wide,
                                           uint32_t* ctl);

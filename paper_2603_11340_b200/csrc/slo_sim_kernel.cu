@@ -155,8 +155,8 @@ __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const
     const uint64_t g1 = W.gap_q16[1] == INF64 ? INF64 : (W.gap_q16[1] << 8) / k.rate_scale_q8;
     R.g[0] = g0;
     R.g[1] = g1;
-    R.rho[0] = g0 == INF64 ? 0 : INF64 / g0;
-    R.rho[1] = g1 == INF64 ? 0 : INF64 / g1;
+    R.rho[0] = g0 == INF64 || g0 == 0 ? 0 : INF64 / g0;   // (g0 = 0: a zero mean think time, kind 4)
+    R.rho[1] = g1 == INF64 || g1 == 0 ? 0 : INF64 / g1;
     R.last = 0;
     R.nphase = 0;
     R.kind = W.kind;
@@ -218,8 +218,8 @@ __device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ 
   const u32x4 w = philox(i, 0, 0, 0, k0, k1);
   const uint64_t E = valid ? exp_q32(w.x) : 0;
   const uint32_t kind = go ? R.kind : 0u;
-  // kind 0: gaps; kinds 1, 2: operational-time increments; kind 3 (closed loop): every a_i = 0
-  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : (kind == 3 ? 0ull : E);
+  // kind 0: gaps; kinds 1, 2: operational-time increments; kinds 3, 4 (closed loop): every a_i = 0
+  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : (kind >= 3 ? 0ull : E);
   const uint64_t last = go ? R.last : 0ull;
   const uint64_t sc = last + gscan64<G>(x, li);     // kind 0: a_i; kinds 1, 2: tau_i; kind 3: 0
   const uint64_t newlast = gshfl64<G>(sc, G - 1);
@@ -333,6 +333,27 @@ __device__ __forceinline__ uint32_t gscan_n(uint32_t v, int li) {
   return v;
 }
 
+// bitonic sort of (t, q) pairs over each G-lane group, ascending by t then q (kind 4's pending issues)
+template <int G>
+__device__ __forceinline__ void gsort_pair(uint64_t& t, uint32_t& q, int li) {
+#pragma unroll
+  for (int kk = 2; kk <= G; kk <<= 1) {
+#pragma unroll
+    for (int jj = kk >> 1; jj >= 1; jj >>= 1) {
+      const uint32_t olo = __shfl_xor_sync(FULL, (uint32_t)t, jj, G);
+      const uint32_t ohi = __shfl_xor_sync(FULL, (uint32_t)(t >> 32), jj, G);
+      const uint32_t oq = __shfl_xor_sync(FULL, q, jj, G);
+      const uint64_t ot = ((uint64_t)ohi << 32) | olo;
+      const bool other_less = ot < t || (ot == t && oq < q);
+      const bool keep_min = ((li & kk) == 0) == ((li & jj) == 0);
+      if (keep_min ? other_less : !other_less) {   // equal pairs are identical: either choice is the same
+        t = ot;
+        q = oq;
+      }
+    }
+  }
+}
+
 struct Counters {   // lane-local work counters (flushed to slo_stats)
   uint32_t steps, blocks, batches, dsteps;
 };
@@ -351,7 +372,9 @@ __device__ __forceinline__ void flush_counters(const SimParams& p, Counters& ct)
 // ------------------------------------------------------------------------------------------------
 // one lane-group mode of K1: groups pull replicas from work list `cls` until it is exhausted
 // ------------------------------------------------------------------------------------------------
-template <int G, bool STOP>
+// THINK (kind 4): issue instants come from the group's C pending user chains, kept sorted in
+// the lanes (lane l = the l-th earliest ready instant, with its chain id) instead of s_j = max(a_j, kappa_{j-C})
+template <int G, bool STOP, bool THINK>
 __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   constexpr int RING = Group<G>::RING;
   const int g = lane / G, li = lane % G;
@@ -366,6 +389,8 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   uint32_t my_slo = 0;
   uint64_t my_sum = 0;
   bool active = false, exhausted = false;
+  uint64_t pq = INF64;        // THINK: this lane's pending ready instant
+  uint32_t pid = 0xFFFFFFFFu; // THINK: its user chain id
 
   for (;;) {
     __syncwarp();   // every lane is past the previous iteration's reads of its group's record
@@ -406,6 +431,10 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
             t_idle = 0;
             my_slo = 0;
             my_sum = 0;
+            if constexpr (THINK) {                 // the first C chains are ready at t = 0
+              pq = ((uint32_t)li < k.conc && (uint32_t)li < N) ? 0ull : INF64;
+              pid = (uint32_t)li;
+            }
             active = true;
           }
         }
@@ -429,7 +458,9 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const uint32_t C = kn.x, B = kn.y, mw = kn.z;
     const uint32_t j = h + li;
     uint64_t sj = INF64;
-    if (active && (uint32_t)li < C && j < N) {
+    if constexpr (THINK) {
+      if (active) sj = pq;                      // issue order = ready order; INF past the pending chains
+    } else if (active && (uint32_t)li < C && j < N) {
       const uint64_t aj = R.a[j % RING];
       const uint64_t kj = j >= C ? R.kap[(j - C) % Group<G>::KRING] : 0;
       sj = aj > kj ? aj : kj;
@@ -484,6 +515,20 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const uint64_t cum = R.alpha0 * Sk + R.alpha1 * summin;
     const uint64_t c = t0 + (f * cum) / 1000000u;
     if (member) R.kap[(h + li) % Group<G>::KRING] = c;
+    if constexpr (THINK) {
+      // completion h + li (sorted position li) starts chain h + li + C, ready Z later (THINK block h + li);
+      // it takes the place of the pending entry lane li just batched, then the pending list is re-sorted
+      const uint32_t kord = h + (uint32_t)li;
+      const bool spawn = member && kord + C < N;
+      uint64_t z = 0;
+      if (spawn) z = mulshr(exp_q32(philox(kord, 4, 0, 0, R.k0, R.k1).x), R.g[0], 48);
+      if (member) {
+        pq = spawn ? c + z : INF64;
+        pid = spawn ? kord + C : 0xFFFFFFFFu;
+      }
+      gsort_pair<G>(pq, pid, li);
+      ct.blocks += spawn ? 1u : 0u;
+    }
     const int lastm = (int)(b > 0 ? b - 1 : 0);
     const uint64_t tend = gshfl64<G>(c, lastm);
     const uint32_t maxS = gshfl<G>(Sk, lastm);
@@ -493,7 +538,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const bool measured = member && i >= p.warmup;
     // latency origin: arrival (open loop, R2) or issue (closed loop, §2.11: s_i sits in window lane orig)
     const uint64_t s_orig = gshfl64<G>(sj, (int)orig);
-    const bool from_issue = R.kind == 3;
+    const bool from_issue = R.kind >= 3;
     if (from_issue && member && i == p.warmup) R.a_w = s_orig;     // the goodput window starts at that issue
     const uint64_t l = c - (member ? (from_issue ? s_orig : R.a[i % RING]) : c);
     // stop rule (§2.14): this batch's measured completions in sorted (= time) order continue the count;
@@ -904,9 +949,32 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel_t(const SimParams p) {
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
-  run_mode<8, STOP>(p, 0, wsmem, lane, ct);
-  run_mode<16, STOP>(p, 1, wsmem, lane, ct);
-  run_mode<32, STOP>(p, 2, wsmem, lane, ct);
+  run_mode<8, STOP, false>(p, 0, wsmem, lane, ct);
+  run_mode<16, STOP, false>(p, 1, wsmem, lane, ct);
+  run_mode<32, STOP, false>(p, 2, wsmem, lane, ct);
+  if (p.stats) {
+    const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
+    const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
+    if (lane == 0) {
+      unsigned long long* st = (unsigned long long*)p.stats;
+      atomicAdd(st + 1, (unsigned long long)batches);
+      atomicAdd(st + 2, (unsigned long long)dsteps);
+      atomicAdd(st + 3, (unsigned long long)steps);
+      atomicAdd(st + 4, (unsigned long long)blocks);
+    }
+  }
+}
+
+// K1t: closed loops with think time (kind 4), launched only when a workload uses it
+template <bool STOP>
+__global__ void __maxnreg__(SLO_MAXNREG) slo_sim_think_kernel_t(const SimParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
+  Counters ct{0, 0, 0, 0};
+  run_mode<8, STOP, true>(p, 6, wsmem, lane, ct);
+  run_mode<16, STOP, true>(p, 7, wsmem, lane, ct);
+  run_mode<32, STOP, true>(p, 8, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -950,6 +1018,8 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimPar
 // carries none of the stop rule's code
 template __global__ void slo_sim_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_kernel_t<true>(const SimParams p);
+template __global__ void slo_sim_think_kernel_t<false>(const SimParams p);
+template __global__ void slo_sim_think_kernel_t<true>(const SimParams p);
 template __global__ void slo_sim_cont_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_cont_kernel_t<true>(const SimParams p);
 
@@ -989,6 +1059,10 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
   const uint32_t need = wide == 2 ? 32u : wide ? max((uint32_t)k.conc, (uint32_t)k.max_num_seqs) : beff;
   const bool spec = k.spec_on && k.draft_len > 0;
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
+  if (wl[k.workload].kind == 4) {     // think time: the C pending chains live in the lanes, G >= max(C, B)
+    const uint32_t tneed = wide == 2 ? 32u : max((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
+    return tneed <= 8 ? 6u : (tneed <= 16 ? 7u : 8u);
+  }
   if (wl[k.workload].batching) {      // continuous batching, ~N*O/beff iterations: lane groups G >= min(C, B)
     // (at most min(C, B) requests run at once and a prefill admits at most that many; `wide`: G >= B)
     bucket = min(14u, (31u - __clz(beff)) + (spec ? 0u : 2u));
