@@ -1,5 +1,5 @@
 """Randomised parity soak: `python tests/soak_parity.py BLOCKS` runs BLOCKS random blocks (20 knob records x 2
-seeds each) across lane-group policies, static/continuous batching, arrival kinds, warmup and the stop rule,
+seeds each) across lane-group policies, static/continuous batching, arrival kinds (kind-4 think-time loops included), warmup and the stop rule,
 and compares every latency and output with the oracle (test infrastructure: it imports oracle/)."""
 import os, random, sys
 import numpy as np, torch
@@ -12,7 +12,9 @@ c = inputs.continuous
 wls = [inputs.preset_ll(), inputs.preset_sim(), inputs.preset_stress(kind=1), inputs.preset_stress(kind=2),
        inputs.preset_ll(rate=40.0, stream_id=7), inputs.preset_closed(stream_id=3),
        c(inputs.preset_ll()), c(inputs.preset_sim()), c(inputs.preset_stress(kind=1)), c(inputs.preset_closed(stream_id=4)),
-       c(inputs.workload(kind=0, rate=200.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0), stream_id=5))]
+       c(inputs.workload(kind=0, rate=200.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0), stream_id=5)),
+       inputs.preset_closed(stream_id=11, think_us=200_000), inputs.preset_closed(stream_id=12, think_us=0),
+       inputs.preset_closed(stream_id=13, think_us=3_000)]
 bad = 0
 total = 0
 for block in range(int(sys.argv[1]) if len(sys.argv) > 1 else 40):
