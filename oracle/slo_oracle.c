@@ -527,9 +527,9 @@ static uint64_t iter_noise(const itnoise* nz, uint64_t it) {
 
 static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t issue_origin,
                          uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
-                         const uint32_t* f, adraw* ad, const itnoise* nz, uint32_t warmup, uint32_t slo_us,
-                         const orc_stop* stop, orc_result* res, uint32_t* latencies, orc_req* trace,
-                         orc_counters* cnt) {
+                         const uint32_t* f, adraw* ad, const itnoise* nz, const thinkdraw* th, uint32_t warmup,
+                         uint32_t slo_us, const orc_stop* stop, orc_result* res, uint32_t* latencies,
+                         orc_req* trace, orc_counters* cnt) {
   uint64_t* s = (uint64_t*)calloc(N, sizeof(uint64_t));
   uint64_t* form = (uint64_t*)calloc(N, sizeof(uint64_t));   /* admission (prefill start) */
   uint64_t* c = (uint64_t*)calloc(N, sizeof(uint64_t));
@@ -539,8 +539,17 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
   uint32_t* run = (uint32_t*)calloc(B, sizeof(uint32_t));
   uint32_t* fin = (uint32_t*)calloc(B, sizeof(uint32_t));
   uint32_t* lat = (uint32_t*)calloc(N, sizeof(uint32_t));
-  if (!s || !form || !c || !steps || !batch_of || !rem || !run || !fin || !lat) abort();
+  uint64_t* rdy_t = (uint64_t*)calloc(C, sizeof(uint64_t));     /* kind 4: ready user chains */
+  uint32_t* rdy_q = (uint32_t*)calloc(C, sizeof(uint32_t));
+  if (!s || !form || !c || !steps || !batch_of || !rem || !run || !fin || !lat || !rdy_t || !rdy_q) abort();
 
+  uint32_t nrdy = 0;
+  uint64_t think_blocks = 0;
+  if (th->on) /* the first C chains are ready at t = 0 */
+    for (uint32_t q = 0; q < C && q < N; ++q) {
+      rdy_t[nrdy] = 0;
+      rdy_q[nrdy++] = q;
+    }
   uint32_t na = 0, ni = 0, nq = 0, inflight = 0, ndone = 0, nrun = 0;
   uint32_t join_lo = 0, join_hi = 0;      /* requests being prefilled: they join R at the iteration end */
   uint32_t nfin = 0;                      /* running members finishing at the iteration end */
@@ -550,14 +559,21 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
   while (ndone < N) {
     uint64_t tn = U64MAX;
     if (busy) tn = iter_end;
-    if (na < N && a[na] < tn) tn = a[na];
+    if (!th->on && na < N && a[na] < tn) tn = a[na];
+    for (uint32_t q = 0; q < nrdy; ++q)
+      if (rdy_t[q] < tn) tn = rdy_t[q];
     if (tn == U64MAX) abort();
     t = tn;
     /* (1) the iteration ending at t: completions leave, prefilled requests join */
     if (busy && iter_end == t) {
-      for (uint32_t q = 0; q < nfin; ++q) {
+      for (uint32_t q = 0; q < nfin; ++q) { /* fin[] is in admission = request-index order */
         c[fin[q]] = t;
         --inflight;
+        if (th->on && ndone + C < N) { /* kind 4: completion ndone starts chain ndone + C after Z_ndone */
+          rdy_t[nrdy] = t + think_time(th, ndone);
+          rdy_q[nrdy++] = ndone + C;
+          ++think_blocks;
+        }
         ++ndone;
       }
       uint32_t kept = 0;                              /* drop finished members, keep admission order */
@@ -569,8 +585,21 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
       join_lo = join_hi = 0;
       busy = 0;
     }
-    /* (2) arrivals at t */
-    while (na < N && a[na] == t) ++na;
+    /* (2) arrivals at t (kind 4: the chains ready at t, in chain order) */
+    if (th->on) {
+      for (;;) {
+        uint32_t best = U32MAX;
+        for (uint32_t q = 0; q < nrdy; ++q)
+          if (rdy_t[q] == t && (best == U32MAX || rdy_q[q] < rdy_q[best])) best = q;
+        if (best == U32MAX) break;
+        rdy_t[best] = rdy_t[nrdy - 1];
+        rdy_q[best] = rdy_q[nrdy - 1];
+        --nrdy;
+        ++na;
+      }
+    } else {
+      while (na < N && a[na] == t) ++na;
+    }
     /* (3) issues at t while fewer than C are in flight */
     while (ni < na && inflight < C) {
       s[ni] = t;
@@ -640,9 +669,10 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
     cnt->batches = prefills;                 /* continuous mode: prefill iterations */
     cnt->decode_steps = decode_iters;        /* continuous mode: decode iterations */
     cnt->member_steps = member_steps;
-    cnt->philox_blocks = spec_blocks + ((nz->philox && nz->step_ppm) ? decode_iters : 0);
+    cnt->philox_blocks = spec_blocks + ((nz->philox && nz->step_ppm) ? decode_iters : 0) + think_blocks;
   }
   free(s); free(form); free(c); free(steps); free(batch_of); free(rem); free(run); free(fin); free(lat);
+  free(rdy_t); free(rdy_q);
   return ad->bad ? -2 : 0;
 }
 
@@ -699,12 +729,8 @@ int orc_run_stop(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint
     return -1;
   }
   if (W->batching == 1) {
-    if (th.on) { /* kind 4 is defined for static batching only */
-      free(a); free(P); free(O); free(w3); free(f);
-      return -1;
-    }
     itnoise nz = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, W->timing.noise_step_ppm};
-    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, closed, N, a, P, O, f, &ad, &nz,
+    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, closed, N, a, P, O, f, &ad, &nz, &th,
                        warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   } else {
     rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, closed, N, a, P, O, f, &ad, &th,
@@ -744,7 +770,7 @@ int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seq
   const thinkdraw th = {0, 0, 0, 0};
   if (continuous) {
     itnoise nz = {0, 0, 0, 0};
-    return simulate_cont(tm, conc, max_num_seqs, gamma_eff, issue_origin, n, a, P, O, f, &ad, &nz, warmup_len,
+    return simulate_cont(tm, conc, max_num_seqs, gamma_eff, issue_origin, n, a, P, O, f, &ad, &nz, &th, warmup_len,
                          slo_us, &stop, res, latencies, trace, cnt);
   }
   return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, &th, warmup_len,

@@ -16,8 +16,8 @@ extern "C" {
 typedef struct {
   uint32_t kind;              /* 0 Poisson, 1 MMPP-2 (exponential sojourns), 2 on/off (fixed sojourns),
                                  3 closed loop: C users, zero think time (every a_i = 0, latency from issue),
-                                 4 closed loop with exponential think time of mean mean_gap_q16[0] (static
-                                   batching only) */
+                                 4 closed loop with exponential think time of mean mean_gap_q16[0]
+                                    */
   uint32_t start_state;
   uint64_t mean_gap_q16[2];   /* Q48.16 us; UINT64_MAX = no arrivals in that state */
   uint64_t mean_sojourn_us[2];

@@ -146,9 +146,80 @@ def test_interactive_response_time_law(orc, C, B, think_s):
     assert X * (R + think_s) == pytest.approx(C, rel=0.04)
 
 
-def test_think_requires_static_batching_and_a_finite_mean(orc):
-    with pytest.raises(ValueError):
-        orc.run([inputs.continuous(inputs.preset_closed(think_us=1000))], inputs.knobs(), 1, 10)
+def brute_force_continuous_think(tm, C, B, N, P, O, Z):
+    """Per-microsecond time stepping of the kind-4 closed loop under continuous batching (DESIGN.md §2.11,
+    §2.12; gamma = 0, no noise), written separately from the oracle: completions at one iteration end are
+    numbered in request-index order; completion k makes chain k + C ready Z_k later."""
+    s, c = [None] * N, [None] * N
+    rem = list(O)
+    ready = {q: 0 for q in range(min(C, N))}
+    t = issued = admitted = done = 0
+    running, joining, finishing = [], [], []
+    end = None
+    while done < N:
+        again = True
+        while again:
+            again = False
+            if end == t:
+                for m in sorted(finishing):
+                    c[m] = t
+                    if done + C < N:
+                        ready[done + C] = t + Z[done]
+                    done += 1
+                running = [m for m in running if m not in finishing] + joining
+                finishing, joining, end = [], [], None
+            for q in sorted(q for q, r in ready.items() if r == t):
+                del ready[q]
+                s[issued] = t
+                issued += 1
+            if end is None:
+                if len(running) < B and admitted < issued:
+                    new = list(range(admitted, admitted + min(B - len(running), issued - admitted)))
+                    admitted += len(new)
+                    joining, end = new, t + tm["pre_base_us"] + tm["pre_tok_us"] * max(P[m] for m in new)
+                elif running:
+                    for m in running:
+                        rem[m] -= 1
+                        if rem[m] == 0:
+                            finishing.append(m)
+                    end = t + tm["dec_base_us"] + tm["dec_seq_us"] * len(running)
+                if end == t:
+                    again = True
+        t += 1
+    return s, c
+
+
+@pytest.mark.parametrize("case", range(60))
+def test_continuous_think_matches_brute_force(orc, case):
+    rng = random.Random(7000 + case)
+    think = rng.choice([0, 1, 4, 9])
+    w = inputs.continuous(_tiny(rng, think, 0))
+    C, B, N = rng.randrange(1, 7), rng.randrange(1, 7), rng.randrange(1, 14)
+    seed = rng.getrandbits(64)
+    k = inputs.knobs(conc=C, max_num_seqs=B)
+    r = orc.run([w], k, seed, N, latencies=True, trace=True)
+    _, P, O, _ = orc.request_draws([w], k, seed, N)
+    Z = _think_draws(orc, seed, N, think * 65536)
+    s, c = brute_force_continuous_think(w["timing"], C, B, N, [int(x) for x in P], [int(x) for x in O], Z)
+    assert list(r["trace"]["s"]) == s
+    assert list(r["trace"]["c"]) == c
+    assert list(r["latencies"]) == [ci - si for ci, si in zip(c, s)]
+
+
+@pytest.mark.parametrize("C,B", [(1, 1), (6, 8), (16, 4)])
+def test_continuous_zero_think_is_kind_3(orc, C, B):
+    k = inputs.knobs(conc=C, max_num_seqs=B, draft_len=4, spec_on=1)
+    for N, warm in ((300, 0), (517, 40)):
+        r3 = orc.run([inputs.continuous(inputs.preset_closed())], k, 11, N - warm, warmup_len=warm, latencies=True)
+        r4 = orc.run([inputs.continuous(inputs.preset_closed(think_us=0))], k, 11, N - warm, warmup_len=warm,
+                     latencies=True)
+        assert np.array_equal(r3["latencies"], r4["latencies"])
+        for key in ("p99_us", "slo_met", "window_us", "sum_latency_us", "flags"):
+            assert r3[key] == r4[key]
+        assert r4["counters"]["philox_blocks"] == r3["counters"]["philox_blocks"] + max(0, N - C)
+
+
+def test_think_requires_a_finite_mean(orc):
     w = inputs.preset_closed(think_us=1000)
     w["arrivals"]["mean_gap_q16"][0] = inputs.NO_ARRIVALS
     with pytest.raises(ValueError):
