@@ -27,7 +27,9 @@ struct slo_sim {
   uint32_t n_wl = 0;
   uint32_t crn = 1;
   bool any_cont = false;            // a workload uses continuous batching: launch K1c
-  bool any_think = false;           // a workload is a closed loop with think time: launch K1t
+  bool any_think = false;           // a static-batching workload has think time (kind 4): launch K1t
+  bool any_cont_think = false;      // a continuous-batching workload has think time: launch K1c on lists 9-11
+  bool any_cont_plain = false;      // a continuous-batching workload without think time: K1c on lists 3-5
   uint32_t group_policy = 0;        // slo_sim_opts.group_policy
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
@@ -160,8 +162,6 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     if (x.arr.kind > 4 || x.arr.start_state > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: bad arrival kind", w);
     if (x.arr.kind == 4 && x.arr.mean_gap_q16[0] == NOA)
       return fail(nullptr, SLO_E_INVAL, "workload %u: think time needs a finite mean (mean_gap_q16[0])", w);
-    if (x.arr.kind == 4 && x.batching == 1)
-      return fail(nullptr, SLO_E_UNSUPPORTED, "workload %u: think time (kind 4) with continuous batching", w);
     for (int s = 0; s < 2; ++s)
       if (x.arr.mean_gap_q16[s] != NOA && x.arr.mean_gap_q16[s] > (1ull << 48))
         return fail(nullptr, SLO_E_INVAL, "workload %u: mean_gap_q16 > 2^48", w);
@@ -223,7 +223,11 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   h->sm_count = prop.multiProcessorCount;
   h->n_wl = n_wl;
   for (uint32_t w = 0; w < n_wl; ++w) h->any_cont |= wl[w].batching == 1;
-  for (uint32_t w = 0; w < n_wl; ++w) h->any_think |= wl[w].arr.kind == 4;
+  for (uint32_t w = 0; w < n_wl; ++w) {
+    h->any_think |= wl[w].arr.kind == 4 && wl[w].batching == 0;
+    h->any_cont_think |= wl[w].arr.kind == 4 && wl[w].batching == 1;
+    h->any_cont_plain |= wl[w].arr.kind != 4 && wl[w].batching == 1;
+  }
   h->crn = o.crn;
   if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
@@ -352,18 +356,24 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   int cont_bps = 1;
   slo::SimParams pc{};
   const size_t cont_smem = slo::cont_warp_bytes() * h->warps_per_block;
-  if (h->any_cont) {
+  if (h->any_cont || h->any_cont_think) {
     if (cont_smem > 48 * 1024)
     {
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)cont_smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)cont_smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
     }
     // occupancy is register-bound; give the group rings the whole carveout so smem never binds first
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel_t<false>, h->warps_per_block * 32,
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel_t<false, false>, h->warps_per_block * 32,
                                                       cont_smem) != cudaSuccess || cont_bps < 1)
       cont_bps = 1;
     if (h->blocks_per_sm_opt > 0 && h->blocks_per_sm_opt < cont_bps) cont_bps = h->blocks_per_sm_opt;
@@ -409,16 +419,21 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
         slo::slo_sim_think_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
       CUDA_TRY(h, cudaGetLastError());
     }
-    if (h->any_cont) {   // K1c: the continuous-batching list, one replica per warp
+    // K1c over the continuous-batching lists (one launch for lists 3-5, one for the think-time lists 9-11)
+    for (uint32_t think = 0; think < 2; ++think) {
+      if (!(think ? h->any_cont_think : h->any_cont_plain)) continue;
       uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;
       const uint64_t cneed = ((uint64_t)nc + h->warps_per_block - 1) / h->warps_per_block;
       if (cblocks > cneed) cblocks = cneed;
       pc = p;
       pc.warp_bytes = (uint32_t)slo::cont_warp_bytes();
-      if (p.stop_n | p.stop_t)
-        slo::slo_sim_cont_kernel_t<true><<<(unsigned)cblocks, h->warps_per_block * 32, cont_smem, st>>>(pc);
+      const dim3 cg((unsigned)cblocks), cb(h->warps_per_block * 32);
+      if (think)
+        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, true><<<cg, cb, cont_smem, st>>>(pc)
+                              : slo::slo_sim_cont_kernel_t<false, true><<<cg, cb, cont_smem, st>>>(pc);
       else
-        slo::slo_sim_cont_kernel_t<false><<<(unsigned)cblocks, h->warps_per_block * 32, cont_smem, st>>>(pc);
+        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, false><<<cg, cb, cont_smem, st>>>(pc)
+                              : slo::slo_sim_cont_kernel_t<false, false><<<cg, cb, cont_smem, st>>>(pc);
       CUDA_TRY(h, cudaGetLastError());
     }
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;

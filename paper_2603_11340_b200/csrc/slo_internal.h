@@ -10,8 +10,8 @@ constexpr int kMaxWarpsPerBlock = 8;
 constexpr int kDefaultWarpsPerBlock = 4;
 // K0 work lists: static batching by lane-group size G = 8, 16, 32 (>= min(C, B) narrow, >= max(C, B) wide, or
 // 32 for a lone replica; K1), then continuous batching by G = 8, 16, 32 >= min(C, B) (wide: >= B) (K1c), then
-// closed loops with think time (kind 4) by G = 8, 16, 32 >= max(C, B) (K1t)
-constexpr int kLists = 9;
+// closed loops with think time (kind 4) by G = 8, 16, 32 >= max(C, B): static (K1t), continuous (K1c, think)
+constexpr int kLists = 12;
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 constexpr int kCtlBucket = 32, kCtlWords = kCtlBucket + 2 * 16 * kLists;
 
@@ -49,7 +49,8 @@ struct SimParams {
 };
 
 template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
-template <bool STOP> __global__ void slo_sim_cont_kernel_t(const SimParams p);  // K1c: continuous batching (§2.12)
+// K1c: continuous batching (§2.12); THINK: the kind-4 (think-time) lists 9-11
+template <bool STOP, bool THINK> __global__ void slo_sim_cont_kernel_t(const SimParams p);
 template <bool STOP> __global__ void slo_sim_think_kernel_t(const SimParams p); // K1t: think-time closed loop (§2.11)
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
                                           uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t wide,

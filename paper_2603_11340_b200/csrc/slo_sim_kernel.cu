@@ -652,7 +652,9 @@ struct alignas(16) CGroup {
   uint32_t cnt_meas, stopped, pad3[2];          // stop rule (§2.14): measured completions so far, stopped
 };
 
-template <int G, bool STOP>
+// THINK (kind 4, §2.11): the C pending user chains sit sorted in the lanes (lane l = request nq + l) and give
+// s_next and the prefill window in place of s_j = max(a_j, kappa_{j-C})
+template <int G, bool STOP, bool THINK>
 __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   using CG = CGroup<G>;
   constexpr int RING = CG::RING, KRING = CG::KRING;
@@ -674,6 +676,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
   // sleft: decode iterations the slot's request still runs; stot: its S (counters); fw: noise window
   uint32_t mi = 0, sleft = 0, stot = 0, fw = 0, fw2 = 0, nzc = 0, my_slo = 0;
   uint64_t origin = 0, my_sum = 0, my_cmax = 0;
+  uint64_t pq = INF64;          // THINK: this lane's pending ready instant
+  uint32_t pid = 0xFFFFFFFFu;   // THINK: its user chain id
 
   for (;;) {
     __syncwarp();
@@ -707,7 +711,11 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
             C = k.conc;
             B = k.max_num_seqs;
-            closed = W.kind == 3;
+            closed = W.kind >= 3;
+            if constexpr (THINK) {                       // the first C chains are ready at t = 0
+              pq = ((uint32_t)li < C && (uint32_t)li < N) ? 0ull : INF64;
+              pid = (uint32_t)li;
+            }
             noise = W.t.noise_step_ppm;
             alpha0 = (uint32_t)R.alpha0;                 // d(n) = alpha0 + alpha1 n
             alpha1 = (uint32_t)R.alpha1;
@@ -739,9 +747,12 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         if (gn) gen += G;
         gn = need_s && gen < N && gen < nq + G;
       }
+      const uint64_t pq0 = gshfl64<G>(pq, 0);
       if (need_s) {
         s_next = INF64;
-        if (nq < min(N, ndone + C)) {
+        if (THINK) {
+          s_next = pq0;
+        } else if (nq < min(N, ndone + C)) {
           const uint64_t aj = R.a[nq % RING];
           const uint64_t kj = nq >= C ? R.kap[(nq - C) % KRING] : 0;
           s_next = aj > kj ? aj : kj;
@@ -763,7 +774,9 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       __syncwarp();
       const uint32_t j = nq + (uint32_t)li;
       uint64_t sj = INF64;
-      if (pre && j < min(N, ndone + C)) {
+      if (THINK) {
+        if (pre) sj = pq;
+      } else if (pre && j < min(N, ndone + C)) {
         const uint64_t aj = R.a[j % RING];
         const uint64_t kj = j >= C ? R.kap[(j - C) % KRING] : 0;
         sj = aj > kj ? aj : kj;
@@ -803,6 +816,15 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         ++npre;
         s_next = sn;
         if (kk == (uint32_t)G) need_s = true;
+      }
+      if constexpr (THINK) {                             // the admitted chains leave the pending list
+        const int src = li + (int)kk;
+        const uint64_t sp = gshfl64<G>(pq, src & (G - 1));
+        const uint32_t sq = gshfl<G>(pid, src & (G - 1));
+        if (pre) {
+          pq = src < G ? sp : INF64;
+          pid = src < G ? sq : 0xFFFFFFFFu;
+        }
       }
     }
     // a group that just prefilled decodes in the same pass unless another prefill is due at once
@@ -886,11 +908,43 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           ct.blocks += gamma > 0 ? (stot + 3u) >> 2 : 0u;
           run = false;
         }
+        if constexpr (THINK) {
+          // completion ndone + (rank of mi among this iteration's finishers) starts chain + C, ready Z later
+          uint32_t rk = 0;
+#pragma unroll 4
+          for (int o = 0; o < G; ++o) {
+            const uint32_t mo = gshfl<G>(mi, o), fo = gshfl<G>(fin ? 1u : 0u, o);
+            rk += (fo && mo < mi) ? 1u : 0u;
+          }
+          const uint32_t kord = ndone + rk;
+          const bool spawn = fin && kord + C < N;
+          const uint64_t z = spawn ? mulshr(exp_q32(philox(kord, 4, 0, 0, k0, k1).x), R.g[0], 48) : 0ull;
+          const uint64_t st_ = spawn ? t + z : INF64;
+          const uint32_t sid = spawn ? kord + C : 0xFFFFFFFFu;
+          const uint32_t sm = gballot<G>(spawn, lane);
+          const int np = __popc(gballot<G>(pq != INF64, lane));   // real pending entries (sorted first)
+          const int idx = li - np;
+          const bool take = idx >= 0 && idx < __popc(sm);
+          const int src = take ? (int)__fns(sm, 0, idx + 1) : 0;
+          const uint64_t v = gshfl64<G>(st_, src);
+          const uint32_t vq = gshfl<G>(sid, src);
+          if (take) {
+            pq = v;
+            pid = vq;
+          }
+          gsort_pair<G>(pq, pid, li);
+          ct.blocks += spawn ? 1u : 0u;
+        }
         if (dec && (uint32_t)li < nf) R.kap[(ndone + li) % KRING] = t;
+        const uint64_t pq0 = THINK ? gshfl64<G>(pq, 0) : 0ull;   // (all lanes: the shuffle needs the warp)
         if (dec) {
           ndone += nf;
           nrun -= nf;
-          if (s_next == INF64 && nq < N) need_s = true;  // completions may have opened the gate for nq
+          if (THINK) {
+            s_next = pq0;                                // the earliest pending chain after the spawns
+          } else if (s_next == INF64 && nq < N) {
+            need_s = true;                               // completions may have opened the gate for nq
+          }
         }
         if constexpr (STOP) {                            // stop rule (§2.14): completions at t continue the count
           const uint32_t nfm = __popc(gballot<G>(fin && mi >= p.warmup, lane));
@@ -992,15 +1046,16 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_think_kernel_t(const SimParams 
 #ifndef SLO_CONT_MAXNREG
 #define SLO_CONT_MAXNREG 96
 #endif
-template <bool STOP>
+template <bool STOP, bool THINK>
 __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
-  run_cont<8, STOP>(p, 3, wsmem, lane, ct);
-  run_cont<16, STOP>(p, 4, wsmem, lane, ct);
-  run_cont<32, STOP>(p, 5, wsmem, lane, ct);
+  constexpr int l0 = THINK ? 9 : 3;   // THINK: the closed loops with think time (kind 4), lists 9-11
+  run_cont<8, STOP, THINK>(p, l0, wsmem, lane, ct);
+  run_cont<16, STOP, THINK>(p, l0 + 1, wsmem, lane, ct);
+  run_cont<32, STOP, THINK>(p, l0 + 2, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -1020,8 +1075,10 @@ template __global__ void slo_sim_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_kernel_t<true>(const SimParams p);
 template __global__ void slo_sim_think_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_think_kernel_t<true>(const SimParams p);
-template __global__ void slo_sim_cont_kernel_t<false>(const SimParams p);
-template __global__ void slo_sim_cont_kernel_t<true>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<false, false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<true, false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<false, true>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<true, true>(const SimParams p);
 
 size_t cont_warp_bytes() {
   size_t m = 4 * sizeof(CGroup<8>);
@@ -1061,7 +1118,8 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
   bucket = min(14u, (31u - __clz(beff * beff)) + (spec ? 0u : 3u));
   if (wl[k.workload].kind == 4) {     // think time: the C pending chains live in the lanes, G >= max(C, B)
     const uint32_t tneed = wide == 2 ? 32u : max((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
-    return tneed <= 8 ? 6u : (tneed <= 16 ? 7u : 8u);
+    const uint32_t base = wl[k.workload].batching ? 9u : 6u;
+    return base + (tneed <= 8 ? 0u : (tneed <= 16 ? 1u : 2u));
   }
   if (wl[k.workload].batching) {      // continuous batching, ~N*O/beff iterations: lane groups G >= min(C, B)
     // (at most min(C, B) requests run at once and a prefill admits at most that many; `wide`: G >= B)

@@ -14,7 +14,8 @@ wls = [inputs.preset_ll(), inputs.preset_sim(), inputs.preset_stress(kind=1), in
        c(inputs.preset_ll()), c(inputs.preset_sim()), c(inputs.preset_stress(kind=1)), c(inputs.preset_closed(stream_id=4)),
        c(inputs.workload(kind=0, rate=200.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0), stream_id=5)),
        inputs.preset_closed(stream_id=11, think_us=200_000), inputs.preset_closed(stream_id=12, think_us=0),
-       inputs.preset_closed(stream_id=13, think_us=3_000)]
+       inputs.preset_closed(stream_id=13, think_us=3_000), c(inputs.preset_closed(stream_id=14, think_us=150_000)),
+       c(inputs.preset_closed(stream_id=15, think_us=2_000))]
 bad = 0
 total = 0
 for block in range(int(sys.argv[1]) if len(sys.argv) > 1 else 40):

@@ -128,10 +128,67 @@ def test_think_full_size_sampled(S, orc):
         _check(g, r, ref, f"row {r}")
 
 
+def _wls_cont():
+    c = inputs.continuous
+    return [c(inputs.preset_ll()), c(inputs.preset_closed(stream_id=3)),
+            c(inputs.preset_closed(stream_id=5, think_us=300_000)), c(inputs.preset_closed(stream_id=6, think_us=0)),
+            c(inputs.preset_closed(stream_id=9, think_us=5_000_000)), inputs.preset_closed(stream_id=8, think_us=40_000)]
+
+
+@pytest.mark.parametrize("policy", [1, 2, 3], ids=["narrow", "wide", "warp"])
+@pytest.mark.parametrize("block", range(3))
+def test_think_continuous_random_configs(S, orc, block, policy):
+    """Kind 4 under continuous batching (K1c's think-time instantiation, lists 9-11) beside plain continuous,
+    zero-think continuous and static think-time replicas in one launch."""
+    rng = random.Random(9300 + block)
+    wls = _wls_cont()
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)]
+    ks[0] = inputs.knobs(conc=32, max_num_seqs=32, draft_len=16, spec_on=1, workload=2)
+    ks[1] = inputs.knobs(conc=1, max_num_seqs=1, workload=2)
+    ks[2] = inputs.knobs(conc=32, max_num_seqs=3, workload=3)
+    ks[3] = inputs.knobs(conc=5, max_num_seqs=16, draft_len=4, spec_on=1, workload=4, rate_scale_q8=64)
+    ks[4] = inputs.knobs(conc=12, max_num_seqs=12, workload=2)
+    seeds = inputs.seeds(3, 11 * block + 1)
+    N = rng.choice([37, 333, 1000])
+    warm = rng.choice([0, 17, 100])
+    s = S.Simulator(wls, device=0, group_policy=policy)
+    out = s.run_batch(S.knobs_tensor(ks), S.seeds_tensor(seeds), N, warmup_len=warm, latencies=True, stats=True,
+                      percentiles=True)
+    g = _fetch(S, out, len(ks) * len(seeds), N + warm)
+    s.close()
+    tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
+    for ci, k in enumerate(ks):
+        for si, sd in enumerate(seeds):
+            ref = orc.run(wls, k, sd, N, warmup_len=warm, latencies=True)
+            _check(g, ci * len(seeds) + si, ref, f"replica {ci},{si} knobs {k}")
+            for f in tot:
+                tot[f] += ref["counters"][f]
+    for f in tot:
+        assert int(g["stats"][f]) == tot[f], f
+
+
+def test_think_continuous_stop_rule(S, orc):
+    rng = random.Random(9400)
+    wls = _wls_cont()
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(10)]
+    ks[0] = inputs.knobs(conc=12, max_num_seqs=4, workload=2)
+    seeds = inputs.seeds(2, 78)
+    N, warm = 700, 30
+    s = S.Simulator(wls, device=0)
+    for n_min, t_min in ((50, 0), (1, 3_000_000), (300, 20_000_000), (10, 10**9)):
+        out = s.run_batch(S.knobs_tensor(ks), S.seeds_tensor(seeds), N, warmup_len=warm, latencies=True,
+                          percentiles=True, stop_n_min=n_min, stop_t_min_us=t_min)
+        g = _fetch(S, out, len(ks) * len(seeds), N + warm)
+        for ci, k in enumerate(ks):
+            for si, sd in enumerate(seeds):
+                ref = orc.run(wls, k, sd, N, warmup_len=warm, latencies=True, stop_n_min=n_min,
+                              stop_t_min_us=t_min)
+                _check(g, ci * len(seeds) + si, ref, f"stop {n_min},{t_min} replica {ci},{si}")
+    s.close()
+
+
 def test_think_create_validation(S):
     from paper_2603_11340_b200._lib import SloError
-    with pytest.raises(SloError):
-        S.Simulator([inputs.continuous(inputs.preset_closed(think_us=1000))], device=0)
     w = inputs.preset_closed(think_us=1000)
     w["arrivals"]["mean_gap_q16"][0] = inputs.NO_ARRIVALS
     with pytest.raises(SloError):
