@@ -59,8 +59,8 @@ typedef struct {
                                 /*   waiting from t = 0 and latency is measured from issue */
                                 /* 4 closed loop with exponential think time of mean mean_gap_q16[0]      */
                                 /*   (finite; 0 allowed): completion k starts user chain k + C after      */
-                                /*   Z_k (THINK block (k, 4, 0)); static batching only, else             */
-                                /*   SLO_E_UNSUPPORTED at create                         */
+                                /*   Z_k (THINK block (k, 4, 0)); static or continuous batching          */
+                                /*                                                       */
   uint32_t start_state;         /* 0 or 1                                                               */
   uint64_t mean_gap_q16[2];     /* per-state mean gap, Q48.16 us, <= 2^48; UINT64_MAX = no arrivals     */
   uint64_t mean_sojourn_us[2];  /* kinds 1, 2: per-state mean/fixed sojourn, >= 1                       */

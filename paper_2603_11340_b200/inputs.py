@@ -129,7 +129,7 @@ def preset_closed(stream_id=0, think_us=None) -> Dict:
     """CLOSED: the paper's live client: a single replayed prompt, 64-token output cap and a
     closed loop of `conc` users with zero think time (arrival kind 3); latency from issue.
     With `think_us` (mean, microseconds; 0 allowed) every user thinks an exponential time between a
-    completion and its next request (arrival kind 4, static batching only)."""
+    completion and its next request (arrival kind 4; static or continuous batching)."""
     w = preset_ll(stream_id=stream_id)
     w["arrivals"]["kind"] = 3
     if think_us is not None:

@@ -11,9 +11,11 @@ rng = random.Random(3)
 wls = [inputs.preset_ll(), inputs.preset_sim(), inputs.preset_stress(kind=1), inputs.preset_stress(kind=2)]
 wls += [inputs.continuous(w) for w in wls] + [inputs.continuous(inputs.preset_closed())]   # K1c
 wls += [inputs.preset_closed(think_us=20_000), inputs.preset_closed(think_us=0)]          # K1t (kind 4, §2.11)
+wls += [inputs.continuous(inputs.preset_closed(think_us=20_000))]                          # K1c, THINK
 ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)] + [inputs.knobs(conc=0)]
 ks += [inputs.knobs(max_num_seqs=b, conc=c, workload=w, draft_len=4, spec_on=1) for b, c, w in
-       ((4, 12, 4), (12, 3, 5), (32, 32, 6), (8, 8, 8), (32, 32, 9), (3, 5, 10), (12, 6, 9))]
+       ((4, 12, 4), (12, 3, 5), (32, 32, 6), (8, 8, 8), (32, 32, 9), (3, 5, 10), (12, 6, 9), (6, 20, 11),
+                      (32, 32, 11))]
 for pol in (1, 2):   # narrow (G >= min(C, B)) and wide (G >= max(C, B)) lane groups
     sp = sim.Simulator(wls, device=0, group_policy=pol)
     sp.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(inputs.seeds(3)), 150, warmup_len=10, latencies=True,
