@@ -96,6 +96,11 @@ def lib():
         L.orc_length.restype = C.c_uint32
         L.orc_thresholds.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
         L.orc_thresholds.restype = C.c_uint32
+        L.orc_noise_factor.argtypes = [C.c_uint32, C.c_uint32]
+        L.orc_noise_factor.restype = C.c_uint32
+        L.orc_phases.argtypes = [C.POINTER(Workload), C.POINTER(Knobs), C.c_uint64, C.c_uint32, C.c_uint32,
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint32)]
         L.orc_fnv1a_knobs.argtypes = [C.POINTER(Knobs)]
         L.orc_fnv1a_knobs.restype = C.c_uint32
         L.orc_knobs_valid.argtypes = [C.POINTER(Knobs), C.c_uint32]
@@ -185,6 +190,26 @@ def thresholds(accept_q16: int, width: int, gamma: int):
     T = (C.c_uint64 * 16)()
     ae = lib().orc_thresholds(accept_q16, width, gamma, T)
     return ae, list(T)[:gamma]
+
+
+def noise_factor(w: int, step_ppm: int) -> int:
+    return lib().orc_noise_factor(w, step_ppm)
+
+
+def phases(workloads: Sequence[Dict], knobs: Dict, seed: int, n: int, crn: int = 1):
+    """The first n bursty phases of a replica: (start, D, U, state) arrays."""
+    ws = _WorkloadSet(workloads)
+    k = make_knobs(knobs)
+    st = np.zeros(n, np.uint64)
+    D = np.zeros(n, np.uint64)
+    U = np.zeros(n, np.uint64)
+    s = np.zeros(n, np.uint32)
+    rc = lib().orc_phases(ws.arr, C.byref(k), seed, crn, n, st.ctypes.data_as(C.POINTER(C.c_uint64)),
+                          D.ctypes.data_as(C.POINTER(C.c_uint64)), U.ctypes.data_as(C.POINTER(C.c_uint64)),
+                          s.ctypes.data_as(C.POINTER(C.c_uint32)))
+    if rc != 0:
+        raise ValueError("orc_phases: not a bursty arrival kind")
+    return st, D, U, s
 
 
 def fnv1a_knobs(d: Dict) -> int:

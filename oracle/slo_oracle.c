@@ -106,6 +106,13 @@ static uint32_t accepted_prefix(uint32_t u, const uint64_t* T, uint32_t gamma) {
   return A;
 }
 
+/* batch noise factor ("light noise"): f = 10^6 + (b0+b1+b2+b3 - 510) * step_ppm from
+ * the four bytes of a word (the head's w3, or an ITER word under continuous batching). */
+uint32_t orc_noise_factor(uint32_t w, uint32_t step_ppm) {
+  int64_t bytesum = (int64_t)(w & 0xFF) + (int64_t)((w >> 8) & 0xFF) + (int64_t)((w >> 16) & 0xFF) + (int64_t)(w >> 24);
+  return (uint32_t)(1000000 + (bytesum - 510) * (int64_t)step_ppm);
+}
+
 /* knob record bytes (little-endian), FNV-1a-32. */
 static void knob_bytes(const orc_knobs* k, uint8_t b[32]) {
   memset(b, 0, 32);
@@ -157,36 +164,87 @@ static uint64_t capacity(uint64_t D, uint64_t rho) {
 }
 
 /* ---------------------------------------------------------------------------------------------- */
+/* bursty phases (kinds 1, 2): phase p is in state (start_state + p) mod 2, lasts D_p    */
+/* (an exponential sojourn from PHASE block p for kind 1, the fixed sojourn for kind 2) and holds U_p     */
+/* operational-time units (its expected arrival count D_p / g_s in Q32 units, reading R26).              */
+/* ---------------------------------------------------------------------------------------------- */
+typedef struct {
+  uint32_t p, state;
+  uint64_t start, D, U, Lambda;   /* start instant, duration, operational capacity, operational start */
+} phase_t;
+
+static void phase_setup(phase_t* ph, const orc_workload* W, uint32_t k0, uint32_t k1, const uint64_t rho[2]) {
+  ph->state = (W->arr.start_state + ph->p) & 1u;
+  if (W->arr.kind == 1) {
+    uint32_t w[4];
+    block(k0, k1, ph->p, 2, 0, w);
+    ph->D = (uint64_t)(((u128)orc_exp_q32(w[0]) * W->arr.mean_sojourn_us[ph->state]) >> 32);
+  } else {
+    ph->D = W->arr.mean_sojourn_us[ph->state];
+  }
+  ph->U = capacity(ph->D, rho[ph->state]);
+}
+
+static void phase_first(phase_t* ph, const orc_workload* W, uint32_t k0, uint32_t k1, const uint64_t rho[2]) {
+  ph->p = 0;
+  ph->start = 0;
+  ph->Lambda = 0;
+  phase_setup(ph, W, k0, k1, rho);
+}
+
+static void phase_next(phase_t* ph, const orc_workload* W, uint32_t k0, uint32_t k1, const uint64_t rho[2]) {
+  ph->Lambda += ph->U;
+  ph->start += ph->D;
+  ph->p += 1;
+  phase_setup(ph, W, k0, k1, rho);
+}
+
+static void replica_keys(const orc_workload* wl, const orc_knobs* k, uint64_t seed, uint32_t crn, uint32_t* k0,
+                         uint32_t* k1, uint64_t g[2], uint64_t rho[2]) {
+  const orc_workload* W = &wl[k->workload];
+  uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
+  *k0 = (uint32_t)seed;
+  *k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+  g[0] = scaled_gap(W->arr.mean_gap_q16[0], k->rate_scale_q8);
+  g[1] = scaled_gap(W->arr.mean_gap_q16[1], k->rate_scale_q8);
+  /* per-state rate rho_s = floor((2^64 - 1) / g_s), 0 for a state without arrivals;
+   * g = 0 only for kind 4, a zero mean think time (rho is used by kinds 1 and 2) */
+  rho[0] = g[0] == U64MAX || g[0] == 0 ? 0 : U64MAX / g[0];
+  rho[1] = g[1] == U64MAX || g[1] == 0 ? 0 : U64MAX / g[1];
+}
+
+int orc_phases(const orc_workload* wl, const orc_knobs* k, uint64_t seed, uint32_t crn, uint32_t n,
+               uint64_t* start, uint64_t* D, uint64_t* U, uint32_t* state) {
+  const orc_workload* W = &wl[k->workload];
+  if (W->arr.kind != 1 && W->arr.kind != 2) return -1;
+  uint32_t k0, k1;
+  uint64_t g[2], rho[2];
+  replica_keys(wl, k, seed, crn, &k0, &k1, g, rho);
+  phase_t ph;
+  phase_first(&ph, W, k0, k1, rho);
+  for (uint32_t q = 0; q < n; ++q) {
+    start[q] = ph.start;
+    D[q] = ph.D;
+    U[q] = ph.U;
+    state[q] = ph.state;
+    phase_next(&ph, W, k0, k1, rho);
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------- */
 /* request draws a_i, P_i, O_i, w3_i                                         */
 /* ---------------------------------------------------------------------------------------------- */
 int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
                       uint32_t n, uint64_t* a, uint32_t* P, uint32_t* O, uint32_t* w3) {
   const orc_workload* W = &wl[k->workload];
-  uint32_t cfgkey = crn ? W->stream_id : orc_fnv1a_knobs(k);
-  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
-  uint64_t g[2] = {scaled_gap(W->arr.mean_gap_q16[0], k->rate_scale_q8),
-                   scaled_gap(W->arr.mean_gap_q16[1], k->rate_scale_q8)};
-  uint32_t kind = W->arr.kind;
-  /* per-state rate rho_s = floor((2^64 - 1) / g_s), 0 for a state without arrivals */
-  uint64_t rho[2] = {g[0] == U64MAX || g[0] == 0 ? 0 : U64MAX / g[0], g[1] == U64MAX || g[1] == 0 ? 0 : U64MAX / g[1]};
-  /* (g = 0 only for kind 4, a zero mean think time; rho is used by kinds 1 and 2) */
-
-  /* bursty phase state (kinds 1, 2) */
-  uint32_t p = 0;
-  uint64_t start = 0, D = 0, U = 0, Lambda = 0, tau = 0;
-  uint32_t state = W->arr.start_state & 1u;
-  if (kind != 0) {
-    uint32_t w[4];
-    if (kind == 1) {
-      block(k0, k1, 0, 2, 0, w);
-      D = (uint64_t)(((u128)orc_exp_q32(w[0]) * W->arr.mean_sojourn_us[state]) >> 32);
-    } else {
-      D = W->arr.mean_sojourn_us[state];
-    }
-    U = capacity(D, rho[state]);
-  }
-
-  uint64_t prev = 0;
+  uint32_t k0, k1;
+  uint64_t g[2], rho[2];
+  replica_keys(wl, k, seed, crn, &k0, &k1, g, rho);
+  const uint32_t kind = W->arr.kind;
+  phase_t ph = {0, 0, 0, 0, 0, 0};
+  if (kind == 1 || kind == 2) phase_first(&ph, W, k0, k1, rho);
+  uint64_t prev = 0, tau = 0;
   for (uint32_t i = 0; i < n; ++i) {
     uint32_t w[4];
     block(k0, k1, i, 0, 0, w);
@@ -198,31 +256,18 @@ int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed,
       uint64_t gap = (uint64_t)(((u128)E * g[0]) >> 48);
       a[i] = prev + gap;
       prev = a[i];
-    } else {
+    } else {                   /* Cox time change: operational epoch tau_i -> the phase holding it */
       tau += E;
-      while (tau >= Lambda + U) { /* advance to the phase containing tau */
-        Lambda += U;
-        start += D;
-        ++p;
-        state = (W->arr.start_state + p) & 1u;
-        if (kind == 1) {
-          uint32_t ph[4];
-          block(k0, k1, p, 2, 0, ph);
-          D = (uint64_t)(((u128)orc_exp_q32(ph[0]) * W->arr.mean_sojourn_us[state]) >> 32);
-        } else {
-          D = W->arr.mean_sojourn_us[state];
-        }
-        U = capacity(D, rho[state]);
-      }
-      uint64_t off = (uint64_t)(((u128)(tau - Lambda) * g[state]) >> 48);
-      if (off > D - 1) off = D - 1;
-      a[i] = start + off;
+      while (tau >= ph.Lambda + ph.U) phase_next(&ph, W, k0, k1, rho);
+      uint64_t off = (uint64_t)(((u128)(tau - ph.Lambda) * g[ph.state]) >> 48);
+      if (off > ph.D - 1) off = ph.D - 1;
+      a[i] = ph.start + off;
     }
     P[i] = orc_length(W->prompt_cw, W->prompt_ncw, W->prompt_lo, w[1]);
     O[i] = orc_length(W->output_cw, W->output_ncw, W->output_lo, w[2]);
     w3[i] = w[3];
   }
-  return (int)((kind == 1 || kind == 2) ? p + 1 : 0); /* phases drawn (kind 1 consumes one block each) */
+  return (int)((kind == 1 || kind == 2) ? ph.p + 1 : 0); /* phases drawn (kind 1 consumes one block each) */
 }
 
 /* ---------------------------------------------------------------------------------------------- */
@@ -520,9 +565,7 @@ static uint64_t iter_noise(const itnoise* nz, uint64_t it) {
   if (!nz->philox || nz->step_ppm == 0) return 1000000u;
   uint32_t w[4];
   block(nz->k0, nz->k1, (uint32_t)it, 3, 0, w);
-  int64_t bytesum = (int64_t)(w[0] & 0xFF) + (int64_t)((w[0] >> 8) & 0xFF) + (int64_t)((w[0] >> 16) & 0xFF) +
-                    (int64_t)(w[0] >> 24);
-  return (uint64_t)(1000000 + (bytesum - 510) * (int64_t)nz->step_ppm);
+  return orc_noise_factor(w[0], nz->step_ppm);
 }
 
 static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t issue_origin,
@@ -710,11 +753,7 @@ int orc_run_stop(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint
   uint32_t* f = (uint32_t*)malloc((size_t)N * sizeof(uint32_t));
   if (!a || !P || !O || !w3 || !f) abort();
   int phases = orc_request_draws(wl, k, seed, crn, N, a, P, O, w3);
-  for (uint32_t i = 0; i < N; ++i) { /* DESIGN.md §2.4 noise factor from w3's four bytes */
-    int64_t bytesum = (int64_t)(w3[i] & 0xFF) + (int64_t)((w3[i] >> 8) & 0xFF) +
-                      (int64_t)((w3[i] >> 16) & 0xFF) + (int64_t)(w3[i] >> 24);
-    f[i] = (uint32_t)(1000000 + (bytesum - 510) * (int64_t)W->timing.noise_step_ppm);
-  }
+  for (uint32_t i = 0; i < N; ++i) f[i] = orc_noise_factor(w3[i], W->timing.noise_step_ppm); /* §2.4 */
   uint32_t gamma = k->spec_on ? k->draft_len : 0;
   uint64_t T[16];
   orc_thresholds(k->accept_q16, k->draft_width, gamma, T);

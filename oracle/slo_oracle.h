@@ -72,6 +72,8 @@ uint64_t orc_exp_q32(uint32_t u);
 uint32_t orc_length(const uint32_t* cw, uint32_t ncw, uint32_t lo, uint32_t u);
 /* acceptance thresholds T_1..T_gamma; returns alpha_eff */
 uint32_t orc_thresholds(uint32_t accept_q16, uint32_t width, uint32_t gamma, uint64_t* T);
+/* batch noise factor f (ppm) from a word's four bytes */
+uint32_t orc_noise_factor(uint32_t w, uint32_t step_ppm);
 /* FNV-1a-32 over the 32 knob bytes */
 uint32_t orc_fnv1a_knobs(const orc_knobs* k);
 /* 1 if the knob record is valid */
@@ -80,6 +82,11 @@ int orc_knobs_valid(const orc_knobs* k, uint32_t n_wl);
 /* Per-request draws of the Philox mode: a_i, P_i, O_i, w3_i for i < n (arrays of length n). */
 int orc_request_draws(const orc_workload* wl, const orc_knobs* k, uint64_t seed, uint32_t crn,
                       uint32_t n, uint64_t* a, uint32_t* P, uint32_t* O, uint32_t* w3);
+
+/* The first n bursty phases (kinds 1, 2) of a replica: start instant, duration D_p,
+ * operational capacity U_p and state.  Returns -1 for other arrival kinds. */
+int orc_phases(const orc_workload* wl, const orc_knobs* k, uint64_t seed, uint32_t crn, uint32_t n,
+               uint64_t* start, uint64_t* D, uint64_t* U, uint32_t* state);
 
 /* Full replica in Philox mode. latencies[N] (stored u32), trace[N], counters nullable.
  * Returns 0, or <0 on an argument error (invalid knobs are not an error: flags bit 0). */
