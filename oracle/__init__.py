@@ -113,7 +113,7 @@ def lib():
         L.orc_run_stop.argtypes = [C.POINTER(Workload), C.c_uint32, C.POINTER(Knobs), C.c_uint64, C.c_uint32,
                                    C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Result),
                                    C.POINTER(C.c_uint32), C.POINTER(Req), C.POINTER(Counters)]
-        L.orc_run_trace_stop.argtypes = [C.POINTER(Timing), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+        L.orc_run_trace_stop.argtypes = [C.POINTER(Timing), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                          C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                          C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32,
@@ -270,8 +270,10 @@ def run(workloads: Sequence[Dict], knobs: Dict, seed: int, segment_len: int, war
 def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_us: int,
               a: Sequence[int], P: Sequence[int], O: Sequence[int], f: Optional[Sequence[int]] = None,
               A: Optional[Sequence[Sequence[int]]] = None, warmup_len: int = 0, slo_us: int = 1_200_000,
-              issue_origin: int = 0, continuous: int = 0, stop_n_min: int = 0, stop_t_min_us: int = 0) -> Dict:
-    """Trace mode: explicit requests (a, P, O), per-request noise factor f (ppm) and accepted-prefix draws."""
+              issue_origin: int = 0, continuous: int = 0, stop_n_min: int = 0, stop_t_min_us: int = 0,
+              width: int = 1) -> Dict:
+    """Trace mode: explicit requests (a, P, O), per-request noise factor f (ppm) and accepted-prefix draws;
+    `width` = draft width W in the speculative step cost (R28)."""
     n = len(a)
     tm = Timing(**timing)
     a_ = (C.c_uint64 * n)(*a)
@@ -289,7 +291,7 @@ def run_trace(timing: Dict, conc: int, max_num_seqs: int, gamma: int, max_wait_u
     res, cnt = Result(), Counters()
     lat = np.zeros(n, np.uint32)
     tr = (Req * n)()
-    rc = lib().orc_run_trace_stop(C.byref(tm), conc, max_num_seqs, gamma, max_wait_us, issue_origin, continuous, n,
+    rc = lib().orc_run_trace_stop(C.byref(tm), conc, max_num_seqs, gamma, width, max_wait_us, issue_origin, continuous, n,
                                   a_, P_, O_, f_, off_, val_, warmup_len, slo_us, stop_n_min, stop_t_min_us,
                                   C.byref(res), lat.ctypes.data_as(C.POINTER(C.c_uint32)), tr, C.byref(cnt))
     if rc != 0:

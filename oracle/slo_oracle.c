@@ -295,11 +295,17 @@ static uint32_t draw_A(adraw* d, uint32_t i, uint32_t j, uint32_t gamma) {
   return d->A_val[d->A_off[i] + j];
 }
 
-static uint64_t step_cost(const orc_timing* tm, uint32_t gamma, uint64_t n) {
+/* DESIGN.md §2.6 decode step cost with n active sequences; with speculation (R10, factorised per R28,
+ * P:98 "draft width W and verifier cadence k", "wider drafts add verifier and compute cost"):
+ * W draft branches of gamma tokens each cost gamma*W*(dr_base + dr_seq*n), and the verifier scores the
+ * W*gamma drafted tokens plus one per sequence: ver_base + ver_seq*n + ver_tok*(W*gamma + 1)*n.  W = 1 is
+ * R10's cost exactly. */
+static uint64_t step_cost(const orc_timing* tm, uint32_t gamma, uint32_t width, uint64_t n) {
   if (gamma == 0) return (uint64_t)tm->dec_base_us + (uint64_t)tm->dec_seq_us * n;
-  return (uint64_t)gamma * ((uint64_t)tm->dr_base_us + (uint64_t)tm->dr_seq_us * n) +
+  const uint64_t drafted = (uint64_t)gamma * width;
+  return drafted * ((uint64_t)tm->dr_base_us + (uint64_t)tm->dr_seq_us * n) +
          (uint64_t)tm->ver_base_us + (uint64_t)tm->ver_seq_us * n +
-         (uint64_t)tm->ver_tok_us * (uint64_t)(gamma + 1) * n;
+         (uint64_t)tm->ver_tok_us * (drafted + 1) * n;
 }
 
 /* DESIGN.md §2.11 kind 4 — closed loop with exponential think time: the k-th completion (k = 0, 1, ...)
@@ -386,7 +392,8 @@ static void outputs(uint32_t N, uint32_t warmup, uint32_t slo_us, const uint64_t
   free(sorted);
 }
 
-static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t mw, uint32_t issue_origin,
+static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t width, uint32_t mw,
+                    uint32_t issue_origin,
                     uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
                     const uint32_t* f, adraw* ad, const thinkdraw* th, uint32_t warmup, uint32_t slo_us,
                     const orc_stop* stop, orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
@@ -484,7 +491,7 @@ static int simulate(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma
         uint32_t j = 0;
         while (active > 0) {
           uint64_t n = active;
-          cum += step_cost(tm, gamma, n);
+          cum += step_cost(tm, gamma, width, n);
           for (uint32_t m = 0; m < b; ++m) {
             if (rem[m] == 0) continue;
             uint32_t e = 1;
@@ -568,7 +575,8 @@ static uint64_t iter_noise(const itnoise* nz, uint64_t it) {
   return orc_noise_factor(w[0], nz->step_ppm);
 }
 
-static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t issue_origin,
+static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t gamma, uint32_t width,
+                         uint32_t issue_origin,
                          uint32_t N, const uint64_t* a, const uint32_t* P, const uint32_t* O,
                          const uint32_t* f, adraw* ad, const itnoise* nz, const thinkdraw* th, uint32_t warmup,
                          uint32_t slo_us, const orc_stop* stop, orc_result* res, uint32_t* latencies,
@@ -669,7 +677,7 @@ static int simulate_cont(const orc_timing* tm, uint32_t C, uint32_t B, uint32_t 
         busy = 1;
       } else if (nrun > 0) {                            /* one decode iteration of the running set */
         uint64_t fi = iter_noise(nz, it);
-        uint64_t D = (uint64_t)(((u128)fi * step_cost(tm, gamma, nrun)) / 1000000u);
+        uint64_t D = (uint64_t)(((u128)fi * step_cost(tm, gamma, width, nrun)) / 1000000u);
         for (uint32_t q = 0; q < nrun; ++q) {
           uint32_t m = run[q];
           uint32_t e = 1;
@@ -769,10 +777,10 @@ int orc_run_stop(const orc_workload* wl, uint32_t n_wl, const orc_knobs* k, uint
   }
   if (W->batching == 1) {
     itnoise nz = {1, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, W->timing.noise_step_ppm};
-    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, closed, N, a, P, O, f, &ad, &nz, &th,
+    rc = simulate_cont(&W->timing, k->conc, k->max_num_seqs, gamma, k->draft_width, closed, N, a, P, O, f, &ad, &nz, &th,
                        warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   } else {
-    rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->max_wait_us, closed, N, a, P, O, f, &ad, &th,
+    rc = simulate(&W->timing, k->conc, k->max_num_seqs, gamma, k->draft_width, k->max_wait_us, closed, N, a, P, O, f, &ad, &th,
                   warmup_len, slo_us, &stop, res, latencies, trace, cnt);
   }
   if (cnt) cnt->philox_blocks += N + (W->arr.kind == 1 ? (uint64_t)phases : 0);
@@ -786,19 +794,19 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
                   const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
-  return orc_run_trace_stop(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, continuous, n, a, P, O, f,
-                            A_off, A_val, warmup_len, slo_us, 0, 0, res, latencies, trace, cnt);
+  return orc_run_trace_stop(tm, conc, max_num_seqs, gamma_eff, 1, max_wait_us, issue_origin, continuous, n, a, P, O,
+                            f, A_off, A_val, warmup_len, slo_us, 0, 0, res, latencies, trace, cnt);
 }
 
 int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
-                       uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
+                       uint32_t draft_width, uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
                        const uint64_t* a, const uint32_t* P,
                        const uint32_t* O, const uint32_t* f, const uint32_t* A_off, const uint32_t* A_val,
                        uint32_t warmup_len, uint32_t slo_us, uint32_t stop_n_min, uint32_t stop_t_min_us,
                        orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt) {
   const orc_stop stop = {stop_n_min, stop_t_min_us};
   if (!tm || !a || !P || !O || !f || !res || n == 0 || warmup_len >= n) return -1;
-  if (conc < 1 || max_num_seqs < 1) return -1;
+  if (conc < 1 || max_num_seqs < 1 || draft_width < 1) return -1;
   if (gamma_eff > 0 && (!A_off || !A_val)) return -1;
   for (uint32_t i = 1; i < n; ++i)
     if (a[i] < a[i - 1]) return -1;
@@ -809,9 +817,9 @@ int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seq
   const thinkdraw th = {0, 0, 0, 0};
   if (continuous) {
     itnoise nz = {0, 0, 0, 0};
-    return simulate_cont(tm, conc, max_num_seqs, gamma_eff, issue_origin, n, a, P, O, f, &ad, &nz, &th, warmup_len,
+    return simulate_cont(tm, conc, max_num_seqs, gamma_eff, draft_width, issue_origin, n, a, P, O, f, &ad, &nz, &th, warmup_len,
                          slo_us, &stop, res, latencies, trace, cnt);
   }
-  return simulate(tm, conc, max_num_seqs, gamma_eff, max_wait_us, issue_origin, n, a, P, O, f, &ad, &th, warmup_len,
+  return simulate(tm, conc, max_num_seqs, gamma_eff, draft_width, max_wait_us, issue_origin, n, a, P, O, f, &ad, &th, warmup_len,
                   slo_us, &stop, res, latencies, trace, cnt);
 }

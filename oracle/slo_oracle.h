@@ -114,8 +114,9 @@ int orc_run_trace(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, ui
                   uint32_t warmup_len, uint32_t slo_us,
                   orc_result* res, uint32_t* latencies, orc_req* trace, orc_counters* cnt);
 
+/* ... with a draft width W (>= 1) in the speculative step cost (R28) and a stop rule (§2.14) */
 int orc_run_trace_stop(const orc_timing* tm, uint32_t conc, uint32_t max_num_seqs, uint32_t gamma_eff,
-                       uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
+                       uint32_t draft_width, uint32_t max_wait_us, uint32_t issue_origin, uint32_t continuous, uint32_t n,
                        const uint64_t* a, const uint32_t* P, const uint32_t* O, const uint32_t* f,
                        const uint32_t* A_off, const uint32_t* A_val, uint32_t warmup_len, uint32_t slo_us,
                        uint32_t stop_n_min, uint32_t stop_t_min_us, orc_result* res, uint32_t* latencies,

@@ -24,7 +24,8 @@ def _traces():
 @pytest.mark.parametrize("tr", _traces(), ids=lambda t: t["name"].split()[0])
 def test_hand_traces(orc, tr):
     r = orc.run_trace(tr["timing"], tr["conc"], tr["B"], tr["gamma"], tr["max_wait_us"], tr["a"], tr["P"],
-                      tr["O"], f=tr.get("f"), A=tr.get("A"), slo_us=tr["slo_us"], continuous=tr.get("continuous", 0))
+                      tr["O"], f=tr.get("f"), A=tr.get("A"), slo_us=tr["slo_us"], continuous=tr.get("continuous", 0),
+                      width=tr.get("W", 1))
     ex = tr["expect"]
     assert list(r["trace"]["c"]) == ex["c"]
     if "s" in ex:
@@ -41,7 +42,7 @@ def test_hand_traces(orc, tr):
 # ------------------------------------------------------------------------------------------------
 # an independent brute-force simulator: advances time one microsecond at a time
 # ------------------------------------------------------------------------------------------------
-def brute_force(tm, C, B, gamma, mw, a, P, O, f, A):
+def brute_force(tm, C, B, gamma, mw, a, P, O, f, A, W=1):
     """Per-microsecond time stepping of DESIGN.md §2.6 (written separately from the oracle's event loop)."""
     N = len(a)
     s = [None] * N
@@ -76,8 +77,8 @@ def brute_force(tm, C, B, gamma, mw, a, P, O, f, A):
                         if gamma == 0:
                             d = tm["dec_base_us"] + tm["dec_seq_us"] * n
                         else:
-                            d = (gamma * (tm["dr_base_us"] + tm["dr_seq_us"] * n) + tm["ver_base_us"]
-                                 + tm["ver_seq_us"] * n + tm["ver_tok_us"] * (gamma + 1) * n)
+                            d = (gamma * W * (tm["dr_base_us"] + tm["dr_seq_us"] * n) + tm["ver_base_us"]
+                                 + tm["ver_seq_us"] * n + tm["ver_tok_us"] * (W * gamma + 1) * n)
                         cum += d
                         for m in sorted(rem):
                             e = 1 if gamma == 0 else min(A[m][j] + 1, rem[m])
@@ -116,8 +117,9 @@ def test_brute_force_agreement(orc, case):
     C = rng.randrange(1, 6)
     B = rng.randrange(1, 6)
     mw = rng.choice([0, 0, rng.randrange(1, 60)])
-    s_bf, c_bf = brute_force(tm, C, B, gamma, mw, a, P, O, f, A)
-    r = orc.run_trace(tm, C, B, gamma, mw, a, P, O, f=f, A=A if gamma else None)
+    W = rng.choice([1, 1, 2, 3, 4])               # draft width in the speculative step cost (R28)
+    s_bf, c_bf = brute_force(tm, C, B, gamma, mw, a, P, O, f, A, W=W)
+    r = orc.run_trace(tm, C, B, gamma, mw, a, P, O, f=f, A=A if gamma else None, width=W)
     assert list(r["trace"]["c"]) == c_bf
     assert list(r["trace"]["s"]) == s_bf
 
@@ -419,7 +421,7 @@ def test_percentiles_nearest_rank(orc):
 # ------------------------------------------------------------------------------------------------
 # NEXT-2: continuous (iteration-level) batching
 # ------------------------------------------------------------------------------------------------
-def brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=False):
+def brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=False, W=1):
     """Per-microsecond time stepping of DESIGN.md §2.12 (written separately from the oracle)."""
     N = len(a)
     s, c = [None] * N, [None] * N
@@ -455,8 +457,8 @@ def brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=False):
                     if gamma == 0:
                         d = tm["dec_base_us"] + tm["dec_seq_us"] * n
                     else:
-                        d = (gamma * (tm["dr_base_us"] + tm["dr_seq_us"] * n) + tm["ver_base_us"]
-                             + tm["ver_seq_us"] * n + tm["ver_tok_us"] * (gamma + 1) * n)
+                        d = (gamma * W * (tm["dr_base_us"] + tm["dr_seq_us"] * n) + tm["ver_base_us"]
+                             + tm["ver_seq_us"] * n + tm["ver_tok_us"] * (W * gamma + 1) * n)
                     for m in running:
                         e = 1 if gamma == 0 else min(A[m][steps[m]] + 1, rem[m])
                         rem[m] -= e
@@ -486,9 +488,10 @@ def test_continuous_brute_force_agreement(orc, case):
     if closed:
         a = [0] * n
     C, B = rng.randrange(1, 6), rng.randrange(1, 6)
-    s_bf, c_bf, l_bf = brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=closed)
+    W = rng.choice([1, 1, 2, 3, 4])
+    s_bf, c_bf, l_bf = brute_force_continuous(tm, C, B, gamma, a, P, O, f, A, issue_origin=closed, W=W)
     r = orc.run_trace(tm, C, B, gamma, 0, a, P, O, f=f, A=A if gamma else None, continuous=1,
-                      issue_origin=int(closed))
+                      issue_origin=int(closed), width=W)
     assert list(r["trace"]["c"]) == c_bf and list(r["trace"]["s"]) == s_bf
     assert list(r["latencies"]) == l_bf
 
