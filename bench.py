@@ -5,8 +5,12 @@
 One step = one pass of the whole hot path (K1 simulate every replica -> K2 per-config
 aggregation -> [N>1: NCCL all-gather of the aggregates + K2b reduce] (+ K3 climb step for c4)) over one
 batch of synthetic input already resident in HBM.  Default workload = BASELINE config 2 (16 C x 8 B x 4 spec
-x 64 seeds, 10k-request segments, LL preset).  N>1 (torchrun): weak scaling, every rank runs the full grid
-on its own seed block; value = all ranks' simulated requests / max-over-ranks device time.
+x 64 seeds, 10k-request segments, LL preset).  N>1 (torchrun): the BASELINE config itself is partitioned
+(SURVEY §8(e)): sweeps are config-sharded (config c -> rank c mod N, all of its seeds local; one NCCL
+all_gather_into_tensor of the per-config aggregates), the climb is seed-sharded (aggregates all-gathered and
+summed by K3) — "scaling": "strong".  `--scaling weak` instead runs the full grid on every rank with its own
+seed block.  value = simulated requests (counted by the kernels, invalid padding excluded) of all ranks /
+max-over-ranks device time.
 
 `--impl reference`: the CPU oracle (oracle/, as it stands) on the host cores on a bounded sample of the
 same workload — the tier's reference arm.  The oracle is otherwise only used by the cpu_baseline leg.
@@ -110,6 +114,25 @@ def cpu_oracle_sample(cfg, budget_s=12.0, seed_offset=0):
     return done_req / dt, cores, done_rep, done_req, dt
 
 
+def cpu_oracle_1core(cfg, budget_s=6.0):
+    """The oracle on ONE host core (this process, no pool), same replica order, ~budget_s of work."""
+    import oracle
+    oracle.build()
+    seeds = cfg.seeds()
+    done_req = done_rep = 0
+    t0 = time.perf_counter()
+    for s in range(cfg.n_seeds):
+        for k in cfg.knobs:
+            oracle.run(cfg.workloads, k, seeds[s], cfg.segment_len)
+            done_req += cfg.segment_len
+            done_rep += 1
+            if time.perf_counter() - t0 > budget_s:
+                dt = time.perf_counter() - t0
+                return done_req / dt, done_rep, done_req, dt
+    dt = time.perf_counter() - t0
+    return done_req / dt, done_rep, done_req, dt
+
+
 # ------------------------------------------------------------------------------------------------
 # clocks sampler (B200_PROFILING.md clocks line)
 # ------------------------------------------------------------------------------------------------
@@ -180,9 +203,12 @@ def main():
     ap.add_argument("--group-policy", type=int, default=0, choices=[0, 1, 2, 3],
                     help="lane groups: 0 auto, 1 narrow G>=min(C,B), 2 wide G>=max(C,B), 3 whole warp")
     ap.add_argument("--eager-climb", action="store_true", help="c4: host loop instead of the CUDA-graph step")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                    help="N>1 aggregate exchange: p2p = K2x/K2w through CUDA IPC peer windows (NEXT-4), "
-                         "nccl = K2 + all_gather_into_tensor + K2b/K3 (also the fallback when p2p cannot map)")
+    ap.add_argument("--exchange", default="nccl", choices=["p2p", "nccl"],
+                    help="N>1 aggregate exchange: nccl = K2 + all_gather_into_tensor (+ K2b / K3 summing the parts); "
+                         "p2p = K2x/K2w through CUDA IPC peer windows (NEXT-4; seed-sharded climb and weak sweeps)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1 sweeps: strong = the BASELINE grid config-sharded over ranks (SURVEY §8(e)); "
+                         "weak = every rank runs the full grid on its own seed block")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -241,16 +267,23 @@ def main():
                       blocks_per_sm=args.blocks_per_sm, group_policy=args.group_policy)
     info = S.info()
 
-    from paper_2603_11340_b200.dist import seed_block, sweep_seed_offset
+    from paper_2603_11340_b200.dist import config_shard, seed_block, sweep_seed_offset
+    strong = args.scaling == "strong" or world == 1
+    knobs_local = cfg.knobs
     if args.workload == "c4":
         # the climb is seed-sharded (strong scaling): the pooled aggregates equal the 1-GPU ones exactly
         lo, hi = seed_block(cfg.n_seeds, rank, world)
         seeds = cfg.seeds()[lo:hi]
+    elif strong:
+        # sweeps are config-sharded: config c -> rank c mod world, all seeds local; every rank's
+        # share is padded to the same length with always-invalid records (no work) for the all-gather
+        seeds = cfg.seeds()
+        knobs_local = config_shard(cfg.knobs, rank, world, pad=inputs.PAD_KNOBS)
     else:
-        # sweeps are weak-scaled: every rank runs the full grid on its own seed block
+        # weak scaling (opt-in): every rank runs the full grid on its own seed block
         seeds = inputs.seeds(cfg.n_seeds, sweep_seed_offset(cfg.n_seeds, rank, cfg.seed_offset))
     n_seeds_local = len(seeds)
-    n_cfg = len(cfg.knobs)
+    n_cfg = len(knobs_local)
     N = cfg.segment_len + cfg.warmup_len
     seeds_t = sim.seeds_tensor(seeds, device=dev)
     if args.workload == "c4":
@@ -259,7 +292,7 @@ def main():
         cands = S.candidates(space, cfg.knobs[0], n_cfg)
         state = S.climb_state(cfg.knobs[0])
     else:
-        cands = sim.knobs_tensor(cfg.knobs, device=dev)
+        cands = sim.knobs_tensor(knobs_local, device=dev)
     R = n_cfg * n_seeds_local
     out = S.alloc_outputs(R, detail=True, stats=True)
     agg = torch.empty((n_cfg, 32), dtype=torch.uint8, device=dev)
@@ -270,7 +303,8 @@ def main():
     k1_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     st_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     # K0 count + K0 classify + K1 simulate + K1b select + K2 aggregate (+ K2b for N>1 sweeps, K3 for the climb)
-    launches_per_step = 5 + (1 if (world > 1 and args.workload != "c4") else 0) + (1 if args.workload == "c4" else 0)
+    launches_per_step = 5 + (1 if (world > 1 and args.workload != "c4" and not strong) else 0) + \
+        (1 if args.workload == "c4" else 0)
     if any(w.get("batching", 0) for w in cfg.workloads):
         launches_per_step += 1                                          # K1c (continuous batching)
 
@@ -278,6 +312,9 @@ def main():
     xchg, exchange_desc = None, None
     if world > 1:
         exchange_desc = "nccl all_gather_into_tensor"
+        if args.exchange == "p2p" and strong and args.workload != "c4":
+            args.exchange = "nccl"           # config shards are concatenated, not summed: the gather is NCCL's
+            exchange_desc = "nccl all_gather_into_tensor (config-sharded: p2p windows sum parts, not gather)"
         if args.exchange == "p2p":
             try:
                 from paper_2603_11340_b200.dist import PeerExchange
@@ -293,6 +330,7 @@ def main():
                                                           or args.exchange == "p2p"):
         from paper_2603_11340_b200.dist import ClimbGraph
         graph = ClimbGraph(S, cfg, seeds, n_cand=n_cfg, exchange=args.exchange).capture()   # one graph per step
+        out_eager = out                                                 # (the untimed per-kernel profile pass)
         out = graph.out                                                 # (replayed on the current stream)
         launches_per_step = 6 + (1 if graph.xchg is not None else 0)    # K0 x2, K1, K1b, K2 (K2x+K2w), K3
 
@@ -323,8 +361,10 @@ def main():
                 dist.all_gather(list(parts.view(world, n_cfg, 32).unbind(0)), agg)
         if args.workload == "c4":                                    # K3 sums the per-rank parts itself
             S.hillclimb_step(space, sp, cands, parts if world > 1 else agg, world, state, stream=stream)
-        elif world > 1:
+        elif world > 1 and not strong:
             S.aggregate_reduce(parts, world, n_cfg, out=pooled, stream=stream)
+        # (strong sweeps: `parts` is the whole grid's aggregate table, rank-major: config c at row
+        #  (c mod world) * n_cfg + c div world)
         if i is not None:
             st_end[i].record(stream)
 
@@ -332,11 +372,21 @@ def main():
         step()
     torch.cuda.synchronize()
     stats = sim.unpack(out["stats"], STATS_DTYPE)[0]       # work of one step (the last warm-up)
+    # simulated requests per step, counted by the kernels (invalid / padding records simulate nothing)
+    req_local = int(stats["requests"])
+    if world > 1:
+        tr = torch.tensor([req_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(tr)
+        req_all = int(tr.item())
+    else:
+        req_all = req_local
 
     clocks = Clocks(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if graph is None:
+        S.profile(True)            # per-kernel CUDA events on the timed launches themselves (roofline below)
     clocks.start()
     for i in range(args.steps):
         flush.zero_()                                       # L2 flush between timed steps (not timed)
@@ -354,23 +404,39 @@ def main():
         te = torch.tensor([extended], dtype=torch.int64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         extended = int(te.item())
+    prof = None
+    if graph is None:
+        prof = S.profile_read()    # exactly the timed steps' K0 / simulation / K1b launches
+        S.profile(False)
     for _ in range(extended):
         step()
     torch.cuda.synchronize()
     clk = clocks.stop()
+    if graph is not None:
+        # the graph's launches record no events: time the same kernels on the same candidates eagerly
+        gc = graph.evaluated
+        S.run_batch(gc, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out_eager, stream=stream)
+        torch.cuda.synchronize()
+        S.profile(True)
+        for _ in range(args.steps):
+            flush.zero_()
+            S.run_batch(gc, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out_eager, stream=stream)
+        prof = S.profile_read()
+        S.profile(False)
     if clk is not None and extended:
         clk["untimed_load_steps_for_sampling"] = extended
     step_ms = [k1_start[i].elapsed_time(st_end[i]) for i in range(args.steps)]
     k1_ms = [k1_start[i].elapsed_time(k1_end[i]) for i in range(args.steps)]
     t_total = sum(step_ms) / 1000.0
-    t_k1 = sum(k1_ms) / 1000.0
+    t_k1 = sum(k1_ms) / 1000.0                         # the whole run call (K0 + simulation + K1b)
+    t_sim = prof["sim_ms"] / 1000.0                    # the simulation kernels alone (K1 / K1t / K1c)
+    t_k1b = prof["k1b_ms"] / 1000.0
     if world > 1:
-        tt = torch.tensor([t_total, t_k1], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_total, t_k1, t_sim, t_k1b], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_total, t_k1 = tt.tolist()
+        t_total, t_k1, t_sim, t_k1b = tt.tolist()
 
-    req_per_step = R * N
-    value = world * req_per_step * args.steps / t_total
+    value = req_all * args.steps / t_total
 
     # ---- e2e: the public API on HOST buffers (pinned), H2D + D2H inside the timed region
     if graph is not None:
@@ -389,7 +455,7 @@ def main():
         h2d = (h_c.numel() + h_s.numel()) / e2e_steps
         d2h = h_s.numel()
     else:
-        hk = sim.knobs_tensor(cfg.knobs if args.workload != "c4" else sim.unpack_knobs(cands.cpu().numpy()),
+        hk = sim.knobs_tensor(knobs_local if args.workload != "c4" else sim.unpack_knobs(cands.cpu().numpy()),
                               device="cpu").pin_memory()
         hs = sim.seeds_tensor(seeds, device="cpu").pin_memory()
         hout = dict(p99_us=torch.empty(R, dtype=torch.int32).pin_memory(),
@@ -408,7 +474,7 @@ def main():
         te = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         t_e2e = te.item()
-    e2e = {"value": world * req_per_step * e2e_steps / t_e2e, "unit": "requests/s",
+    e2e = {"value": req_all * e2e_steps / t_e2e, "unit": "requests/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     if graph is not None:
         e2e["api"] = "dist.ClimbGraph.run_host: climb trajectory read back every step"
@@ -416,14 +482,14 @@ def main():
     # K5 (supplementary, untimed): the Pareto front of this step's per-config aggregates
     pareto = None
     if args.workload != "c4":
-        src = pooled if world > 1 else S.aggregate(out["detail"], n_cfg, n_seeds_local)
+        src = (parts if strong else pooled) if world > 1 else S.aggregate(out["detail"], n_cfg, n_seeds_local)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         S.pareto_front(src, count=True)
         e0.record(stream)
         _, cnt = S.pareto_front(src, count=True)
         e1.record(stream)
         e1.synchronize()
-        pareto = {"configs": n_cfg, "on_front": int(cnt.item()), "ms": e0.elapsed_time(e1)}
+        pareto = {"configs": len(cfg.knobs), "on_front": int(cnt.item()), "ms": e0.elapsed_time(e1)}
     x_err = 0
     if world > 1:
         xo = xchg if xchg is not None else (graph.xchg if graph is not None else None)
@@ -435,7 +501,8 @@ def main():
         pk = peaks()
         blocks = int(stats["philox_blocks"])
         peak_gops = 148 * 4 * 32 * pk["sm_max_mhz"] * 1e6 / 1e9      # lane-ops/s at 1 warp-instr/clk/SMSP
-        achieved_gops = blocks * OPS_PER_PHILOX_BLOCK / (t_k1 / args.steps) / 1e9
+        # the dominant kernel's own time: the simulation kernels' CUDA events over the timed launches
+        achieved_gops = blocks * OPS_PER_PHILOX_BLOCK / (t_sim / args.steps) / 1e9
         # K4: measured Philox4x32-10 throughput of this GPU at full occupancy (untimed, after the run)
         rng_peak_gops = S.philox_peak() * OPS_PER_PHILOX_BLOCK / 1e9
         traffic = None
@@ -449,9 +516,9 @@ def main():
         issue_util = None
         try:
             import glob
-            pat = "r01_k1c_v*_c2c_ncu.json" if args.workload == "c2c" else "r01_k1_v*_c2_ncu.json"
+            pat = "r0*_k1c_v*_c2c_ncu.json" if args.workload == "c2c" else "r0*_k1_v*_c2_ncu.json"
             fs = sorted(glob.glob(os.path.join(ROOT, "profiles", pat)),
-                        key=lambda f: int(f.rsplit("_v", 1)[1].split("_")[0]))
+                        key=lambda f: (os.path.basename(f)[:3], int(f.rsplit("_v", 1)[1].split("_")[0])))
             if fs:
                 with open(fs[-1]) as fh:
                     m = json.load(fh)["metrics"]
@@ -461,33 +528,37 @@ def main():
             issue_util = None
         hbm = None
         if traffic:
-            gbs = traffic / (t_k1 / args.steps) / 1e9
+            gbs = traffic / (t_sim / args.steps) / 1e9
             hbm = {"gb_per_s": gbs, "peak_gb_per_s": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
         line = {
             "metric": "simulated requests/s", "value": value, "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.workload == "c4" else "weak",
+            "higher_is_better": True, "scaling": "strong" if (strong or args.workload == "c4") else "weak",
             "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded Philox streams; LL/STRESS presets of DESIGN.md §5)",
             "config": {"workload": DESCR[args.workload], "replicas_per_gpu": R, "requests_per_replica": N,
-                       "requests_per_step_per_gpu": req_per_step, "preset": "STRESS" if args.workload.startswith("c5") else "LL",
+                       "requests_per_step": req_all, "preset": "STRESS" if args.workload.startswith("c5") else "LL",
                        "l2": "flushed between timed steps (256 MiB write, untimed); inputs are < 1 MB",
-                       "parallelism": f"dp{world} over replicas ({'seed-sharded climb' if args.workload == 'c4' else 'weak: full grid, per-rank seed block'})",
+                       "parallelism": f"dp{world} over replicas ({'seed-sharded climb' if args.workload == 'c4' else ('config-sharded: config c on rank c mod N, all seeds local' if strong else 'weak: full grid, per-rank seed block')})",
                        "exchange": exchange_desc,
                        "launch": {"blocks_per_sm": info["blocks_per_sm"], "warps_per_block": info["warps_per_block"],
                                   "regs_per_thread": info["regs_per_thread"]}},
-            "replica_segments_per_s": world * R * args.steps / t_total,
-            "k1_ms_per_step": 1000.0 * t_k1 / args.steps,
+            "replica_segments_per_s": (req_all // N) * args.steps / t_total,
+            "run_ms_per_step": 1000.0 * t_k1 / args.steps,
+            "kernel_ms_per_step": {"simulate": 1000.0 * t_sim / args.steps, "k1b_select": 1000.0 * t_k1b / args.steps,
+                                   "source": "CUDA events around each launch (slo_sim_profile) on the launching "
+                                             "stream, " + ("the timed launches" if graph is None else
+                                                           "an eager replay of the graph's launches")},
             "work_per_step_per_gpu": {"philox_blocks": blocks, "batches": int(stats["batches"]),
                                       "member_steps": int(stats["member_steps"]),
                                       "decode_steps": int(stats["decode_steps"])},
             "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
                          "frac": achieved_gops / peak_gops, "traffic": traffic,
+                         "dominant_kernel_share_of_step": t_sim / t_total,
                          "issue_util_ncu": issue_util, "hbm": hbm,
-                         "kernel": ("slo_sim_run_batch = K0 classify + K1c continuous-batching simulate + K1b p99 "
-                                    "select (K1c dominates)" if args.workload == "c2c" else
-                                    "slo_sim_run_batch = K0 classify + K1 simulate + K1b p99 select (K1 dominates, "
-                                    "see profiles/ launch list)"),
+                         "kernel": ("K1c slo_sim_cont_kernel_t (continuous-batching simulation), its own CUDA-event "
+                                    "time" if args.workload == "c2c" else
+                                    "K1 slo_sim_kernel_t (static-batching simulation), its own CUDA-event time"),
                          "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
                                  "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)",
                          "measured_rng_peak": rng_peak_gops,
@@ -502,15 +573,21 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             v, cores, reps, reqs, dt = cpu_oracle_sample(cfg, budget_s=args.cpu_budget)
+            v1, reps1, reqs1, dt1 = cpu_oracle_1core(cfg, budget_s=max(3.0, args.cpu_budget / 2))
             line["cpu_baseline"] = {"value": v, "unit": "requests/s", "cores": cores, "kind": "oracle",
                                     "sample": f"{reps} replicas ({reqs} requests) of {args.workload.upper()} in "
-                                              f"seed-major order, {dt:.1f} s on {cores} worker processes"}
+                                              f"seed-major order, {dt:.1f} s on {cores} worker processes",
+                                    "value_1core": v1,
+                                    "sample_1core": f"{reps1} replicas ({reqs1} requests), same order, {dt1:.1f} s "
+                                                    f"in one process (1 core)"}
         print(json.dumps(line))
     if world > 1:
         dist.barrier()                         # no rank still reads a peer window
         for xo in (xchg, graph.xchg if graph is not None else None):
             if xo is not None:
                 xo.close()
+    if graph is not None:
+        graph.close()
     S.close()
     if world > 1:
         dist.destroy_process_group()

@@ -43,12 +43,13 @@ typedef int32_t slo_status;
 
 typedef struct slo_sim slo_sim; /* opaque: one CUDA device, owns scratch and the copied workload tables */
 
-/* Integer microsecond timing block.  Each value must be < 2^20.       */
+/* Integer microsecond timing block.  Each value must be < 2^20 and the     */
+/* worst-case step (gamma = 16, W = 4, n = 32) < 2^31 us, else slo_sim_create returns SLO_E_INVAL.        */
 typedef struct {
   uint32_t pre_base_us, pre_tok_us;             /* prefill = f * (pre_base + pre_tok * max P) / 1e6      */
   uint32_t dec_base_us, dec_seq_us;             /* plain step  d(n) = dec_base + dec_seq * n             */
-  uint32_t dr_base_us, dr_seq_us;               /* spec step   d(n) = g*(dr_base + dr_seq*n) + ver_base   */
-  uint32_t ver_base_us, ver_seq_us, ver_tok_us; /*                    + ver_seq*n + ver_tok*(g+1)*n      */
+  uint32_t dr_base_us, dr_seq_us;               /* spec step   d(n) = g*W*(dr_base + dr_seq*n) + ver_base */
+  uint32_t ver_base_us, ver_seq_us, ver_tok_us; /*            + ver_seq*n + ver_tok*(W*g+1)*n (R10, R28)  */
   uint32_t noise_step_ppm;                      /* per-batch Irwin-Hall noise step, <= 1960; 0 = none    */
 } slo_timing;                                   /* 40 B */
 
@@ -168,7 +169,10 @@ typedef struct {
    * the first measured completion t* with >= stop_min_completions measured completions and
    * t* - t0 >= stop_min_time_us; only requests completing by t* count (n_measured varies), later ones
    * store latency UINT32_MAX; flags bit 2 if the segment's requests ran out first.  Work counters then
-   * count what was simulated up to the stop. */
+   * count what was simulated up to the stop.  The kernels stop simulating at t*, which is exact only if no
+   * later batch or iteration can also end at t*: with a stop rule every workload must have
+   * pre_base + pre_tok >= 3 and dec_base + dec_seq >= 3 and ver_base + ver_seq + ver_tok >= 3 (every batch and
+   * iteration then lasts >= 1 us under any noise factor >= 0.4004), else SLO_E_INVAL. */
   uint32_t stop_min_completions, stop_min_time_us;
   uint32_t reserved[2];         /* must be 0                                                              */
 } slo_run_args;
@@ -281,6 +285,33 @@ slo_status slo_pareto_front(slo_sim* h, const slo_config_agg* d_agg, uint32_t n_
  * into d_sink[thread] (so nothing is dead code); blocks drawn = sm_count * 2048 * iters.  The caller times
  * it on `stream` (bench.py reports blocks/s next to the simulator's).  d_sink: >= sm_count * 2048 u32. */
 slo_status slo_philox_peak(slo_sim* h, uint32_t iters, uint32_t* d_sink, void* stream);
+
+/* Measurement hook (bench.py's per-kernel roofline): while enabled, every run call records CUDA events on its
+ * stream around each launch chunk's K0 (classify), simulation kernels (K1 / K1t / K1c) and K1b (select);
+ * slo_sim_profile_read waits for them and returns the summed elapsed milliseconds h_ms[0..2] = (K0, simulation,
+ * K1b) and the number of chunks, then clears the marks.  Calls made while the stream is being captured into a
+ * CUDA graph record nothing.  Errors: SLO_E_INVAL (null), SLO_E_CUDA. */
+slo_status slo_sim_profile(slo_sim* h, uint32_t enable);
+slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks);
+
+/* K6 (test instrumentation): exhaustive self-test of the integer transforms the simulation kernels use —
+ * the SAME device functions, over all 2^32 inputs (SURVEY §8(c) pins table) — so tests can compare them with
+ * the oracle (E_q) and with exact closed forms (lengths, acceptance, noise).  `what`:
+ *   SLO_SELFTEST_EXP    : d_out[b] (b < 4096) = sum over u in [b 2^20, (b+1) 2^20) of
+ *                         (E_q(u) ^ (u * 0x9E3779B97F4A7C15)) * 0xBF58476D1CE4E5B9 mod 2^64;
+ *                         d_out[4096] = #{u : E_q(u) > E_q(u - 1)}.  out_len >= 4097.
+ *   SLO_SELFTEST_LENGTH : workload arg0, table arg1 (0 prompt, 1 output): d_out[l - lo] =
+ *                         #{u : length(u) = l} for l = lo .. lo + ncw; d_out[ncw + 1] = #{u : length(u) <
+ *                         length(u - 1)} + out-of-range values.  out_len >= ncw + 2.
+ *   SLO_SELFTEST_ACCEPT : accept_q16 arg0, draft_width arg1, gamma arg2: d_out[A] = #{u : A(u) =
+ *                         A}, A = 0..16; d_out[17] = #{u : A(u) > A(u - 1)}.  out_len >= 18.
+ *   SLO_SELFTEST_NOISE  : noise_step_ppm arg0: d_out[k] = #{w : f(w) = 10^6 + (k - 510) arg0},
+ *                         k = 0..1020; d_out[1021] = #{w : f(w) off that lattice}.  out_len >= 1022.
+ * d_out (device, u64) is zeroed by the call; results are valid after `stream` completes.
+ * Errors: SLO_E_INVAL (null pointers, unknown `what`, bad arguments, short out_len), SLO_E_CUDA. */
+enum { SLO_SELFTEST_EXP = 0, SLO_SELFTEST_LENGTH = 1, SLO_SELFTEST_ACCEPT = 2, SLO_SELFTEST_NOISE = 3 };
+slo_status slo_selftest_transforms(slo_sim* h, uint32_t what, uint32_t arg0, uint32_t arg1, uint32_t arg2,
+                                   uint64_t* d_out, uint32_t out_len, void* stream);
 
 const char* slo_status_string(slo_status s);
 const char* slo_last_error(const slo_sim* h); /* detail of the last failing call on h (NULL h: global) */

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "slo_internal.h"
@@ -31,6 +32,7 @@ struct slo_sim {
   bool any_cont_think = false;      // a continuous-batching workload has think time: launch K1c on lists 9-11
   bool any_cont_plain = false;      // a continuous-batching workload without think time: K1c on lists 3-5
   uint32_t group_policy = 0;        // slo_sim_opts.group_policy
+  std::vector<slo::DevWorkload> h_wl;  // host copy of the device workload descriptors
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
   uint32_t* d_ctl = nullptr;        // [slo::kCtlWords]: list lengths, K1 cursors, K0 bucket counts/cursors
@@ -48,6 +50,11 @@ struct slo_sim {
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
   int regs = 0;
+  bool pinned = false;              // scratch referenced by a captured CUDA graph: never regrown (ensure())
+  // measurement hook (slo_sim_profile): events around each chunk's K0 | simulation kernels | K1b
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_free;             // recycled events
+  std::vector<std::array<cudaEvent_t, 4>> ev_marks;  // recorded, not yet read
   std::string err;
 };
 
@@ -108,10 +115,17 @@ bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
 
 }  // namespace
 
-// grow-only device scratch owned by the handle (callers synchronise before a regrow)
+// grow-only device scratch owned by the handle (callers synchronise before a regrow).  A call made while `st`
+// is being captured into a CUDA graph pins the handle's scratch: the graph holds its pointers, so every later
+// call that would regrow (free + reallocate) the scratch is refused instead of leaving the graph dangling.
 template <typename T>
 slo_status ensure(slo_sim* h, T*& ptr, size_t& cap, size_t need, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) h->pinned = true;
   if (need <= cap) return SLO_OK;
+  if (h->pinned)
+    return fail(h, SLO_E_RANGE, "scratch of %zu B needed, but this handle's scratch is held by a captured CUDA graph "
+                "(use a separate handle for larger runs)", need * sizeof(T));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   if (ptr) cudaFree(ptr);
   ptr = nullptr;
@@ -182,6 +196,15 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     for (int i = 0; i < 9; ++i)
       if (tv[i] >= (1u << 20)) return fail(nullptr, SLO_E_INVAL, "workload %u: timing value >= 2^20", w);
     if (x.timing.noise_step_ppm > 1960) return fail(nullptr, SLO_E_INVAL, "workload %u: noise_step_ppm > 1960", w);
+    {   // worst-case decode step d(n) over gamma <= 16, W <= 4, n <= 32 (R10, R28) must stay below 2^31 us: K1c
+        // keeps a step's duration in 32 bits
+      const slo_timing& t = x.timing;
+      const uint64_t dmax_spec = 64ull * (t.dr_base_us + 32ull * t.dr_seq_us) + t.ver_base_us + 32ull * t.ver_seq_us +
+                                 65ull * 32ull * t.ver_tok_us;
+      const uint64_t dmax_plain = t.dec_base_us + 32ull * t.dec_seq_us;
+      if (dmax_spec >= (1ull << 31) || dmax_plain >= (1ull << 31))
+        return fail(nullptr, SLO_E_INVAL, "workload %u: worst-case decode step cost >= 2^31 us", w);
+    }
     if (x.batching > 1) return fail(nullptr, SLO_E_INVAL, "workload %u: batching must be 0 or 1", w);
     slo::DevWorkload& d = hw[w];
     memset(&d, 0, sizeof d);
@@ -213,8 +236,10 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
     return fail(nullptr, SLO_E_DEVICE, "create: no CUDA device %d", device);
   cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10)
-    return fail(nullptr, SLO_E_DEVICE, "create: device %d is not sm_100", device);
+  // the library carries sm_100a SASS only (no PTX): any other architecture could create a handle but fail
+  // every launch with "no kernel image", so it is refused here
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, SLO_E_DEVICE, "create: device %d is not sm_100 (B200)", device);
   DeviceGuard g(device);
 
   slo_sim* h = new (std::nothrow) slo_sim();
@@ -233,8 +258,14 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
   if (o.scratch_mb) h->lat_budget = (size_t)o.scratch_mb << 20;
   h->group_policy = o.group_policy;
+  h->h_wl = hw;
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel_t<false>) == cudaSuccess) h->regs = fa.numRegs;
+  if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel_t<false>) != cudaSuccess) {
+    cudaGetLastError();
+    slo_sim_destroy(h);
+    return fail(nullptr, SLO_E_DEVICE, "create: no sm_100a kernel image for device %d", device);
+  }
+  h->regs = fa.numRegs;
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
@@ -252,6 +283,30 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   return SLO_OK;
 }
 
+slo_status slo_sim_profile(slo_sim* h, uint32_t enable) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "profile: null handle");
+  h->profile = enable != 0;
+  return SLO_OK;
+}
+
+slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks) {
+  if (!h || !h_ms) return fail(h, SLO_E_INVAL, "profile_read: null argument");
+  DeviceGuard g(h->device);
+  h_ms[0] = h_ms[1] = h_ms[2] = 0.0;
+  for (auto& m : h->ev_marks) {
+    CUDA_TRY(h, cudaEventSynchronize(m[3]));
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.0f;
+      CUDA_TRY(h, cudaEventElapsedTime(&ms, m[i], m[i + 1]));
+      h_ms[i] += ms;
+    }
+    for (int i = 0; i < 4; ++i) h->ev_free.push_back(m[i]);
+  }
+  if (h_chunks) *h_chunks = (uint32_t)h->ev_marks.size();
+  h->ev_marks.clear();
+  return SLO_OK;
+}
+
 slo_status slo_sim_destroy(slo_sim* h) {
   if (!h) return SLO_OK;
   {
@@ -265,6 +320,9 @@ slo_status slo_sim_destroy(slo_sim* h) {
     if (h->d_part) cudaFree(h->d_part);
     if (h->d_scratch) cudaFree(h->d_scratch);
     if (h->d_pareto) cudaFree(h->d_pareto);
+    for (auto& m : h->ev_marks)
+      for (cudaEvent_t e : m) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_free) cudaEventDestroy(e);
   }
   delete h;
   return SLO_OK;
@@ -383,12 +441,32 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   const uint32_t sel_vals = 0u;
   const size_t sel_smem = (256u + sel_vals) * sizeof(uint32_t);
   if (d_stats) CUDA_TRY(h, cudaMemsetAsync(d_stats, 0, sizeof(slo_stats), st));
+  bool prof = h->profile;
+  if (prof) {                                     // no event marks inside a graph capture
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) prof = false;
+  }
+  std::array<cudaEvent_t, 4> ev{};
+  auto mark = [&](int i) -> slo_status {
+    if (!prof) return SLO_OK;
+    if (h->ev_free.empty()) {
+      cudaEvent_t e;
+      CUDA_TRY(h, cudaEventCreate(&e));
+      h->ev_free.push_back(e);
+    }
+    ev[i] = h->ev_free.back();
+    h->ev_free.pop_back();
+    CUDA_TRY(h, cudaEventRecord(ev[i], st));
+    if (i == 3) h->ev_marks.push_back(ev);
+    return SLO_OK;
+  };
   for (uint64_t r0 = 0; r0 < n_rep; r0 += chunk) {
     const uint32_t nc = (uint32_t)((n_rep - r0) < chunk ? (n_rep - r0) : chunk);
     p.r_base = (uint32_t)r0;
     p.n_chunk = nc;
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
+    if ((s = mark(0)) != SLO_OK) return s;
     CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * slo::kCtlWords, st));
     // lane groups: narrow (G >= min(C, B), up to four replicas per warp) by default — measured best from
     // 512-replica climb steps (one 8-GPU rank of C4) up to the full sweeps; a chunk of at most one replica per
@@ -403,6 +481,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc, h->n_wl,
                                                               wide, h->d_ctl, h->d_lists);
     CUDA_TRY(h, cudaGetLastError());
+    if ((s = mark(1)) != SLO_OK) return s;
     uint64_t blocks = (uint64_t)bps * h->sm_count;
     const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);
     if (blocks > need) blocks = need;
@@ -436,9 +515,11 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                               : slo::slo_sim_cont_kernel_t<false, false><<<cg, cb, cont_smem, st>>>(pc);
       CUDA_TRY(h, cudaGetLastError());
     }
+    if ((s = mark(2)) != SLO_OK) return s;
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
     slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
     CUDA_TRY(h, cudaGetLastError());
+    if ((s = mark(3)) != SLO_OK) return s;
   }
   return SLO_OK;
 }
@@ -462,6 +543,17 @@ slo_status slo_sim_run(slo_sim* h, const slo_run_args* a, void* stream) {
     if (a->reserved[i]) return fail(h, SLO_E_INVAL, "run: reserved must be 0");
   slo_status s = check_run_args(h, a->n_configs, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us);
   if (s != SLO_OK) return s;
+  if (a->stop_min_completions || a->stop_min_time_us) {
+    // the kernels end a replica at t*: exact only if nothing else can complete at t* after it, i.e. every batch
+    // / iteration lasts >= 1 us.  floor(f x / 10^6) >= 1 for x >= 3 and f >= 10^6 - 510 * 1960 = 400,400 ppm.
+    for (uint32_t w = 0; w < h->n_wl; ++w) {
+      const slo_timing& t = h->h_wl[w].t;
+      if ((uint64_t)t.pre_base_us + t.pre_tok_us < 3 || (uint64_t)t.dec_base_us + t.dec_seq_us < 3 ||
+          (uint64_t)t.ver_base_us + t.ver_seq_us + t.ver_tok_us < 3)
+        return fail(h, SLO_E_INVAL, "run: a stop rule needs every batch and iteration to last >= 1 us (workload %u "
+                    "allows a zero-duration one)", w);
+    }
+  }
   DeviceGuard g(h->device);
   return launch_sim(h, a->d_configs, a->n_configs, a->d_seeds, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us,
                     a->d_p99_us, a->d_goodput, a->d_detail, a->d_latencies, a->d_stats, a->d_p50_us, a->d_p95_us,
@@ -637,7 +729,12 @@ slo_status slo_exchange_open(slo_exchange* x, const void* h_handles) {
     memcpy(&hd, hb + (size_t)r * SLO_EXCHANGE_HANDLE_BYTES, sizeof hd);
     void* p = nullptr;
     const cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) return fail(x->h, SLO_E_CUDA, "exchange_open: rank %u: %s", r, cudaGetErrorString(e));
+    if (e != cudaSuccess) {       // unmap what this call mapped so a retry starts clean (no leaked mappings)
+      for (uint32_t q = 0; q < r; ++q)
+        if (q != x->rank && x->h_peers[q]) cudaIpcCloseMemHandle(x->h_peers[q]);
+      for (uint32_t q = 0; q < x->world; ++q) x->h_peers[q] = nullptr;
+      return fail(x->h, SLO_E_CUDA, "exchange_open: rank %u: %s", r, cudaGetErrorString(e));
+    }
     x->h_peers[r] = static_cast<char*>(p);
   }
   CUDA_TRY(x->h, cudaMemcpy(x->d_peers, x->h_peers, sizeof(char*) * slo::kXMaxRanks, cudaMemcpyHostToDevice));
@@ -681,6 +778,55 @@ slo_status slo_philox_peak(slo_sim* h, uint32_t iters, uint32_t* d_sink, void* s
   if (!h || !d_sink || iters == 0) return fail(h, SLO_E_INVAL, "philox_peak: bad arguments");
   DeviceGuard g(h->device);
   slo::slo_philox_peak_kernel<<<(unsigned)h->sm_count * 8u, 256, 0, (cudaStream_t)stream>>>(iters, d_sink);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+slo_status slo_selftest_transforms(slo_sim* h, uint32_t what, uint32_t arg0, uint32_t arg1, uint32_t arg2,
+                                   uint64_t* d_out, uint32_t out_len, void* stream) {
+  if (!h || !d_out) return fail(h, SLO_E_INVAL, "selftest: null argument");
+  slo::SelftestArgs a{};
+  a.what = what;
+  a.arg0 = arg0;
+  a.arg1 = arg1;
+  a.arg2 = arg2;
+  uint32_t need = 0;
+  switch (what) {
+    case SLO_SELFTEST_EXP:
+      need = 4097;
+      break;
+    case SLO_SELFTEST_LENGTH: {
+      if (arg0 >= h->n_wl || arg1 > 1) return fail(h, SLO_E_INVAL, "selftest: bad workload / table");
+      const slo::DevWorkload& w = h->h_wl[arg0];
+      a.off = arg1 ? w.o_off : w.p_off;
+      a.goff = arg1 ? w.o_goff : w.p_goff;
+      a.lo = arg1 ? w.o_lo : w.p_lo;
+      a.nbins = (arg1 ? w.o_ncw : w.p_ncw) + 1;
+      a.viol_slot = a.nbins;
+      need = a.nbins + 1;
+      break;
+    }
+    case SLO_SELFTEST_ACCEPT:
+      if (arg0 > 65536 || arg1 < 1 || arg1 > 4 || arg2 > 16) return fail(h, SLO_E_INVAL, "selftest: bad acceptance");
+      a.nbins = 17;
+      a.viol_slot = 17;
+      need = 18;
+      break;
+    case SLO_SELFTEST_NOISE:
+      if (arg0 > 1960) return fail(h, SLO_E_INVAL, "selftest: noise step > 1960");
+      a.nbins = 1021;
+      a.viol_slot = 1021;
+      need = 1022;
+      break;
+    default:
+      return fail(h, SLO_E_INVAL, "selftest: unknown what %u", what);
+  }
+  if (out_len < need) return fail(h, SLO_E_INVAL, "selftest: out_len %u < %u", out_len, need);
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(h, cudaMemsetAsync(d_out, 0, (size_t)need * sizeof(uint64_t), st));
+  const size_t smem = (size_t)a.nbins * sizeof(uint32_t);
+  slo::slo_selftest_kernel<<<4096, 256, smem, st>>>(a, h->d_tables, d_out);
   CUDA_TRY(h, cudaGetLastError());
   return SLO_OK;
 }

@@ -93,6 +93,73 @@ __device__ __forceinline__ uint32_t length_guided(const uint32_t* __restrict__ t
   return lo + base;
 }
 
+// ---- acceptance: thresholds T_a - 1 (a = 1..gp, gp = the last a with T_a > 0) and the
+// 256-entry bucket guide (A at the top of bucket u >> 24, | 0x80 if a threshold falls inside the bucket).
+// Used by K1/K1c's replica setup and by the exhaustive self-test (K6), so both run the same code.
+__device__ __forceinline__ uint32_t accept_thresholds(uint32_t accept_q16, uint32_t width, uint32_t gamma,
+                                                      uint32_t* tm1, bool write) {
+  uint64_t rr = 65536;
+  for (uint32_t w = 0; w < width; ++w) rr = (rr * (65536u - accept_q16)) >> 16;
+  const uint64_t ae = 65536u - rr;
+  uint64_t prev = 1ull << 32;
+  uint32_t gp = 0;
+  for (uint32_t a = 1; a <= gamma; ++a) {
+    prev = (prev * ae) >> 16;
+    if (prev > 0) {
+      if (write) tm1[a - 1] = (uint32_t)(prev - 1);
+      gp = a;
+    }
+  }
+  return gp;
+}
+
+// guide entries kk = first, first + stride, ... (a group's lanes split the 256 buckets)
+__device__ __forceinline__ void accept_guide(const uint32_t* tm1, uint32_t gp, uint8_t* guide, uint32_t first,
+                                             uint32_t stride) {
+  for (uint32_t kk = first; kk < 256; kk += stride) {
+    const uint32_t lo = kk << 24, top = lo | 0xFFFFFFu;
+    uint32_t A = 0, inside = 0;
+    for (uint32_t a = 0; a < gp; ++a) {
+      const uint32_t t = tm1[a];
+      A += (top <= t);
+      inside |= (t >= lo && t < top);
+    }
+    guide[kk] = (uint8_t)(A | (inside << 7));
+  }
+}
+
+// A(u) = #{a in [1, gp] : u < T_a} through the bucket guide
+__device__ __forceinline__ uint32_t accepted_guided(const uint8_t* guide, const uint32_t* tm1, uint32_t u,
+                                                    uint32_t gp) {
+  const uint32_t g = guide[u >> 24];
+  uint32_t A = g & 0x7Fu;
+  if (g & 0x80u) {
+    while (A < gp && u <= tm1[A]) ++A;
+  }
+  return A;
+}
+
+// ---- decode step cost d(n) = alpha0 + alpha1 n (R10 factorised by R28: W draft branches of
+// gamma tokens, W gamma + 1 verified tokens per sequence)
+__device__ __forceinline__ void step_coeffs(const slo_timing& t, uint32_t gamma, uint32_t width, uint64_t& alpha0,
+                                            uint64_t& alpha1) {
+  if (gamma == 0) {
+    alpha0 = t.dec_base_us;
+    alpha1 = t.dec_seq_us;
+  } else {
+    const uint64_t drafted = (uint64_t)gamma * width;
+    alpha0 = drafted * t.dr_base_us + t.ver_base_us;
+    alpha1 = drafted * t.dr_seq_us + t.ver_seq_us + (uint64_t)t.ver_tok_us * (drafted + 1);
+  }
+}
+
+// ---- batch noise factor: f = 10^6 + (b0 + b1 + b2 + b3 - 510) step ppm of a word's bytes
+// (step <= 1960, so f > 0); the head's w3 for a static batch or a prefill, an ITER word for a decode iteration
+__device__ __forceinline__ uint32_t noise_factor(uint32_t w, uint32_t step) {
+  const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
+  return (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)step);
+}
+
 // ---- FNV-1a-32 of the 32 knob bytes (independent key mode)
 __host__ __device__ inline uint32_t fnv1a_knobs(const slo_knobs& k) {
   uint8_t b[32];

@@ -81,6 +81,12 @@ __global__ void slo_exchange_wait_kernel(const char* window, uint32_t n_cfg, uin
                                          slo_config_agg* out);
 
 __global__ void slo_philox_peak_kernel(uint32_t iters, uint32_t* sink);   // K4: RNG roofline
+// K6 exhaustive transform self-test (slo_selftest.cu): what 0 E_q, 1 a length table, 2 A(u), 3 noise factor
+struct SelftestArgs {
+  uint32_t what, arg0, arg1, arg2;
+  uint32_t off, goff, lo, nbins, viol_slot, pad;
+};
+__global__ void slo_selftest_kernel(SelftestArgs a, const uint32_t* tables, uint64_t* out);
 // K5 Pareto front (slo_pareto.cu): scratch bytes for n configs (cub temp part returned separately), launch
 size_t pareto_scratch_bytes(uint32_t n, size_t* cub_bytes_out);
 cudaError_t pareto_launch(const slo_config_agg* agg, uint32_t n, uint8_t* front, uint32_t* count, void* scratch,

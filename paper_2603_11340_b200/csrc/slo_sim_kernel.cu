@@ -124,32 +124,14 @@ struct alignas(16) Group {
 // A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
 template <class GR>
 __device__ __forceinline__ uint32_t accepted(const GR& R, uint32_t u, uint32_t gp) {
-  const uint32_t g = R.guide[u >> 24];
-  uint32_t A = g & 0x7Fu;
-  if (g & 0x80u) {
-    while (A < gp && u <= R.tm1[A]) ++A;
-  }
-  return A;
+  return accepted_guided(R.guide, R.tm1, u, gp);
 }
 
 // (a1) set up a newly acquired replica (group-convergent; other groups do not enter)
 template <int G, class GR>
 __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const slo_knobs& k, uint32_t k0,
                                               uint32_t k1, uint32_t gamma, uint32_t& gp, int li, uint32_t gmask) {
-  gp = 0;
-  {
-    uint64_t rr = 65536;
-    for (uint32_t w = 0; w < k.draft_width; ++w) rr = (rr * (65536u - k.accept_q16)) >> 16;
-    const uint64_t ae = 65536u - rr;
-    uint64_t prev = 1ull << 32;
-    for (uint32_t a = 1; a <= gamma; ++a) {
-      prev = (prev * ae) >> 16;
-      if (prev > 0) {
-        if (li == 0) R.tm1[a - 1] = (uint32_t)(prev - 1);
-        gp = a;
-      }
-    }
-  }
+  gp = accept_thresholds(k.accept_q16, k.draft_width, gamma, R.tm1, li == 0);
   if (li == 0) {
     const uint64_t g0 = W.gap_q16[0] == INF64 ? INF64 : (W.gap_q16[0] << 8) / k.rate_scale_q8;
     const uint64_t g1 = W.gap_q16[1] == INF64 ? INF64 : (W.gap_q16[1] << 8) / k.rate_scale_q8;
@@ -161,9 +143,10 @@ __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const
     R.nphase = 0;
     R.kind = W.kind;
     R.start_state = W.start_state;
-    R.alpha0 = gamma == 0 ? (uint64_t)W.t.dec_base_us : (uint64_t)gamma * W.t.dr_base_us + W.t.ver_base_us;
-    R.alpha1 = gamma == 0 ? (uint64_t)W.t.dec_seq_us
-                          : (uint64_t)gamma * W.t.dr_seq_us + W.t.ver_seq_us + (uint64_t)W.t.ver_tok_us * (gamma + 1);
+    uint64_t a0, a1;
+    step_coeffs(W.t, gamma, k.draft_width, a0, a1);     // d(n) = alpha0 + alpha1 n (R10, R28)
+    R.alpha0 = a0;
+    R.alpha1 = a1;
     R.pre_base = W.t.pre_base_us;
     R.pre_tok = W.t.pre_tok_us;
     R.noise = W.t.noise_step_ppm;
@@ -193,18 +176,7 @@ __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const
     R.stopped = 0;
   }
   __syncwarp(gmask);
-  if (gamma > 0) {  // bucket guide for A(u)
-    for (uint32_t kk = li; kk < 256; kk += G) {
-      const uint32_t lo = kk << 24, top = lo | 0xFFFFFFu;
-      uint32_t A = 0, inside = 0;
-      for (uint32_t a = 0; a < gp; ++a) {
-        const uint32_t t = R.tm1[a];
-        A += (top <= t);
-        inside |= (t >= lo && t < top);
-      }
-      R.guide[kk] = (uint8_t)(A | (inside << 7));
-    }
-  }
+  if (gamma > 0) accept_guide(R.tm1, gp, R.guide, (uint32_t)li, G);   // bucket guide for A(u)
   __syncwarp(gmask);
 }
 
@@ -487,9 +459,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     const bool spec = kn.w > 0;
 
     // ---- (a6) prefill with the head's noise factor
-    const uint32_t w3h = R.w3[h % RING];
-    const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
-    const uint64_t f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)R.noise);
+    const uint64_t f = noise_factor(R.w3[h % RING], R.noise);
     const uint32_t maxP = gmax<G>(po & 0xFFFFu);
     const uint64_t t0 = t_form + f * ((uint64_t)R.pre_base + (uint64_t)R.pre_tok * maxP) / 1000000u;
 
@@ -807,9 +777,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       // s_next = s_{nq + k} straight from the window (INF if beyond the gate); k = G: recompute at the top
       const uint64_t sn = gshfl64<G>(sj, (int)(kk & (G - 1)));
       if (pre) {
-        const uint32_t w3h = R.w3[nq % RING];
-        const uint32_t bytesum = (w3h & 0xFF) + ((w3h >> 8) & 0xFF) + ((w3h >> 16) & 0xFF) + (w3h >> 24);
-        const uint64_t f = (uint64_t)(int64_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+        const uint64_t f = noise_factor(R.w3[nq % RING], noise);
         t += f * ((uint64_t)R.pre_base + (uint64_t)R.pre_tok * maxP) / 1000000u;
         nq += kk;
         nrun += kk;
@@ -850,16 +818,12 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           if (sA < (uint32_t)(2 * G)) {
             fw = sA < (uint32_t)G ? a0 : b0;
           } else {                                       // ITER block it + li, word 0 (§2.12)
-            const uint32_t w = philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x;
-            const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
-            fw = (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+            fw = noise_factor(philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x, noise);
           }
           if (sB < (uint32_t)(2 * G)) {
             fw2 = b1;
           } else {                                       // ITER block it + G + li
-            const uint32_t w = philox(it + (uint32_t)(G + li), 3, 0, 0, k0, k1).x;
-            const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
-            fw2 = (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)noise);
+            fw2 = noise_factor(philox(it + (uint32_t)(G + li), 3, 0, 0, k0, k1).x, noise);
           }
           nzc = 0;
         }

@@ -7,8 +7,10 @@ reduced on the device by K2b (`slo_aggregate_reduce`).  Integer sums make the po
 of rank order, so every rank holds bit-identical aggregates and takes the identical climb step.
 
 Sharding rules:
-  * sweeps (C2, C3, C5): weak scaling — every rank runs the full config grid on its own seed block
-    (seed offset rank * n_seeds); pooled aggregates then cover world * n_seeds seeds per config;
+  * sweeps (C2, C3, C5), default: config-sharded — config c on rank c mod world with all its
+    seeds, one all-gather of the per-config aggregates assembles the grid (strong scaling: the BASELINE grid
+    is split, unchanged); opt-in weak scaling — every rank runs the full config grid on its own seed block
+    (seed offset rank * n_seeds), pooled aggregates then cover world * n_seeds seeds per config;
   * climb (C4): seed-sharded — the n_seeds seeds are split into contiguous per-rank blocks, so the pooled
     aggregate equals the single-GPU one exactly.
 """
@@ -32,6 +34,25 @@ def seed_block(n_seeds: int, rank: int, world_size: int) -> Tuple[int, int]:
     lo = rank * base + min(rank, extra)
     hi = lo + base + (1 if rank < extra else 0)
     return lo, hi
+
+
+def config_shard(knobs: List, rank: int, world_size: int, pad=None) -> List:
+    """Config-sharded sweep: config c goes to rank c mod world_size (round-robin balances the
+    grid's heterogeneous costs), with all of its seeds, so per-config sums stay local.  With `pad` every rank's
+    share is padded to ceil(n / world_size) records (an always-invalid record simulates nothing) so the
+    aggregate all-gather has equal parts; the gathered table is rank-major: config c at row
+    (c mod world_size) * per + c div world_size."""
+    mine = list(knobs[rank::world_size])
+    if pad is not None:
+        per = -(-len(knobs) // world_size)
+        mine += [pad] * (per - len(mine))
+    return mine
+
+
+def unshard_rows(n_cfg: int, world_size: int) -> List[int]:
+    """Row of config c in the rank-major gathered table of config_shard(pad=...) shares."""
+    per = -(-n_cfg // world_size)
+    return [(c % world_size) * per + c // world_size for c in range(n_cfg)]
 
 
 def sweep_seed_offset(n_seeds: int, rank: int, base_offset: int = 0) -> int:
@@ -97,6 +118,9 @@ class ClimbGraph:
 
     def __init__(self, sim, cfg, seeds: List[int], n_cand: int = 32, sp=None, exchange: str = "nccl"):
         from . import sim as S
+        # the graph holds pointers into its handle's scratch, so it gets a handle of its own: no other call can
+        # regrow that scratch under it (the library also refuses any regrow of a captured handle)
+        sim = sim.twin()
         self.sim, self.cfg = sim, cfg
         self.space = cfg.extra["space"]
         self.sp = dict(sp if sp is not None else cfg.extra["score"])
@@ -148,6 +172,13 @@ class ClimbGraph:
         with torch.cuda.graph(self.graph, stream=self.stream):
             self._step()
         return self
+
+    def close(self):
+        if self.xchg is not None:
+            self.xchg.close()
+            self.xchg = None
+        self.graph = None
+        self.sim.close()
 
     def run(self, steps: int):
         if self.graph is None:

@@ -109,6 +109,8 @@ class Simulator:
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
+        self.options = dict(crn=crn, warps_per_block=warps_per_block, blocks_per_sm=blocks_per_sm,
+                            scratch_mb=scratch_mb, group_policy=group_policy)
         self.workloads = list(workloads)
         n = len(self.workloads)
         arr = (_lib.slo_workload * n)()
@@ -137,6 +139,10 @@ class Simulator:
         h = C.c_void_p()
         check(lib().slo_sim_create(self.device, arr, n, C.byref(opts), C.byref(h)))
         self.h = h
+
+    def twin(self) -> "Simulator":
+        """A new handle on the same device with the same workloads and options (its own scratch)."""
+        return Simulator(self.workloads, device=self.device, **self.options)
 
     def close(self):
         if getattr(self, "h", None):
@@ -254,6 +260,26 @@ class Simulator:
         check(lib().slo_pareto_front(self.h, agg.data_ptr(), n, front.data_ptr(), _ptr(cnt), _stream_ptr(stream)),
               self.h)
         return (front, cnt) if count else front
+
+    def profile(self, enable: bool = True) -> None:
+        """Record per-kernel CUDA events around every later run (slo_sim_profile)."""
+        check(lib().slo_sim_profile(self.h, 1 if enable else 0), self.h)
+
+    def profile_read(self) -> Dict:
+        """Summed ms of the recorded runs per kernel class {k0, sim, k1b} and the chunk count; clears them."""
+        ms = (C.c_double * 3)()
+        n = C.c_uint32(0)
+        check(lib().slo_sim_profile_read(self.h, ms, C.byref(n)), self.h)
+        return {"k0_ms": ms[0], "sim_ms": ms[1], "k1b_ms": ms[2], "chunks": n.value}
+
+    def selftest(self, what: str, arg0: int = 0, arg1: int = 0, arg2: int = 0, stream=None) -> np.ndarray:
+        """K6: exhaustive 2^32-input hashes / histograms of a transform (slo_selftest_transforms), as uint64."""
+        from ._lib import SELFTEST
+        out = torch.empty(8192, dtype=torch.int64, device=torch.device("cuda", self.device))
+        check(lib().slo_selftest_transforms(self.h, SELFTEST[what], arg0, arg1, arg2, out.data_ptr(), out.numel(),
+                                            _stream_ptr(stream)), self.h)
+        torch.cuda.synchronize(self.device)
+        return out.cpu().numpy().view(np.uint64)
 
     def philox_peak(self, iters: int = 2048, repeats: int = 3) -> float:
         """K4: measured Philox4x32-10 blocks/s at full occupancy (the RNG roofline)."""

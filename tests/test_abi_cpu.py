@@ -65,6 +65,10 @@ def test_create_rejects_bad_arguments(L):
     w.arr.mean_gap_q16[0] = (1 << 64) - 1   # Poisson needs a finite gap
     assert lib.slo_sim_create(0, C.byref(w), 1, None, C.byref(h)) == -1
     w.arr.mean_gap_q16[0] = inputs.mean_gap_q16(10.0)
+    w.timing.ver_tok_us = (1 << 20) - 1  # each value < 2^20, but the worst-case step (gamma 16, W 4, n 32) >= 2^31
+    assert lib.slo_sim_create(0, C.byref(w), 1, None, C.byref(h)) == -1
+    assert b"worst-case" in lib.slo_last_error(None)
+    w.timing.ver_tok_us = 0
     w.batching = 2                     # 0 static, 1 continuous
     assert lib.slo_sim_create(0, C.byref(w), 1, None, C.byref(h)) == -1
     assert b"batching" in lib.slo_last_error(None)

@@ -103,3 +103,62 @@ def test_two_rank_pooled_climb_matches_single_process():
         _, aggs = _agg_records(oracle, cfg, cands, cfg.seeds(), cfg.segment_len)
         st, moved, idx, scores = climb.step(st, cands, aggs, sp)
         assert (moved, idx, scores, dict(st["K"])) == res[0][step]
+
+
+def test_config_shard_partition():
+    from paper_2603_11340_b200.dist import config_shard, unshard_rows
+    for n in (1, 7, 512, 1000):
+        for w in (1, 2, 3, 8):
+            shares = [config_shard(list(range(n)), r, w, pad=-1) for r in range(w)]
+            per = -(-n // w)
+            assert all(len(s) == per for s in shares)
+            table = [x for s in shares for x in s]                 # the rank-major all-gather
+            rows = unshard_rows(n, w)
+            assert [table[rows[c]] for c in range(n)] == list(range(n))
+            assert sorted(x for x in table if x >= 0) == list(range(n))
+
+
+def _sweep_worker(rank, world_size, port, q):
+    """Config-sharded sweep: config c on rank c mod world with all its seeds; the one exchange
+    is an all-gather of the per-config aggregates (padding records are invalid and simulate nothing)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        import oracle
+        from paper_2603_11340_b200.dist import config_shard
+        cfg = inputs.config_c2(n_seeds=3, segment_len=200)
+        knobs = cfg.knobs[::37]                                       # 14 configs: uneven over 2 and 3 ranks
+        mine = config_shard(knobs, rank, world_size, pad=inputs.PAD_KNOBS)
+        recs, _ = _agg_records(oracle, cfg, mine, cfg.seeds(), cfg.segment_len)
+        local = torch.from_numpy(recs.view(np.uint8).reshape(len(mine), 32).copy())
+        parts = gather_aggregates(local)
+        q.put((rank, parts.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world_size", [2, 3])
+def test_config_sharded_sweep_matches_single_process(world_size):
+    import oracle
+    from paper_2603_11340_b200.dist import unshard_rows
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, world_size, port, q)) for r in range(world_size)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(set(res.values())) == 1                              # every rank holds the same table
+    cfg = inputs.config_c2(n_seeds=3, segment_len=200)
+    knobs = cfg.knobs[::37]
+    table = np.frombuffer(res[0], dtype=AGG)
+    rows = unshard_rows(len(knobs), world_size)
+    ref, _ = _agg_records(oracle, cfg, knobs, cfg.seeds(), cfg.segment_len)
+    assert table[rows].tobytes() == ref.tobytes()                  # = the single-process grid, config order
+    pad_rows = sorted(set(range(len(table))) - set(rows))
+    assert all(int(table[r]["flags"]) & 1 for r in pad_rows)      # padding: invalid, no work

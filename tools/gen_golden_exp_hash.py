@@ -16,6 +16,7 @@ with open(path, "w") as fh:
     fh.write("# E_q (DESIGN.md §2.2) of the CPU oracle over all 2^32 inputs: block b = [b 2^20, (b+1) 2^20),\n")
     fh.write("# hash_b = sum_u (E_q(u) ^ (u * 0x9E3779B97F4A7C15)) * 0xBF58476D1CE4E5B9 mod 2^64.\n")
     fh.write("# Written by tools/gen_golden_exp_hash.py (calls only oracle/).\n")
+    fh.write(f"# nonmono {nonmono}\n")
     for b, v in enumerate(h):
         fh.write(f"{b} {v:016x}\n")
 print(f"wrote {path}: nonmono={nonmono} maxerr={maxerr:.3e}")
