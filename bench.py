@@ -202,6 +202,8 @@ def main():
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--group-policy", type=int, default=0, choices=[0, 1, 2, 3],
                     help="lane groups: 0 auto, 1 narrow G>=min(C,B), 2 wide G>=max(C,B), 3 whole warp")
+    ap.add_argument("--gen-policy", type=int, default=0, choices=[0, 1, 2],
+                    help="static batching: 0 auto, 1 inline generation in K1, 2 split K1g + K1s")
     ap.add_argument("--eager-climb", action="store_true", help="c4: host loop instead of the CUDA-graph step")
     ap.add_argument("--exchange", default="nccl", choices=["p2p", "nccl"],
                     help="N>1 aggregate exchange: nccl = K2 + all_gather_into_tensor (+ K2b / K3 summing the parts); "
@@ -209,6 +211,9 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N>1 sweeps: strong = the BASELINE grid config-sharded over ranks (SURVEY §8(e)); "
                          "weak = every rank runs the full grid on its own seed block")
+    ap.add_argument("--share-of", type=int, default=1,
+                    help="N=1 only: time rank 0's share of a W-GPU partition of the workload on this one GPU (no "
+                         "exchange) — the per-rank step of a W-GPU run, for strong-scaling analysis")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -264,21 +269,23 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     S = sim.Simulator(cfg.workloads, device=local, warps_per_block=args.warps_per_block,
-                      blocks_per_sm=args.blocks_per_sm, group_policy=args.group_policy)
+                      blocks_per_sm=args.blocks_per_sm, group_policy=args.group_policy,
+                      gen_policy=args.gen_policy)
     info = S.info()
 
     from paper_2603_11340_b200.dist import config_shard, seed_block, sweep_seed_offset
     strong = args.scaling == "strong" or world == 1
     knobs_local = cfg.knobs
+    pworld = world if world > 1 else max(1, args.share_of)   # partition width (--share-of: rank 0 of W)
     if args.workload == "c4":
         # the climb is seed-sharded (strong scaling): the pooled aggregates equal the 1-GPU ones exactly
-        lo, hi = seed_block(cfg.n_seeds, rank, world)
+        lo, hi = seed_block(cfg.n_seeds, rank, pworld)
         seeds = cfg.seeds()[lo:hi]
     elif strong:
         # sweeps are config-sharded: config c -> rank c mod world, all seeds local; every rank's
         # share is padded to the same length with always-invalid records (no work) for the all-gather
         seeds = cfg.seeds()
-        knobs_local = config_shard(cfg.knobs, rank, world, pad=inputs.PAD_KNOBS)
+        knobs_local = config_shard(cfg.knobs, rank, pworld, pad=inputs.PAD_KNOBS)
     else:
         # weak scaling (opt-in): every rank runs the full grid on its own seed block
         seeds = inputs.seeds(cfg.n_seeds, sweep_seed_offset(cfg.n_seeds, rank, cfg.seed_offset))
@@ -429,12 +436,14 @@ def main():
     k1_ms = [k1_start[i].elapsed_time(k1_end[i]) for i in range(args.steps)]
     t_total = sum(step_ms) / 1000.0
     t_k1 = sum(k1_ms) / 1000.0                         # the whole run call (K0 + simulation + K1b)
-    t_sim = prof["sim_ms"] / 1000.0                    # the simulation kernels alone (K1 / K1t / K1c)
+    t_gen = prof["gen_ms"] / 1000.0                    # K1g (split path; 0 with inline generation)
+    t_chain = prof["sim_ms"] / 1000.0                  # the chain kernels (K1 / K1s / K1t / K1c)
+    t_sim = t_gen + t_chain                            # the simulation as a whole
     t_k1b = prof["k1b_ms"] / 1000.0
     if world > 1:
-        tt = torch.tensor([t_total, t_k1, t_sim, t_k1b], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_total, t_k1, t_sim, t_k1b, t_gen, t_chain], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_total, t_k1, t_sim, t_k1b = tt.tolist()
+        t_total, t_k1, t_sim, t_k1b, t_gen, t_chain = tt.tolist()
 
     value = req_all * args.steps / t_total
 
@@ -537,7 +546,7 @@ def main():
             "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded Philox streams; LL/STRESS presets of DESIGN.md §5)",
             "config": {"workload": DESCR[args.workload], "replicas_per_gpu": R, "requests_per_replica": N,
-                       "requests_per_step": req_all, "preset": "STRESS" if args.workload.startswith("c5") else "LL",
+                       "requests_per_step": req_all, **({"share_of": pworld} if world == 1 and pworld > 1 else {}), "preset": "STRESS" if args.workload.startswith("c5") else "LL",
                        "l2": "flushed between timed steps (256 MiB write, untimed); inputs are < 1 MB",
                        "parallelism": f"dp{world} over replicas ({'seed-sharded climb' if args.workload == 'c4' else ('config-sharded: config c on rank c mod N, all seeds local' if strong else 'weak: full grid, per-rank seed block')})",
                        "exchange": exchange_desc,
@@ -545,7 +554,8 @@ def main():
                                   "regs_per_thread": info["regs_per_thread"]}},
             "replica_segments_per_s": (req_all // N) * args.steps / t_total,
             "run_ms_per_step": 1000.0 * t_k1 / args.steps,
-            "kernel_ms_per_step": {"simulate": 1000.0 * t_sim / args.steps, "k1b_select": 1000.0 * t_k1b / args.steps,
+            "kernel_ms_per_step": {"simulate": 1000.0 * t_sim / args.steps, "k1g_generate": 1000.0 * t_gen / args.steps,
+                                   "chain": 1000.0 * t_chain / args.steps, "k1b_select": 1000.0 * t_k1b / args.steps,
                                    "source": "CUDA events around each launch (slo_sim_profile) on the launching "
                                              "stream, " + ("the timed launches" if graph is None else
                                                            "an eager replay of the graph's launches")},

@@ -124,7 +124,11 @@ typedef struct {
   uint32_t group_policy;        /* static-batching lane groups (results never depend on it): 0 auto      */
                                 /* (whole warp for <= 1 replica per SM, else narrow G >= min(C,B)),       */
                                 /* 1 narrow, 2 wide G >= max(C,B), 3 whole warp (G = 32); else INVAL      */
-  uint32_t reserved[3];         /* must be 0                                                              */
+  uint32_t gen_policy;          /* static batching without think time (results never depend on it):      */
+                                /* 0 auto (= 2), 1 inline generation inside K1, 2 split: K1g writes every */
+                                /* request's 16-B record (16 B x chunk x N of scratch), K1s runs the     */
+                                /* batch chain over them; else INVAL                                      */
+  uint32_t reserved[2];         /* must be 0                                                              */
 } slo_sim_opts;
 
 typedef struct {                /* read-only launch facts of a handle                                    */
@@ -287,9 +291,10 @@ slo_status slo_pareto_front(slo_sim* h, const slo_config_agg* d_agg, uint32_t n_
 slo_status slo_philox_peak(slo_sim* h, uint32_t iters, uint32_t* d_sink, void* stream);
 
 /* Measurement hook (bench.py's per-kernel roofline): while enabled, every run call records CUDA events on its
- * stream around each launch chunk's K0 (classify), simulation kernels (K1 / K1t / K1c) and K1b (select);
- * slo_sim_profile_read waits for them and returns the summed elapsed milliseconds h_ms[0..2] = (K0, simulation,
- * K1b) and the number of chunks, then clears the marks.  Calls made while the stream is being captured into a
+ * stream around each launch chunk's K0 (classify), K1g (split-path generation; 0 when inline), simulation kernels
+ * (K1 / K1s / K1t / K1c) and K1b (select); slo_sim_profile_read waits for them and returns the summed elapsed
+ * milliseconds h_ms[0..3] = (K0, K1g, simulation, K1b) (h_ms: >= 4 doubles) and the number of chunks, then clears
+ * the marks.  Calls made while the stream is being captured into a
  * CUDA graph record nothing.  Errors: SLO_E_INVAL (null), SLO_E_CUDA. */
 slo_status slo_sim_profile(slo_sim* h, uint32_t enable);
 slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks);
@@ -304,12 +309,15 @@ slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks);
  *                         #{u : length(u) = l} for l = lo .. lo + ncw; d_out[ncw + 1] = #{u : length(u) <
  *                         length(u - 1)} + out-of-range values.  out_len >= ncw + 2.
  *   SLO_SELFTEST_ACCEPT : accept_q16 arg0, draft_width arg1, gamma arg2: d_out[A] = #{u : A(u) =
- *                         A}, A = 0..16; d_out[17] = #{u : A(u) > A(u - 1)}.  out_len >= 18.
+ *                         A}, A = 0..16; d_out[17] = #{u : A(u) > A(u - 1)}.  out_len >= 18.  (K1 / K1c's 256-entry
+ *                         byte guide.)
+ *   SLO_SELFTEST_ACCEPT2: the same through K1g's 4096-entry fine guide (K1g).
  *   SLO_SELFTEST_NOISE  : noise_step_ppm arg0: d_out[k] = #{w : f(w) = 10^6 + (k - 510) arg0},
  *                         k = 0..1020; d_out[1021] = #{w : f(w) off that lattice}.  out_len >= 1022.
  * d_out (device, u64) is zeroed by the call; results are valid after `stream` completes.
  * Errors: SLO_E_INVAL (null pointers, unknown `what`, bad arguments, short out_len), SLO_E_CUDA. */
-enum { SLO_SELFTEST_EXP = 0, SLO_SELFTEST_LENGTH = 1, SLO_SELFTEST_ACCEPT = 2, SLO_SELFTEST_NOISE = 3 };
+enum { SLO_SELFTEST_EXP = 0, SLO_SELFTEST_LENGTH = 1, SLO_SELFTEST_ACCEPT = 2, SLO_SELFTEST_NOISE = 3,
+       SLO_SELFTEST_ACCEPT2 = 4 };
 slo_status slo_selftest_transforms(slo_sim* h, uint32_t what, uint32_t arg0, uint32_t arg1, uint32_t arg2,
                                    uint64_t* d_out, uint32_t out_len, void* stream);
 

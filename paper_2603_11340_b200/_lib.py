@@ -24,7 +24,7 @@ EXPORTS = ("slo_sim_create", "slo_sim_destroy", "slo_sim_get_info", "slo_sim_run
            "slo_hillclimb_step", "slo_exchange_create", "slo_exchange_open", "slo_aggregate_exchange",
            "slo_exchange_error", "slo_exchange_destroy", "slo_philox_peak", "slo_pareto_front", "slo_status_string",
            "slo_last_error", "slo_selftest_transforms", "slo_sim_profile", "slo_sim_profile_read")
-SELFTEST = {"exp": 0, "length": 1, "accept": 2, "noise": 3}   # SLO_SELFTEST_* (include/slo_sim.h)
+SELFTEST = {"exp": 0, "length": 1, "accept": 2, "noise": 3, "accept2": 4}   # SLO_SELFTEST_* (include/slo_sim.h)
 EXCHANGE_HANDLE_BYTES = 64
 
 
@@ -54,7 +54,8 @@ class slo_workload(C.Structure):
 
 class slo_sim_opts(C.Structure):
     _fields_ = [("crn", C.c_uint32), ("warps_per_block", C.c_uint32), ("blocks_per_sm", C.c_uint32),
-                ("scratch_mb", C.c_uint32), ("group_policy", C.c_uint32), ("reserved", C.c_uint32 * 3)]
+                ("scratch_mb", C.c_uint32), ("group_policy", C.c_uint32), ("gen_policy", C.c_uint32),
+                ("reserved", C.c_uint32 * 2)]
 
 
 class slo_sim_info(C.Structure):

@@ -32,6 +32,8 @@ struct slo_sim {
   bool any_cont_think = false;      // a continuous-batching workload has think time: launch K1c on lists 9-11
   bool any_cont_plain = false;      // a continuous-batching workload without think time: K1c on lists 3-5
   uint32_t group_policy = 0;        // slo_sim_opts.group_policy
+  uint32_t gen_policy = 0;          // slo_sim_opts.gen_policy
+  bool any_static_plain = false;    // a static-batching workload without think time (K1 / K1g + K1s)
   std::vector<slo::DevWorkload> h_wl;  // host copy of the device workload descriptors
   slo::DevWorkload* d_wl = nullptr;
   uint32_t* d_tables = nullptr;
@@ -43,6 +45,8 @@ struct slo_sim {
   size_t lat_cap = 0;
   slo_replica_result* d_part = nullptr;
   size_t part_cap = 0;
+  uint4* d_rec = nullptr;           // split path: K1g's request records, [chunk][N]
+  size_t rec_cap = 0;
   size_t lat_budget = (size_t)4 << 30;  // bytes of latency rows per launch chunk
   char* d_pareto = nullptr;         // K5 scratch (grow-only)
   size_t pareto_cap = 0;
@@ -54,7 +58,7 @@ struct slo_sim {
   // measurement hook (slo_sim_profile): events around each chunk's K0 | simulation kernels | K1b
   bool profile = false;
   std::vector<cudaEvent_t> ev_free;             // recycled events
-  std::vector<std::array<cudaEvent_t, 4>> ev_marks;  // recorded, not yet read
+  std::vector<std::array<cudaEvent_t, 5>> ev_marks;  // recorded, not yet read
   std::string err;
 };
 
@@ -160,9 +164,10 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
   o.crn = 1;
   if (opts) {
     o = *opts;
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 2; ++i)
       if (o.reserved[i]) return fail(nullptr, SLO_E_INVAL, "create: opts.reserved must be 0");
     if (o.group_policy > 3) return fail(nullptr, SLO_E_INVAL, "create: opts.group_policy must be 0..3");
+    if (o.gen_policy > 2) return fail(nullptr, SLO_E_INVAL, "create: opts.gen_policy must be 0..2");
     if (o.crn > 1) return fail(nullptr, SLO_E_INVAL, "create: opts.crn must be 0 or 1");
     if (o.warps_per_block > (uint32_t)slo::kMaxWarpsPerBlock)
       return fail(nullptr, SLO_E_INVAL, "create: warps_per_block > %d", slo::kMaxWarpsPerBlock);
@@ -252,12 +257,14 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     h->any_think |= wl[w].arr.kind == 4 && wl[w].batching == 0;
     h->any_cont_think |= wl[w].arr.kind == 4 && wl[w].batching == 1;
     h->any_cont_plain |= wl[w].arr.kind != 4 && wl[w].batching == 1;
+    h->any_static_plain |= wl[w].arr.kind != 4 && wl[w].batching == 0;
   }
   h->crn = o.crn;
   if (o.warps_per_block) h->warps_per_block = (int)o.warps_per_block;
   h->blocks_per_sm_opt = (int)o.blocks_per_sm;
   if (o.scratch_mb) h->lat_budget = (size_t)o.scratch_mb << 20;
   h->group_policy = o.group_policy;
+  h->gen_policy = o.gen_policy;
   h->h_wl = hw;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, slo::slo_sim_kernel_t<false>) != cudaSuccess) {
@@ -292,15 +299,15 @@ slo_status slo_sim_profile(slo_sim* h, uint32_t enable) {
 slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks) {
   if (!h || !h_ms) return fail(h, SLO_E_INVAL, "profile_read: null argument");
   DeviceGuard g(h->device);
-  h_ms[0] = h_ms[1] = h_ms[2] = 0.0;
+  h_ms[0] = h_ms[1] = h_ms[2] = h_ms[3] = 0.0;
   for (auto& m : h->ev_marks) {
-    CUDA_TRY(h, cudaEventSynchronize(m[3]));
-    for (int i = 0; i < 3; ++i) {
+    CUDA_TRY(h, cudaEventSynchronize(m[4]));
+    for (int i = 0; i < 4; ++i) {
       float ms = 0.0f;
       CUDA_TRY(h, cudaEventElapsedTime(&ms, m[i], m[i + 1]));
       h_ms[i] += ms;
     }
-    for (int i = 0; i < 4; ++i) h->ev_free.push_back(m[i]);
+    for (int i = 0; i < 5; ++i) h->ev_free.push_back(m[i]);
   }
   if (h_chunks) *h_chunks = (uint32_t)h->ev_marks.size();
   h->ev_marks.clear();
@@ -318,6 +325,7 @@ slo_status slo_sim_destroy(slo_sim* h) {
     if (h->d_lists) cudaFree(h->d_lists);
     if (h->d_lat) cudaFree(h->d_lat);
     if (h->d_part) cudaFree(h->d_part);
+    if (h->d_rec) cudaFree(h->d_rec);
     if (h->d_scratch) cudaFree(h->d_scratch);
     if (h->d_pareto) cudaFree(h->d_pareto);
     for (auto& m : h->ev_marks)
@@ -371,6 +379,28 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   if ((s = ensure(h, h->d_lists, h->lists_cap, (size_t)slo::kLists * chunk, st)) != SLO_OK) return s;
   if (!d_lat && (s = ensure(h, h->d_lat, h->lat_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
   if (!d_detail && (s = ensure(h, h->d_part, h->part_cap, (size_t)n_rep, st)) != SLO_OK) return s;
+  // static batching without think time runs the split path (K1g records, K1s chain) unless gen_policy = 1 asks
+  // for K1's inline generation: 16 B of K1g records per request of the chunk
+  const bool split = h->any_static_plain && h->gen_policy != 1;
+  if (split && (s = ensure(h, h->d_rec, h->rec_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
+  constexpr uint32_t kGenTile = slo::kGenThreads * slo::kGenPerThread;
+  int gen_bps = 1, serve_bps = 1;
+  const size_t serve_smem = slo::serve_warp_bytes() * h->warps_per_block;
+  if (split) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gen_bps, slo::slo_gen_kernel, slo::kGenThreads, 0) != cudaSuccess ||
+        gen_bps < 1)
+      gen_bps = 1;
+    if (serve_smem > 48 * 1024) {
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_serve_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)serve_smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_serve_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)serve_smem));
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&serve_bps, slo::slo_serve_kernel_t<false>, h->warps_per_block * 32,
+                                                      serve_smem) != cudaSuccess || serve_bps < 1)
+      serve_bps = 1;
+    if (h->blocks_per_sm_opt > 0 && h->blocks_per_sm_opt < serve_bps) serve_bps = h->blocks_per_sm_opt;
+  }
 
   slo::SimParams p{};
   p.cfg = d_configs;
@@ -446,7 +476,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) prof = false;
   }
-  std::array<cudaEvent_t, 4> ev{};
+  std::array<cudaEvent_t, 5> ev{};
   auto mark = [&](int i) -> slo_status {
     if (!prof) return SLO_OK;
     if (h->ev_free.empty()) {
@@ -457,7 +487,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     ev[i] = h->ev_free.back();
     h->ev_free.pop_back();
     CUDA_TRY(h, cudaEventRecord(ev[i], st));
-    if (i == 3) h->ev_marks.push_back(ev);
+    if (i == 4) h->ev_marks.push_back(ev);
     return SLO_OK;
   };
   for (uint64_t r0 = 0; r0 < n_rep; r0 += chunk) {
@@ -486,10 +516,36 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    if (p.stop_n | p.stop_t)
-      slo::slo_sim_kernel_t<true><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
-    else
-      slo::slo_sim_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+    const bool stop = (p.stop_n | p.stop_t) != 0;
+    if (split) {   // K1g: every request's record at full width, then K1s: the batch chain over the records
+      p.rec = h->d_rec;
+      const uint32_t tpr = (N + kGenTile - 1) / kGenTile;
+      uint64_t gblocks = (uint64_t)gen_bps * h->sm_count;
+      if (gblocks > (uint64_t)nc * tpr) gblocks = (uint64_t)nc * tpr;
+      slo::slo_gen_kernel<<<(unsigned)gblocks, slo::kGenThreads, 0, st>>>(p, h->d_rec);
+      CUDA_TRY(h, cudaGetLastError());
+      if ((s = mark(2)) != SLO_OK) return s;
+      // K1s lane groups per warp: the fewest that still fit every replica of the chunk into the resident warp
+      // slots (one wave) — the chain is latency-bound, so a small launch runs one replica per warp
+      const uint64_t slots = (uint64_t)serve_bps * h->sm_count * h->warps_per_block;
+      uint64_t gpw = (nc + slots - 1) / slots;
+      if (gpw < 1) gpw = 1;
+      if (gpw > 4) gpw = 4;
+      slo::SimParams ps = p;
+      ps.gpw = (uint32_t)gpw;
+      ps.warp_bytes = (uint32_t)slo::serve_warp_bytes();
+      uint64_t sblocks = (uint64_t)serve_bps * h->sm_count;
+      const uint64_t sneed = ((uint64_t)nc + gpw * h->warps_per_block - 1) / (gpw * h->warps_per_block);
+      if (sblocks > sneed) sblocks = sneed;
+      if (sblocks < 1) sblocks = 1;
+      stop ? slo::slo_serve_kernel_t<true><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps)
+           : slo::slo_serve_kernel_t<false><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps);
+      p.rec = nullptr;
+    } else {
+      if ((s = mark(2)) != SLO_OK) return s;          // (no K1g: an empty interval)
+      stop ? slo::slo_sim_kernel_t<true><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p)
+           : slo::slo_sim_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
+    }
     CUDA_TRY(h, cudaGetLastError());
     if (h->any_think) {  // K1t: closed loops with think time (same group layout and grid as K1)
       if (p.stop_n | p.stop_t)
@@ -515,11 +571,11 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                               : slo::slo_sim_cont_kernel_t<false, false><<<cg, cb, cont_smem, st>>>(pc);
       CUDA_TRY(h, cudaGetLastError());
     }
-    if ((s = mark(2)) != SLO_OK) return s;
+    if ((s = mark(3)) != SLO_OK) return s;
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
     slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
     CUDA_TRY(h, cudaGetLastError());
-    if ((s = mark(3)) != SLO_OK) return s;
+    if ((s = mark(4)) != SLO_OK) return s;
   }
   return SLO_OK;
 }
@@ -807,6 +863,7 @@ slo_status slo_selftest_transforms(slo_sim* h, uint32_t what, uint32_t arg0, uin
       break;
     }
     case SLO_SELFTEST_ACCEPT:
+    case SLO_SELFTEST_ACCEPT2:
       if (arg0 > 65536 || arg1 < 1 || arg1 > 4 || arg2 > 16) return fail(h, SLO_E_INVAL, "selftest: bad acceptance");
       a.nbins = 17;
       a.viol_slot = 17;

@@ -33,6 +33,35 @@ __device__ __forceinline__ u32x4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
   return {c0, c1, c2, c3};
 }
 
+// Philox4x32-10 with the round keys precomputed (rk0[r] = k0 + r W0, rk1[r] = k1 + r W1): the same function as
+// philox(), for loops that draw many blocks under one key (K1g)
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+};
+__device__ __forceinline__ PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
+  PhiloxKeys K;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    K.k0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    K.k1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  return K;
+}
+__device__ __forceinline__ u32x4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const PhiloxKeys& K) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ K.k0[r];
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ K.k1[r];
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+  }
+  return {c0, c1, c2, c3};
+}
+
 // ---- E_q(u) ~ 2^32 * -ln((u+1)/2^32) in Q32.32.
 __device__ __forceinline__ uint64_t exp_q32(uint32_t u) {
   if (u == 0xFFFFFFFFu) return 0;                   // x = 2^32
@@ -133,6 +162,41 @@ __device__ __forceinline__ uint32_t accepted_guided(const uint8_t* guide, const 
                                                     uint32_t gp) {
   const uint32_t g = guide[u >> 24];
   uint32_t A = g & 0x7Fu;
+  if (g & 0x80u) {
+    while (A < gp && u <= tm1[A]) ++A;
+  }
+  return A;
+}
+
+// ---- fine acceptance guide (K1g, K6): 4096 byte entries by u >> 20, entry = (A_top + 1) | inside << 7 with
+// A_top = #{a : T_a - 1 >= top of the bucket} and inside = a threshold T_a - 1 falls in [bottom, top).  In a
+// bucket without an inside threshold A(u) = A_top for every u, so the common case is one byte load and the four
+// draws of a SPEC block sum their (A + 1) bytes with two adds (an inside flag lifts the sum past 127).  Built
+// by `stride` threads: each writes the A_top of its contiguous entries by a walk down the sorted thresholds,
+// then (after a barrier of the caller) accept_guide_fine_mark() flags the buckets holding a threshold.
+constexpr uint32_t kGuideFine = 4096;
+__device__ __forceinline__ void accept_guide_fine(const uint32_t* tm1, uint32_t gp, uint8_t* guide, uint32_t first,
+                                                  uint32_t stride) {
+  const uint32_t per = (kGuideFine + stride - 1) / stride;
+  const uint32_t k_lo = first * per, k_hi = min(kGuideFine, k_lo + per);
+  // A_top(k) = #{a : tm1_a >= (k << 20) | 0xFFFFF}: non-increasing in k; tm1 is non-increasing in a
+  uint32_t A = 0;
+  while (A < gp && tm1[A] >= (((k_hi - 1) << 20) | 0xFFFFFu)) ++A;   // count at the last entry
+  for (uint32_t k = k_hi; k-- > k_lo;) {
+    while (A < gp && tm1[A] >= ((k << 20) | 0xFFFFFu)) ++A;
+    guide[k] = (uint8_t)(A + 1u);
+  }
+}
+__device__ __forceinline__ void accept_guide_fine_mark(const uint32_t* tm1, uint32_t gp, uint8_t* guide, uint32_t t) {
+  if (t == 0) {
+    for (uint32_t a = 0; a < gp; ++a)
+      if ((tm1[a] & 0xFFFFFu) != 0xFFFFFu) guide[tm1[a] >> 20] |= 0x80u;
+  }
+}
+// A(u) from the entry g of bucket u >> 20; an inside bucket finishes the count over the thresholds below its
+// top, which are tm1[A_top ...] in order
+__device__ __forceinline__ uint32_t accepted_fine(uint32_t g, const uint32_t* tm1, uint32_t u, uint32_t gp) {
+  uint32_t A = (g & 0x7Fu) - 1u;
   if (g & 0x80u) {
     while (A < gp && u <= tm1[A]) ++A;
   }

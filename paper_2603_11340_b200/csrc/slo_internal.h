@@ -44,11 +44,17 @@ struct SimParams {
   uint32_t n_cfg, n_seeds, n_rep, n_wl;
   uint32_t r_base, n_chunk;    // this launch covers replicas [r_base, r_base + n_chunk)
   uint32_t warmup, seg, slo_us, crn;
-  uint32_t warp_bytes, pad;
+  uint32_t warp_bytes, gpw;    // per-warp shared memory; K1s: lane groups per warp in use (1..4)
   uint32_t stop_n, stop_t;     // segment stop rule, 0, 0 = off
+  const uint4* rec;            // split path: [n_chunk][N] request records written by K1g (nullptr: inline)
 };
 
 template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
+// K1s: the static-batching chain over K1g's request records (split path)
+template <bool STOP> __global__ void slo_serve_kernel_t(const SimParams p);
+// K1g: per-request records of the static-batching replicas (split path), one block per 2,048-request tile
+constexpr int kGenThreads = 256, kGenPerThread = 8;
+__global__ void slo_gen_kernel(const SimParams p, uint4* rec);
 // K1c: continuous batching (§2.12); THINK: the kind-4 (think-time) lists 9-11
 template <bool STOP, bool THINK> __global__ void slo_sim_cont_kernel_t(const SimParams p);
 template <bool STOP> __global__ void slo_sim_think_kernel_t(const SimParams p); // K1t: think-time closed loop (§2.11)
@@ -59,6 +65,7 @@ __global__ void slo_classify_kernel(const slo_knobs* cfg, const DevWorkload* wl,
                                     uint32_t n_chunk, uint32_t n_wl, uint32_t wide, uint32_t* ctl, uint32_t* lists);
 __global__ void slo_select_kernel(const SimParams p, uint32_t smem_vals);
 size_t group_warp_bytes();   // per-warp shared memory of K1
+size_t serve_warp_bytes();   // per-warp shared memory of K1s
 size_t cont_warp_bytes();    // per-warp shared memory of K1c
 __global__ void slo_aggregate_kernel(const slo_replica_result* detail, uint32_t n_cfg, uint32_t n_seeds,
                                      slo_config_agg* agg);

@@ -1,7 +1,7 @@
 // slo_selftest.cu — K6: exhaustive self-test of the integer transforms K1/K1c use (SURVEY §8(c) pins table).
 //
 // Every 2^32 input of E_q, a length table's lookup (§2.4), the acceptance prefix A(u) (§2.5)
-// and the noise factor (§2.4) is evaluated with the SAME device functions the simulation kernels call
+// (both guides: K1 / K1c's byte guide and K1g's two-level guide) and the noise factor (§2.4) is evaluated with the SAME device functions the simulation kernels call
 // (slo_device.cuh), and reduced to order-free block hashes / histograms that tests compare with the oracle
 // (E_q) or with exact closed forms (lengths: #{u -> l} = cw[l] - cw[l-1]; acceptance: #{u : A(u) >= a} = T_a;
 // noise: the 4-fold byte convolution).  One CUDA block per 2^20 inputs (4096 blocks), 256 threads, each thread
@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(256) slo_selftest_kernel(SelftestArgs a, const
   extern __shared__ __align__(16) uint32_t sh[];        // histogram bins (what 1-3)
   __shared__ uint32_t tm1[16];
   __shared__ uint8_t guide[256];
+  __shared__ uint8_t guide2[kGuideFine];
   __shared__ unsigned long long s_hash, s_viol;
   const uint32_t nb = a.nbins;
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
@@ -30,10 +31,13 @@ __global__ void __launch_bounds__(256) slo_selftest_kernel(SelftestArgs a, const
     s_viol = 0;
   }
   uint32_t gp = 0;
-  if (a.what == 2) {
+  if (a.what == 2 || a.what == 4) {
     gp = accept_thresholds(a.arg0, a.arg1, a.arg2, tm1, threadIdx.x == 0);
     __syncthreads();
-    accept_guide(tm1, gp, guide, threadIdx.x, blockDim.x);
+    if (a.what == 2) accept_guide(tm1, gp, guide, threadIdx.x, blockDim.x);
+    else accept_guide_fine(tm1, gp, guide2, threadIdx.x, blockDim.x);
+    __syncthreads();
+    if (a.what == 4) accept_guide_fine_mark(tm1, gp, guide2, threadIdx.x);
   }
   __syncthreads();
 
@@ -43,6 +47,7 @@ __global__ void __launch_bounds__(256) slo_selftest_kernel(SelftestArgs a, const
       case 0: return exp_q32(u);
       case 1: return length_guided(tables, a.off, a.goff, a.lo, u) - a.lo;
       case 2: return accepted_guided(guide, tm1, u, gp);
+      case 4: return accepted_fine(guide2[u >> 20], tm1, u, gp);
       default: return noise_factor(u, a.arg0);
     }
   };
@@ -54,7 +59,7 @@ __global__ void __launch_bounds__(256) slo_selftest_kernel(SelftestArgs a, const
     if (a.what == 0) {
       h += selftest_mix(u, v);
       viol += (u > 0 && v > prev);                     // E_q increase (R27: expected, counted)
-    } else if (a.what == 1 || a.what == 2) {
+    } else if (a.what == 1 || a.what == 2 || a.what == 4) {
       if (v < nb) atomicAdd(&sh[v], 1u);
       else ++viol;                                     // out of range
       // lengths must be non-decreasing in u, A non-increasing

@@ -121,17 +121,13 @@ struct alignas(16) Group {
   uint32_t cnt_meas, cnt_incl, stopped, pad3;   // stop rule (§2.14): measured completions, counted ones, done
 };
 
-// A(u) = #{a in [1, gp] : u < T_a} via the bucket guide
-template <class GR>
-__device__ __forceinline__ uint32_t accepted(const GR& R, uint32_t u, uint32_t gp) {
-  return accepted_guided(R.guide, R.tm1, u, gp);
-}
-
 // (a1) set up a newly acquired replica (group-convergent; other groups do not enter)
-template <int G, class GR>
+// (ACCEPT = false: K1s, whose chain never draws acceptance words — K1g resolved every S_i)
+template <int G, bool ACCEPT = true, class GR>
 __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const slo_knobs& k, uint32_t k0,
                                               uint32_t k1, uint32_t gamma, uint32_t& gp, int li, uint32_t gmask) {
-  gp = accept_thresholds(k.accept_q16, k.draft_width, gamma, R.tm1, li == 0);
+  gp = 0;
+  if constexpr (ACCEPT) gp = accept_thresholds(k.accept_q16, k.draft_width, gamma, R.tm1, li == 0);
   if (li == 0) {
     const uint64_t g0 = W.gap_q16[0] == INF64 ? INF64 : (W.gap_q16[0] << 8) / k.rate_scale_q8;
     const uint64_t g1 = W.gap_q16[1] == INF64 ? INF64 : (W.gap_q16[1] << 8) / k.rate_scale_q8;
@@ -176,22 +172,55 @@ __device__ __forceinline__ void setup_replica(GR& R, const DevWorkload& W, const
     R.stopped = 0;
   }
   __syncwarp(gmask);
-  if (gamma > 0) accept_guide(R.tm1, gp, R.guide, (uint32_t)li, G);   // bucket guide for A(u)
+  if constexpr (ACCEPT) {
+    if (gamma > 0) accept_guide(R.tm1, gp, R.guide, (uint32_t)li, G);   // bucket guide for A(u)
+  }
   __syncwarp(gmask);
 }
 
-// (a2, a3) generate requests [gen, gen + G) for every group with `go` (all lanes execute)
+// (a3, a7) request i's lengths and decode step count from its REQ block w: P and O through
+// the length tables' bucket guides, and S_i = min{s : sum_{j<s} (A(u_{i,j}) + 1) >= O_i}.  With static batches a
+// member's j counts its steps within its batch and with continuous batching its own decode iterations, so in
+// both models S_i depends on request i's own SPEC stream only and is resolved here, one SPEC block (4 steps)
+// per loop trip.  gp = 0 (no speculation, or alpha_eff = 0): A = 0 and S = O.  Shared by the inline
+// generation of K1 / K1c and by K1g, so both paths run the same arithmetic.
+__device__ __forceinline__ void request_attrs(const DevWorkload& W, const uint32_t* __restrict__ tables,
+                                              const uint8_t* guide, const uint32_t* tm1, uint32_t gp, uint32_t i,
+                                              uint32_t k0, uint32_t k1, const u32x4& w, uint32_t& P, uint32_t& S) {
+  P = length_guided(tables, W.p_off, W.p_goff, W.p_lo, w.y);
+  const uint32_t O = length_guided(tables, W.o_off, W.o_goff, W.o_lo, w.z);
+  S = O;
+  if (gp > 0) {
+    uint32_t tok = 0;
+    for (uint32_t q = 0;; ++q) {
+      const u32x4 b = philox(i, 1, q, 0, k0, k1);
+      uint32_t g0 = guide[b.x >> 24], g1 = guide[b.y >> 24];
+      uint32_t g2 = guide[b.z >> 24], g3 = guide[b.w >> 24];
+      if ((g0 | g1 | g2 | g3) & 0x80u) {           // a threshold inside one of the buckets (rare)
+        g0 = accepted_guided(guide, tm1, b.x, gp);
+        g1 = accepted_guided(guide, tm1, b.y, gp);
+        g2 = accepted_guided(guide, tm1, b.z, gp);
+        g3 = accepted_guided(guide, tm1, b.w, gp);
+      }
+      const uint32_t c1 = tok + (g0 & 0x7Fu) + 1u, c2 = c1 + (g1 & 0x7Fu) + 1u;
+      const uint32_t c3 = c2 + (g2 & 0x7Fu) + 1u, c4 = c3 + (g3 & 0x7Fu) + 1u;
+      if (c4 >= O) {
+        S = 4u * q + 1u + (c1 < O) + (c2 < O) + (c3 < O);
+        break;
+      }
+      tok = c4;
+    }
+  }
+}
+
+// (a2) arrival instants of requests [gen, gen + G) from their increments x: a group scan with
+// the carry R.last gives a_i (kind 0) or the operational epoch tau_i (kinds 1, 2), then the bursty Cox time
+// change walks the phases in order (kind 1 draws a PHASE block per new phase).  All lanes execute.
 template <int G, class GR>
-__device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ wls, uint32_t wl,
-                                         const uint32_t* __restrict__ tables, uint32_t k0, uint32_t k1, uint32_t gen,
-                                         uint32_t N, uint32_t warmup, bool go, int lane, int li) {
-  const uint32_t i = gen + (uint32_t)li;
-  const bool valid = go && i < N;
-  const u32x4 w = philox(i, 0, 0, 0, k0, k1);
-  const uint64_t E = valid ? exp_q32(w.x) : 0;
+__device__ __forceinline__ uint64_t arrivals(GR& R, const DevWorkload* __restrict__ wls, uint32_t wl, uint32_t k0,
+                                             uint32_t k1, uint64_t x, uint32_t i, uint32_t N, bool go, int lane,
+                                             int li) {
   const uint32_t kind = go ? R.kind : 0u;
-  // kind 0: gaps; kinds 1, 2: operational-time increments; kinds 3, 4 (closed loop): every a_i = 0
-  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : (kind >= 3 ? 0ull : E);
   const uint64_t last = go ? R.last : 0ull;
   const uint64_t sc = last + gscan64<G>(x, li);     // kind 0: a_i; kinds 1, 2: tau_i; kind 3: 0
   const uint64_t newlast = gshfl64<G>(sc, G - 1);
@@ -235,47 +264,207 @@ __device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ 
   }
   __syncwarp();     // every lane has read R.last
   if (go && li == 0) R.last = newlast;
+  return a;
+}
+
+// (a2, a3) generate requests [gen, gen + G) for every group with `go` (all lanes execute)
+template <int G, class GR>
+__device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ wls, uint32_t wl,
+                                         const uint32_t* __restrict__ tables, uint32_t k0, uint32_t k1, uint32_t gen,
+                                         uint32_t N, uint32_t warmup, bool go, int lane, int li) {
+  const uint32_t i = gen + (uint32_t)li;
+  const bool valid = go && i < N;
+  const uint32_t kind = go ? R.kind : 0u;
+  const u32x4 w = philox(i, 0, 0, 0, k0, k1);
+  const uint64_t E = valid ? exp_q32(w.x) : 0;
+  // kind 0: gaps; kinds 1, 2: operational-time increments; kinds 3, 4 (closed loop): every a_i = 0
+  const uint64_t x = kind == 0 ? mulshr(E, go ? R.g[0] : 0ull, 48) : (kind >= 3 ? 0ull : E);
+  const uint64_t a = arrivals<G>(R, wls, wl, k0, k1, x, i, N, go, lane, li);
   if (valid) {
-    const DevWorkload& W = wls[wl];
-    const uint32_t P = length_guided(tables, W.p_off, W.p_goff, W.p_lo, w.y);
-    const uint32_t O = length_guided(tables, W.o_off, W.o_goff, W.o_lo, w.z);
+    uint32_t P, S;
+    request_attrs(wls[wl], tables, R.guide, R.tm1, R.gp, i, k0, k1, w, P, S);
     R.a[i % GR::RING] = a;
-    R.po[i % GR::RING] = P | (O << 16);
+    R.po[i % GR::RING] = P;             // (the chain reads P only; O is folded into S)
     R.w3[i % GR::RING] = w.w;
     if (i == warmup) R.a_w = a;
-    // (a7) S_i = min{s : sum_{j<s} (A(u_{i,j}) + 1) >= O_i}.  With static batches a
-    // member's j counts its steps within its batch and with continuous batching its own decode iterations,
-    // so in both models S_i depends on request i's own SPEC stream only and is resolved here, lane-parallel
-    // over the generated requests, one SPEC block (4 steps) per loop trip.  gp = 0 (no speculation, or
-    // alpha_eff = 0): A = 0 and S = O.
-    uint32_t S = O;
-    const uint32_t gp = R.gp;
-    if (gp > 0) {
-      uint32_t tok = 0;
-      for (uint32_t q = 0;; ++q) {
-        const u32x4 b = philox(i, 1, q, 0, k0, k1);
-        uint32_t g0 = R.guide[b.x >> 24], g1 = R.guide[b.y >> 24];
-        uint32_t g2 = R.guide[b.z >> 24], g3 = R.guide[b.w >> 24];
-        if ((g0 | g1 | g2 | g3) & 0x80u) {           // a threshold inside one of the buckets (rare)
-          g0 = accepted(R, b.x, gp);
-          g1 = accepted(R, b.y, gp);
-          g2 = accepted(R, b.z, gp);
-          g3 = accepted(R, b.w, gp);
-        }
-        const uint32_t c1 = tok + (g0 & 0x7Fu) + 1u, c2 = c1 + (g1 & 0x7Fu) + 1u;
-        const uint32_t c3 = c2 + (g2 & 0x7Fu) + 1u, c4 = c3 + (g3 & 0x7Fu) + 1u;
-        if (c4 >= O) {
-          S = 4u * q + 1u + (c1 < O) + (c2 < O) + (c3 < O);
-          break;
-        }
-        tok = c4;
-      }
-    }
     R.ss[i % GR::RING] = (uint16_t)S;
   }
   __syncwarp();
 }
 
+// ------------------------------------------------------------------------------------------------
+// K1g: the per-request attributes of the static-batching replicas (split path).  Everything a
+// request draws from its own streams — REQ block (arrival increment, P, O, noise word) and the SPEC blocks
+// that resolve S_i — is independent of the batch chain, so it is computed here at full width (one thread per
+// request, 4 requests per thread, one block per 1,024-request tile of a replica) and handed to K1s as one
+// 16-B record per request: {x lo, x hi, P | S << 16, w3} with x = the scaled Poisson gap (kind 0), the
+// operational increment E_q (kinds 1, 2) or 0 (closed loop).  K1s keeps only the scan of x, the bursty phase
+// walk and the batch chain.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool split_static(const slo_knobs& k, const DevWorkload* __restrict__ wl, uint32_t n_wl) {
+  return knobs_valid(k, n_wl) && wl[k.workload].batching == 0 && wl[k.workload].kind != 4;
+}
+
+#ifndef SLO_GEN_PAIR
+#define SLO_GEN_PAIR 1
+#endif
+#ifndef SLO_GEN_RK
+#define SLO_GEN_RK 1
+#endif
+#if SLO_GEN_RK   // round keys precomputed per replica (registers) or bumped per round
+#define GEN_PHILOX(c0, c1, c2, c3) philox_rk(c0, c1, c2, c3, K)
+#else
+#define GEN_PHILOX(c0, c1, c2, c3) philox(c0, c1, c2, c3, k0, k1)
+#endif
+#ifndef SLO_GEN_MINB
+#define SLO_GEN_MINB 3
+#endif
+__global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(const SimParams p, uint4* __restrict__ rec) {
+  __shared__ uint32_t s_tm1[16];
+  __shared__ __align__(16) uint8_t s_guide[kGuideFine];
+  constexpr uint32_t TILE = kGenThreads * kGenPerThread;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t N = p.warmup + p.seg;
+  // a block takes whole replicas when the launch has enough of them to fill the grid (the guide is then rebuilt
+  // at most once per replica, and no block barrier falls between its tiles); a small launch splits replicas
+  // into 2,048-request tiles so every block has work
+  const uint32_t tpr0 = (N + TILE - 1) / TILE;
+  const uint32_t tpr = (uint64_t)p.n_chunk >= 2ull * gridDim.x ? 1u : tpr0;   // tiles per replica
+  const uint32_t rounds = tpr == 1 ? tpr0 : 1u;                                  // 2,048-request rounds per tile
+  const uint64_t total = (uint64_t)p.n_chunk * tpr;
+  uint32_t cur = 0xFFFFFFFFu, gp = 0, kind = 0, wl = 0, gkey = 0xFFFFFFFFu;
+  bool spec = false;                                   // gamma_eff > 0: a SPEC stream is consumed (S_i blocks)
+  PhiloxKeys K = philox_keys(0, 0);
+  uint32_t k0 = 0, k1 = 0;
+  const bool count = p.stats && !(p.stop_n | p.stop_t);  // (under a stop rule K1s counts what it simulates)
+  unsigned long long steps = 0, blocks = 0;               // member steps (sum of S) and SPEC blocks consumed
+  uint64_t g0 = 0;
+  bool skip = true;
+  for (uint64_t tt = blockIdx.x; tt < total; tt += gridDim.x) {
+    const uint32_t rl = (uint32_t)(tt / tpr), tile = (uint32_t)(tt - (uint64_t)rl * tpr);
+    if (rl != cur) {                                   // block-uniform: a new replica
+      cur = rl;
+      const uint32_t r = p.r_base + rl, ci = r / p.n_seeds;
+      const slo_knobs k = p.cfg[ci];
+      skip = !split_static(k, p.wl, p.n_wl);
+      if (!skip) {
+        wl = k.workload;
+        const DevWorkload& W = p.wl[wl];
+        const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+        const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+        k0 = (uint32_t)seed;
+        k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+        K = philox_keys(k0, k1);
+        kind = W.kind;
+        g0 = kind == 0 ? (W.gap_q16[0] << 8) / k.rate_scale_q8 : 0ull;   // (kind 0: finite, validated)
+        const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+        spec = gamma > 0;
+        // the guide depends on (alpha, W, gamma) only: rebuilt when they change
+        const uint32_t key = gamma == 0 ? 0u : (k.accept_q16 << 7) ^ (k.draft_width << 5) ^ gamma;
+        if (key != gkey) {
+          gkey = key;
+          __syncthreads();                             // the previous guide's reads are done
+          gp = accept_thresholds(k.accept_q16, k.draft_width, gamma, s_tm1, tid == 0);
+          __syncthreads();
+          if (gamma > 0) accept_guide_fine(s_tm1, gp, s_guide, tid, kGenThreads);
+          __syncthreads();
+          if (gamma > 0) accept_guide_fine_mark(s_tm1, gp, s_guide, tid);
+          __syncthreads();
+        }
+      }
+    }
+    if (skip) continue;
+    const DevWorkload& W = p.wl[wl];
+    uint4* out = rec + (size_t)rl * N;
+#pragma unroll 1
+    for (uint32_t e = 0; e < rounds * (uint32_t)kGenPerThread; ++e) {
+      const uint32_t i = tile * TILE + e * kGenThreads + tid;
+      if (i >= N) break;
+      // REQ block: arrival increment, lengths, noise word
+      const u32x4 w = GEN_PHILOX(i, 0, 0, 0);
+      const uint64_t E = exp_q32(w.x);
+      const uint64_t x = kind == 0 ? mulshr(E, g0, 48) : (kind >= 3 ? 0ull : E);
+      const uint32_t P = length_guided(p.tables, W.p_off, W.p_goff, W.p_lo, w.y);
+      const uint32_t O = length_guided(p.tables, W.o_off, W.o_goff, W.o_lo, w.z);
+      // S_i = min{s : sum_{j<s} (A(u_{i,j}) + 1) >= O_i}, one SPEC block (4 steps) per trip
+      uint32_t S = O;
+      if (gp > 0) {
+        uint32_t tok = 0;
+#if SLO_GEN_PAIR
+        // two SPEC blocks per trip (q, q + 1): independent Philox chains interleave (the kernel is bound by the
+        // rounds' dependency latency); the second block of the last trip is drawn but not consumed when the
+        // crossing falls in the first (it is not counted as consumed work)
+        for (uint32_t q = 0;; q += 2) {
+          const u32x4 ba = GEN_PHILOX(i, 1, q, 0);
+          const u32x4 bb = GEN_PHILOX(i, 1, q + 1u, 0);
+          uint32_t a0 = s_guide[ba.x >> 20], a1 = s_guide[ba.y >> 20], a2 = s_guide[ba.z >> 20], a3 = s_guide[ba.w >> 20];
+          uint32_t b0 = s_guide[bb.x >> 20], b1 = s_guide[bb.y >> 20], b2 = s_guide[bb.z >> 20], b3 = s_guide[bb.w >> 20];
+          uint32_t sa = a0 + a1 + a2 + a3, sb = b0 + b1 + b2 + b3;   // sums of (A + 1) unless a flag lifts one >= 128
+          if ((sa | sb) >= 128u) {                      // a threshold inside one of the buckets (rare)
+            a0 = accepted_fine(a0, s_tm1, ba.x, gp) + 1u;
+            a1 = accepted_fine(a1, s_tm1, ba.y, gp) + 1u;
+            a2 = accepted_fine(a2, s_tm1, ba.z, gp) + 1u;
+            a3 = accepted_fine(a3, s_tm1, ba.w, gp) + 1u;
+            b0 = accepted_fine(b0, s_tm1, bb.x, gp) + 1u;
+            b1 = accepted_fine(b1, s_tm1, bb.y, gp) + 1u;
+            b2 = accepted_fine(b2, s_tm1, bb.z, gp) + 1u;
+            b3 = accepted_fine(b3, s_tm1, bb.w, gp) + 1u;
+            sa = a0 + a1 + a2 + a3;
+            sb = b0 + b1 + b2 + b3;
+          }
+          if (tok + sa >= O) {
+            const uint32_t c1 = tok + a0, c2 = c1 + a1, c3 = c2 + a2;
+            S = 4u * q + 1u + (c1 < O) + (c2 < O) + (c3 < O);
+            break;
+          }
+          tok += sa;
+          if (tok + sb >= O) {
+            const uint32_t c1 = tok + b0, c2 = c1 + b1, c3 = c2 + b2;
+            S = 4u * q + 5u + (c1 < O) + (c2 < O) + (c3 < O);
+            break;
+          }
+          tok += sb;
+        }
+#else
+        for (uint32_t q = 0;; ++q) {
+          const u32x4 bl = GEN_PHILOX(i, 1, q, 0);
+          uint32_t g0_ = s_guide[bl.x >> 20], g1 = s_guide[bl.y >> 20];
+          uint32_t g2 = s_guide[bl.z >> 20], g3 = s_guide[bl.w >> 20];
+          uint32_t sum = g0_ + g1 + g2 + g3;             // sum of (A + 1) unless an inside flag lifts it >= 128
+          if (sum >= 128u) {                            // a threshold inside one of the buckets (rare)
+            g0_ = accepted_fine(g0_, s_tm1, bl.x, gp) + 1u;
+            g1 = accepted_fine(g1, s_tm1, bl.y, gp) + 1u;
+            g2 = accepted_fine(g2, s_tm1, bl.z, gp) + 1u;
+            g3 = accepted_fine(g3, s_tm1, bl.w, gp) + 1u;
+            sum = g0_ + g1 + g2 + g3;
+          }
+          if (tok + sum >= O) {
+            const uint32_t c1 = tok + g0_, c2 = c1 + g1, c3 = c2 + g2;
+            S = 4u * q + 1u + (c1 < O) + (c2 < O) + (c3 < O);
+            break;
+          }
+          tok += sum;
+        }
+#endif
+      }
+      out[i] = make_uint4((uint32_t)x, (uint32_t)(x >> 32), P | (S << 16), w.w);
+      steps += S;
+      blocks += spec ? (S + 3u) >> 2 : 0u;
+    }
+  }
+  if (count) {
+    steps = warp_sum64(steps);
+    blocks = warp_sum64(blocks);
+    if ((tid & 31) == 0) {
+      atomicAdd((unsigned long long*)&p.stats->member_steps, steps);
+      atomicAdd((unsigned long long*)&p.stats->philox_blocks, blocks);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// group-scoped sorting networks and scans (K1, K1t, K1c)
+// ------------------------------------------------------------------------------------------------
 // bitonic sort of u32 keys over the first 2^LG lanes of each G-lane group (ascending)
 template <int G, int LG>
 __device__ __forceinline__ uint32_t gsort_n(uint32_t key, int li) {
@@ -583,6 +772,267 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
     }
     if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u) flush_counters(p, ct);  // rare
   }
+}
+
+// ------------------------------------------------------------------------------------------------
+// K1s: the static-batching batch chain over K1g's request records (split path).
+//
+// Generation (Philox, E_q, lengths, S_i) already happened in K1g, so a batch iteration is only the chain of
+// §2.6's closed forms.  Per batch, lane li of a group holds request j = h + li of the issue window:
+//   s_j = max(a_j, kappa_{j-C}); t_form and b from two shuffles and a ballot (as K1);
+//   completion order and cumulative cost by RANK COUNTING instead of a sorting network: every member shuffles in
+//   the packed words w_m = S_m << 18 | m << 13 | P_m of the members (distinct, ordered by (S, m)), and
+//     rank_li = #{m < b : w_m < w_li}            (its completion index: kappa_{h + rank} = c_li),
+//     sum_m min(S_m, S_li) = sum_m (min(w_m, w_li) >> 18),  max P, max S, sum S  (prefill, batch end);
+//   so every lane computes its OWN completion c_li = t0 + f (alpha0 S + alpha1 sum min) / 10^6 and latency,
+//   stored in request order (no permutation shuffles), and the batch end t_end = c of the largest S.
+// Records are register-staged one refill ahead (a refill falls at least one batch after its load was issued).
+// A launch with few replicas spreads them over more warps (p.gpw groups per warp): the chain is latency-bound,
+// so one replica per warp on an otherwise idle scheduler runs fastest.
+// ------------------------------------------------------------------------------------------------
+template <int G>
+struct alignas(16) SGroup {
+  static constexpr int RING = 4 * G;                  // a, w, f for [h, gen), gen <= h + 2G
+  static constexpr int KRING = 4 * G > 64 ? 4 * G : 64;   // kappa for [h - C, h + b): C + b <= 64
+  uint64_t a[RING];                                   // arrival time a_j at a[j % RING]
+  uint64_t kap[KRING];                                // kappa_k (k-th completion) at kap[k % KRING]
+  uint32_t w[RING];                                   // S_j << 18 | P_j (the lane index is or-ed in at use)
+  uint32_t f[RING];                                   // noise factor of request j as a batch head (ppm, §2.4)
+  uint64_t g[2], rho[2];                              // arrival-process state (arrivals(), setup_replica())
+  uint64_t last, pstart, pD, pU, pLam, nphase, a_w, alpha0, alpha1;
+  uint32_t ph, pstate, pre_base, pre_tok, noise, kind, start_state, gp;
+  uint32_t k0, k1, wl, cnt_meas, cnt_incl, stopped;
+};
+
+template <int G, bool STOP>
+__device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
+  using SG = SGroup<G>;
+  constexpr int RING = SG::RING, KRING = SG::KRING;
+  const int g = lane / G, li = lane % G;
+  SG& R = reinterpret_cast<SG*>(wsmem)[g];
+  const uint32_t gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
+  const uint32_t N = p.warmup + p.seg;
+  const uint32_t count = p.counts[cls];
+  const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
+
+  uint32_t r = 0, h = 0, gen = 0, rowoff = 0;          // rowoff = (r - r_base) * N: the replica's row
+  uint32_t C = 0, B = 0, mw = 0, pre_base = 0, pre_tok = 0, noise = 0;
+  uint64_t alpha0 = 0, alpha1 = 0, t_idle = 0, my_sum = 0;
+  uint32_t my_slo = 0;
+  unsigned long long dsteps = 0;                       // decode steps (sum over batches of max S), lane 0
+  bool active = false, exhausted = (uint32_t)g >= p.gpw, closed = false, spec = false;
+  uint4 stg{0, 0, 0, 0};                               // K1g record of request gen + li, loaded ahead
+
+  for (;;) {
+    __syncwarp();
+    // ---- acquire replicas for idle groups
+    bool want = !active && !exhausted;
+    while (__any_sync(FULL, want)) {
+      uint32_t idx = 0;
+      if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
+      idx = gshfl<G>(idx, 0);
+      if (want) {
+        if (idx >= count) {
+          exhausted = true;
+        } else {
+          r = list[idx];
+          const uint32_t ci = r / p.n_seeds;
+          const slo_knobs k = p.cfg[ci];
+          if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
+            if (li == 0) {
+              p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+              if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+            }
+          } else {
+            const DevWorkload& W = p.wl[k.workload];
+            const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+            const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+            const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+            uint32_t gp;
+            if (li == 0) {
+              R.wl = k.workload;
+              R.cnt_incl = 0;
+            }
+            setup_replica<G, false>(R, W, k, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, gamma, gp, li, gmask);
+            C = k.conc;
+            B = k.max_num_seqs;
+            mw = k.max_wait_us;
+            spec = gamma > 0;
+            closed = W.kind >= 3;
+            pre_base = W.t.pre_base_us;
+            pre_tok = W.t.pre_tok_us;
+            noise = W.t.noise_step_ppm;
+            step_coeffs(W.t, gamma, k.draft_width, alpha0, alpha1);   // d(n) = alpha0 + alpha1 n (R10, R28)
+            rowoff = (r - p.r_base) * N;
+            stg = (uint32_t)li < N ? __ldcs(p.rec + rowoff + li) : uint4{0, 0, 0, 0};
+            h = 0;
+            gen = 0;
+            t_idle = 0;
+            my_slo = 0;
+            my_sum = 0;
+            active = true;
+          }
+        }
+      }
+      want = !active && !exhausted;
+    }
+    if (!__any_sync(FULL, active)) break;
+    __syncwarp();
+
+    // ---- (a2) keep [h, h + G) in the ring, up to 2G ahead: scan of the increments, bursty time change
+    bool need = active && gen < N && gen < h + G;
+    while (__any_sync(FULL, need)) {
+      const bool go = active && gen < N && gen < h + 2 * G;
+      const uint32_t i = gen + (uint32_t)li;
+      const bool valid = go && i < N;
+      const uint64_t x = valid ? (((uint64_t)stg.y << 32) | stg.x) : 0ull;
+      const uint64_t a = arrivals<G>(R, p.wl, R.wl, R.k0, R.k1, x, i, N, go, lane, li);
+      if (valid) {
+        R.a[i % RING] = a;
+        R.w[i % RING] = ((stg.z >> 16) << 18) | (stg.z & 0xFFFFu);
+        R.f[i % RING] = noise_factor(stg.w, noise);
+        if (i == p.warmup) R.a_w = a;
+      }
+      if (go) {
+        gen += G;
+        if (gen + (uint32_t)li < N) stg = __ldcs(p.rec + rowoff + gen + li);
+      }
+      need = active && gen < N && gen < h + G;
+    }
+    __syncwarp();
+
+    // ---- (a4) issue window j = h + li: s_j = max(a_j, kappa_{j-C})
+    const uint32_t j = h + (uint32_t)li;
+    uint64_t sj = INF64, aj = 0;
+    uint32_t wj = 0xFFFFE000u;                         // not a member: above every real word, P = 0
+    if (active && j < N) {
+      aj = R.a[j % RING];
+      wj = R.w[j % RING] | ((uint32_t)li << 13);
+      if ((uint32_t)li < C) {
+        const uint64_t kj = j >= C ? R.kap[(j - C) % KRING] : 0;
+        sj = aj > kj ? aj : kj;
+      }
+    }
+    // ---- (a5) formation instant and batch size (DESIGN.md §2.6 closed form 2)
+    const uint64_t sh = gshfl64<G>(sj, 0);
+    const uint64_t slB = gshfl64<G>(sj, (int)(B - 1) & (G - 1));
+    uint64_t t_form = t_idle > sh ? t_idle : sh;
+    if (mw > 0) {
+      const uint64_t sl = B > C ? INF64 : slB;
+      const uint64_t dl = sh + mw;
+      const uint64_t x = dl < sl ? dl : sl;
+      if (x > t_form) t_form = x;
+    }
+    uint32_t b = __popc(gballot<G>(sj <= t_form, lane));
+    if (b > B) b = B;
+    if (!active) b = 0;
+    const bool member = (uint32_t)li < b;
+
+    // ---- (a6, a7) rank counting over the members' words: rank = #{m < b : w_m < w_li}, lts = the S of those
+    // m; then sum_m min(S_m, S_li) = lts + S_li (b - rank) and the batch ends with the largest key (rank b - 1)
+    const uint32_t bmax = __reduce_max_sync(FULL, b);
+    const uint32_t S = wj >> 18;
+    uint32_t rank = 0, lts = 0, mrank = 0;
+#pragma unroll
+    for (int m = 0; m < G; ++m) {
+      if ((uint32_t)m >= bmax) break;
+      const uint32_t wm = __shfl_sync(FULL, wj, m, G);
+      const bool lt = (uint32_t)m < b && wm < wj;
+      rank += lt ? 1u : 0u;
+      lts += lt ? wm >> 18 : 0u;
+      if (STOP) mrank += lt && h + (uint32_t)m >= p.warmup;   // measured completions before this one
+    }
+    const uint32_t maxP = gmax<G>(member ? wj & 0x1FFFu : 0u);
+    const uint64_t f = R.f[h % RING];                  // the head's noise factor
+    const uint64_t t0 = t_form + f * ((uint64_t)pre_base + (uint64_t)pre_tok * maxP) / 1000000u;
+    const uint32_t summin = lts + S * (b - rank);
+    const uint64_t c = t0 + f * (alpha0 * S + alpha1 * summin) / 1000000u;
+    if (member) R.kap[(h + rank) % KRING] = c;
+    const uint32_t lastm = gballot<G>(member && rank + 1u == b, lane);
+    const int ll = lastm ? __ffs(lastm) - 1 : 0;
+    const uint64_t tend = gshfl64<G>(c, ll);           // the largest completion: the batch end
+    const uint32_t Smax = gshfl<G>(S, ll);
+
+    // ---- (a8) this lane's own latency: from arrival (open loop, R2) or issue (closed loop, §2.11)
+    const bool measured = member && j >= p.warmup;
+    if (closed && member && j == p.warmup) R.a_w = sj;   // the goodput window starts at that issue
+    const uint64_t l = c - (closed ? sj : aj);
+    bool inc = true;
+    if constexpr (STOP) {                              // stop rule (§2.14), completion order = rank order
+      __syncwarp();                                    // R.a_w of a closed-loop warmup issue written above
+      const uint32_t mm = gballot<G>(measured, lane);
+      const uint32_t before = active ? R.cnt_meas : 0u;
+      const uint32_t kpos = before + mrank + 1u;
+      const uint32_t need_n = p.stop_n ? p.stop_n : 1u;
+      const bool cand = active && !R.stopped && measured && kpos >= need_n && c >= R.a_w + p.stop_t;
+      const uint32_t rmin = gmin<G>(cand ? rank : 0xFFFFFFFFu);
+      const uint32_t cmk = gballot<G>(cand && rank == rmin, lane);
+      const uint64_t tstar = gshfl64<G>(c, (int)((cmk ? __ffs(cmk) - 1 : 0) & (G - 1)));
+      inc = cmk == 0 || c <= tstar;
+      const uint32_t ninc = __popc(gballot<G>(measured && inc, lane));
+      __syncwarp();
+      if (active && li == 0) {
+        R.cnt_meas = before + __popc(mm);
+        R.cnt_incl += ninc;
+        if (cmk) R.stopped = 1;
+      }
+    }
+    if (measured && inc) {
+      my_slo += (l <= p.slo_us);
+      my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
+      my_sum += l;
+    }
+    if (member) p.lat[rowoff + j] = !inc ? 0xFFFFFFFFu : (l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l);
+
+    // work counters, lane-local (member steps and SPEC blocks are counted by K1g, except under a stop rule,
+    // where only what was simulated counts)
+    if constexpr (STOP) {
+      if (member) {
+        ct.steps += S;
+        ct.blocks += spec ? (S + 3u) >> 2 : 0u;
+      }
+    }
+    if (active && li == 0) {
+      ct.batches += 1;
+      dsteps += Smax;
+    }
+    if (active) {
+      t_idle = tend;
+      h += b;
+    }
+    if constexpr (STOP) {                              // stopped: the rest of the segment is never simulated
+      __syncwarp();
+      if (active && R.stopped) {
+        for (uint32_t jj = h + (uint32_t)li; jj < N; jj += G) p.lat[rowoff + jj] = 0xFFFFFFFFu;
+        h = N;
+      }
+    }
+
+    // ---- groups that finished their replica: outputs (p99 and goodput follow in K1b)
+    const bool fin = active && h >= N;
+    if (__any_sync(FULL, fin)) {
+      const uint32_t slo_met = gsum<G>(my_slo & 0x7FFFFFFFu);
+      const uint64_t sum = gsum64<G>(my_sum);
+      const bool sat = gballot<G>((my_slo >> 31) != 0, lane) != 0;
+      // the window ends at the last MEASURED completion (§2.8): the largest c among this last batch's measured
+      // members (every earlier batch ended before this one formed)
+      const uint64_t cm = gmax64<G>(measured && inc ? c : 0ull);
+      if (fin && li == 0) {
+        const uint64_t Tw = cm - R.a_w;
+        const uint32_t fl = (sat ? 2u : 0u) | (STOP && !R.stopped ? 4u : 0u);
+        p.part[r] = slo_replica_result{0, slo_met, STOP ? R.cnt_incl : p.seg, fl, Tw < 1 ? 1 : Tw, sum};
+        if (p.stats) {
+          unsigned long long* st = (unsigned long long*)p.stats;
+          atomicAdd(st + 0, (unsigned long long)N);
+          atomicAdd(st + 4, (unsigned long long)(N + R.nphase));
+          atomicAdd(st + 5, 1ull);
+        }
+      }
+      if (fin) active = false;
+    }
+    if (STOP && ct.steps >= 0x40000000u) flush_counters(p, ct);  // rare
+  }
+  if (p.stats && dsteps) atomicAdd((unsigned long long*)&p.stats->decode_steps, dsteps);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -983,6 +1433,32 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_kernel_t(const SimParams p) {
   }
 }
 
+// K1s: the static-batching chain over K1g's request records (split path); leaner than K1, so a lower register cap
+#ifndef SLO_SERVE_MAXNREG
+#define SLO_SERVE_MAXNREG 80
+#endif
+template <bool STOP>
+__global__ void __maxnreg__(SLO_SERVE_MAXNREG) slo_serve_kernel_t(const SimParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
+  Counters ct{0, 0, 0, 0};
+  serve_mode<8, STOP>(p, 0, wsmem, lane, ct);
+  serve_mode<16, STOP>(p, 1, wsmem, lane, ct);
+  serve_mode<32, STOP>(p, 2, wsmem, lane, ct);
+  if (p.stats) {
+    const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
+    const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
+    if (lane == 0) {
+      unsigned long long* st = (unsigned long long*)p.stats;
+      atomicAdd(st + 1, (unsigned long long)batches);
+      atomicAdd(st + 2, (unsigned long long)dsteps);
+      atomicAdd(st + 3, (unsigned long long)steps);
+      atomicAdd(st + 4, (unsigned long long)blocks);
+    }
+  }
+}
+
 // K1t: closed loops with think time (kind 4), launched only when a workload uses it
 template <bool STOP>
 __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_think_kernel_t(const SimParams p) {
@@ -1037,6 +1513,8 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimPar
 // carries none of the stop rule's code
 template __global__ void slo_sim_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_kernel_t<true>(const SimParams p);
+template __global__ void slo_serve_kernel_t<false>(const SimParams p);
+template __global__ void slo_serve_kernel_t<true>(const SimParams p);
 template __global__ void slo_sim_think_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_think_kernel_t<true>(const SimParams p);
 template __global__ void slo_sim_cont_kernel_t<false, false>(const SimParams p);
@@ -1048,6 +1526,13 @@ size_t cont_warp_bytes() {
   size_t m = 4 * sizeof(CGroup<8>);
   if (2 * sizeof(CGroup<16>) > m) m = 2 * sizeof(CGroup<16>);
   if (sizeof(CGroup<32>) > m) m = sizeof(CGroup<32>);
+  return m;
+}
+
+size_t serve_warp_bytes() {
+  size_t m = 4 * sizeof(SGroup<8>);
+  if (2 * sizeof(SGroup<16>) > m) m = 2 * sizeof(SGroup<16>);
+  if (sizeof(SGroup<32>) > m) m = sizeof(SGroup<32>);
   return m;
 }
 

@@ -105,12 +105,13 @@ class Simulator:
     """One libslosim handle on one CUDA device."""
 
     def __init__(self, workloads: Sequence[Dict], device: Optional[int] = None, crn: int = 1,
-                 warps_per_block: int = 0, blocks_per_sm: int = 0, scratch_mb: int = 0, group_policy: int = 0):
+                 warps_per_block: int = 0, blocks_per_sm: int = 0, scratch_mb: int = 0, group_policy: int = 0,
+                 gen_policy: int = 0):
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
         self.options = dict(crn=crn, warps_per_block=warps_per_block, blocks_per_sm=blocks_per_sm,
-                            scratch_mb=scratch_mb, group_policy=group_policy)
+                            scratch_mb=scratch_mb, group_policy=group_policy, gen_policy=gen_policy)
         self.workloads = list(workloads)
         n = len(self.workloads)
         arr = (_lib.slo_workload * n)()
@@ -136,6 +137,7 @@ class Simulator:
         opts.crn, opts.warps_per_block, opts.blocks_per_sm = crn, warps_per_block, blocks_per_sm
         opts.scratch_mb = scratch_mb
         opts.group_policy = group_policy
+        opts.gen_policy = gen_policy
         h = C.c_void_p()
         check(lib().slo_sim_create(self.device, arr, n, C.byref(opts), C.byref(h)))
         self.h = h
@@ -266,11 +268,11 @@ class Simulator:
         check(lib().slo_sim_profile(self.h, 1 if enable else 0), self.h)
 
     def profile_read(self) -> Dict:
-        """Summed ms of the recorded runs per kernel class {k0, sim, k1b} and the chunk count; clears them."""
-        ms = (C.c_double * 3)()
+        """Summed ms of the recorded runs per kernel class {k0, k1g, sim, k1b} and the chunk count; clears them."""
+        ms = (C.c_double * 4)()
         n = C.c_uint32(0)
         check(lib().slo_sim_profile_read(self.h, ms, C.byref(n)), self.h)
-        return {"k0_ms": ms[0], "sim_ms": ms[1], "k1b_ms": ms[2], "chunks": n.value}
+        return {"k0_ms": ms[0], "gen_ms": ms[1], "sim_ms": ms[2], "k1b_ms": ms[3], "chunks": n.value}
 
     def selftest(self, what: str, arg0: int = 0, arg1: int = 0, arg2: int = 0, stream=None) -> np.ndarray:
         """K6: exhaustive 2^32-input hashes / histograms of a transform (slo_selftest_transforms), as uint64."""

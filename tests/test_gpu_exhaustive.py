@@ -64,10 +64,13 @@ def test_length_tables_all_inputs(S, wl, table):
 
 
 @pytest.mark.parametrize("accept,width,gamma", [(32768, 1, 16), (inputs.q16(0.3), 2, 8), (inputs.q16(0.9), 4, 16),
-                                                (0, 1, 4), (65536, 3, 16), (12345, 1, 1), (60000, 2, 12)])
-def test_acceptance_all_inputs(S, orc, accept, width, gamma):
+                                                (0, 1, 4), (65536, 3, 16), (12345, 1, 1), (60000, 2, 12),
+                                                (inputs.q16(0.3), 1, 16), (65500, 1, 16), (inputs.q16(0.7), 2, 16)])
+@pytest.mark.parametrize("guide", ["accept", "accept2"], ids=["byte-guide", "two-level-guide"])
+def test_acceptance_all_inputs(S, orc, accept, width, gamma, guide):
+    """Both acceptance guides (K1 / K1c's byte guide, K1g's two-level guide) fix A at every u."""
     s, _ = S
-    out = s.selftest("accept", accept, width, gamma)
+    out = s.selftest(guide, accept, width, gamma)
     _, T = orc.thresholds(accept, width, gamma)
     hist = [int(x) for x in out[:17]]
     assert sum(hist) == 2 ** 32

@@ -75,9 +75,10 @@ def _wls():
             inputs.preset_ll(rate=40.0, stream_id=7), inputs.preset_closed(stream_id=3)]
 
 
+@pytest.mark.parametrize("gen", [1, 2], ids=["inline", "split"])
 @pytest.mark.parametrize("policy", [1, 2, 3], ids=["narrow", "wide", "warp"])
 @pytest.mark.parametrize("block", range(6))
-def test_random_small_configs(S, orc, block, policy):
+def test_random_small_configs(S, orc, block, policy, gen):
     """Random valid knob records over every workload kind, lengths spanning several 32-request windows
     and a ragged tail, warmup on/off — every latency and output bit-exact, plus the work counters; in both
     lane-group policies (narrow G >= min(C, B), the throughput default; wide G >= max(C, B))."""
@@ -95,7 +96,7 @@ def test_random_small_configs(S, orc, block, policy):
     ks[7] = inputs.knobs(conc=30, max_num_seqs=2, max_wait_us=20_000, workload=4)
     N = rng.choice([37, 333, 1000, 1234])
     warmup = rng.choice([0, 0, 17, 100])
-    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup, group_policy=policy)
+    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup, group_policy=policy, gen_policy=gen)
     tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
     for ci, k in enumerate(ks):
         for si, sd in enumerate(seeds):
@@ -106,8 +107,9 @@ def test_random_small_configs(S, orc, block, policy):
         assert int(g["stats"][f]) == tot[f], f
 
 
+@pytest.mark.parametrize("gen", [1, 2], ids=["inline", "split"])
 @pytest.mark.parametrize("policy", [1, 2], ids=["narrow", "wide"])
-def test_edge_cases(S, orc, policy):
+def test_edge_cases(S, orc, policy, gen):
     """Degenerate sizes and values: one request, N < 32, invalid records, saturating SLO, zero noise."""
     wls = [inputs.preset_ll(), inputs.workload(kind=0, rate=1000.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0))]
     ks = [inputs.knobs(conc=8, max_num_seqs=16), inputs.knobs(conc=0), inputs.knobs(max_num_seqs=33),
@@ -116,7 +118,7 @@ def test_edge_cases(S, orc, policy):
                                                                           draft_len=3, spec_on=1)]
     seeds = inputs.seeds(2, 900)
     for N, warm in ((1, 0), (1, 5), (31, 0), (32, 1), (33, 0), (65, 64)):
-        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm, group_policy=policy)
+        g = _run_gpu(S, wls, ks, seeds, N, warmup=warm, group_policy=policy, gen_policy=gen)
         for ci, k in enumerate(ks):
             for si, sd in enumerate(seeds):
                 r = ci * len(seeds) + si
@@ -585,8 +587,9 @@ def test_pareto_front_properties_at_scale(S):
     s.close()
 
 
+@pytest.mark.parametrize("gen", [1, 2], ids=["inline", "split"])
 @pytest.mark.parametrize("cont", [0, 1], ids=["static", "continuous"])
-def test_stop_rule_matches_oracle(S, orc, cont):
+def test_stop_rule_matches_oracle(S, orc, cont, gen):
     """NEXT-3 segment stop rule: with (n_min, t_min) the device stops each
     replica at t* — the first measured completion that is at least the n_min-th and t_min after t0 — and
     counts only requests completed by then; every stored latency (sentinels included), p50/p95/p99,
@@ -597,7 +600,7 @@ def test_stop_rule_matches_oracle(S, orc, cont):
     ks[0] = inputs.knobs(conc=8, max_num_seqs=8, draft_len=4, spec_on=1, workload=5)       # closed loop
     seeds = inputs.seeds(2, 900 + cont)
     N, warm = 700, 30
-    s = S.Simulator(wls, device=0)
+    s = S.Simulator(wls, device=0, gen_policy=gen)
     for n_min, t_min in ((50, 0), (1, 3_000_000), (300, 20_000_000), (700, 0), (10, 10**9)):
         out = s.run_batch(S.knobs_tensor(ks), S.seeds_tensor(seeds), N, warmup_len=warm, latencies=True,
                           percentiles=True, stop_n_min=n_min, stop_t_min_us=t_min)

@@ -1,9 +1,12 @@
-"""Per-CUDA-source-line instruction and stall totals from an ncu report (needs -lineinfo)."""
+"""Per-CUDA-source-line instruction and stall totals from an ncu report (needs -lineinfo).
+usage: python tools/ncu_lines.py REPORT [TOP] [KERNEL_REGEX]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if len(sys.argv) > 3:
+    cmd += ["-k", "regex:" + sys.argv[3]]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname = "?"
 hdr = None
