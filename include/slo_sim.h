@@ -291,10 +291,10 @@ slo_status slo_pareto_front(slo_sim* h, const slo_config_agg* d_agg, uint32_t n_
 slo_status slo_philox_peak(slo_sim* h, uint32_t iters, uint32_t* d_sink, void* stream);
 
 /* Measurement hook (bench.py's per-kernel roofline): while enabled, every run call records CUDA events on its
- * stream around each launch chunk's K0 (classify), K1g (split-path generation; 0 when inline), simulation kernels
+ * stream around each launch chunk's K0 (classify), K1g (split-path generation; 0 when inline), the chain kernels
  * (K1 / K1s / K1t / K1c) and K1b (select); slo_sim_profile_read waits for them and returns the summed elapsed
- * milliseconds h_ms[0..3] = (K0, K1g, simulation, K1b) (h_ms: >= 4 doubles) and the number of chunks, then clears
- * the marks.  Calls made while the stream is being captured into a
+ * milliseconds h_ms[0..4] = (K0, K1g, chain, K1b, simulation = end of K0 to start of K1b) (h_ms: >= 5 doubles)
+ * and the number of chunks, then clears the marks.  Calls made while the stream is being captured into a
  * CUDA graph record nothing.  Errors: SLO_E_INVAL (null), SLO_E_CUDA. */
 slo_status slo_sim_profile(slo_sim* h, uint32_t enable);
 slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks);

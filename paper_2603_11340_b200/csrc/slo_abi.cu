@@ -58,7 +58,8 @@ struct slo_sim {
   // measurement hook (slo_sim_profile): events around each chunk's K0 | simulation kernels | K1b
   bool profile = false;
   std::vector<cudaEvent_t> ev_free;             // recycled events
-  std::vector<std::array<cudaEvent_t, 5>> ev_marks;  // recorded, not yet read
+  std::vector<std::array<cudaEvent_t, 7>> ev_marks;  // recorded, not yet read
+
   std::string err;
 };
 
@@ -299,15 +300,18 @@ slo_status slo_sim_profile(slo_sim* h, uint32_t enable) {
 slo_status slo_sim_profile_read(slo_sim* h, double* h_ms, uint32_t* h_chunks) {
   if (!h || !h_ms) return fail(h, SLO_E_INVAL, "profile_read: null argument");
   DeviceGuard g(h->device);
-  h_ms[0] = h_ms[1] = h_ms[2] = h_ms[3] = 0.0;
+  h_ms[0] = h_ms[1] = h_ms[2] = h_ms[3] = h_ms[4] = 0.0;
+  // marks per chunk: 0/1 around K0, 2/3 around K1g, 4/5 around the chain kernels, 5/6 K1b; 1/5 the simulation
+  static const int from[5] = {0, 2, 4, 5, 1}, to[5] = {1, 3, 5, 6, 5};
   for (auto& m : h->ev_marks) {
-    CUDA_TRY(h, cudaEventSynchronize(m[4]));
-    for (int i = 0; i < 4; ++i) {
+    CUDA_TRY(h, cudaEventSynchronize(m[6]));
+    CUDA_TRY(h, cudaEventSynchronize(m[3]));
+    for (int i = 0; i < 5; ++i) {
       float ms = 0.0f;
-      CUDA_TRY(h, cudaEventElapsedTime(&ms, m[i], m[i + 1]));
+      CUDA_TRY(h, cudaEventElapsedTime(&ms, m[from[i]], m[to[i]]));
       h_ms[i] += ms;
     }
-    for (int i = 0; i < 5; ++i) h->ev_free.push_back(m[i]);
+    for (int i = 0; i < 7; ++i) h->ev_free.push_back(m[i]);
   }
   if (h_chunks) *h_chunks = (uint32_t)h->ev_marks.size();
   h->ev_marks.clear();
@@ -331,6 +335,7 @@ slo_status slo_sim_destroy(slo_sim* h) {
     for (auto& m : h->ev_marks)
       for (cudaEvent_t e : m) cudaEventDestroy(e);
     for (cudaEvent_t e : h->ev_free) cudaEventDestroy(e);
+
   }
   delete h;
   return SLO_OK;
@@ -375,14 +380,16 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   if (chunk * N >= (1ull << 31)) chunk = ((1ull << 31) - 1) / N;
   if (chunk < 1) chunk = 1;
   if (chunk > n_rep) chunk = n_rep;
+  // static batching without think time runs the split path (K1g records, K1s chain) unless gen_policy = 1 asks
+  // for K1's inline generation
+  const bool split = h->any_static_plain && h->gen_policy != 1;
   slo_status s;
   if ((s = ensure(h, h->d_lists, h->lists_cap, (size_t)slo::kLists * chunk, st)) != SLO_OK) return s;
   if (!d_lat && (s = ensure(h, h->d_lat, h->lat_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
   if (!d_detail && (s = ensure(h, h->d_part, h->part_cap, (size_t)n_rep, st)) != SLO_OK) return s;
-  // static batching without think time runs the split path (K1g records, K1s chain) unless gen_policy = 1 asks
-  // for K1's inline generation: 16 B of K1g records per request of the chunk
-  const bool split = h->any_static_plain && h->gen_policy != 1;
+  // 16 B of K1g records per request of the chunk
   if (split && (s = ensure(h, h->d_rec, h->rec_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
+
   constexpr uint32_t kGenTile = slo::kGenThreads * slo::kGenPerThread;
   int gen_bps = 1, serve_bps = 1;
   const size_t serve_smem = slo::serve_warp_bytes() * h->warps_per_block;
@@ -476,8 +483,8 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) prof = false;
   }
-  std::array<cudaEvent_t, 5> ev{};
-  auto mark = [&](int i) -> slo_status {
+  std::array<cudaEvent_t, 7> ev{};
+  auto mark = [&](int i, cudaStream_t on) -> slo_status {
     if (!prof) return SLO_OK;
     if (h->ev_free.empty()) {
       cudaEvent_t e;
@@ -486,32 +493,33 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     }
     ev[i] = h->ev_free.back();
     h->ev_free.pop_back();
-    CUDA_TRY(h, cudaEventRecord(ev[i], st));
-    if (i == 4) h->ev_marks.push_back(ev);
+    CUDA_TRY(h, cudaEventRecord(ev[i], on));
+    if (i == 6) h->ev_marks.push_back(ev);
     return SLO_OK;
   };
+
   for (uint64_t r0 = 0; r0 < n_rep; r0 += chunk) {
     const uint32_t nc = (uint32_t)((n_rep - r0) < chunk ? (n_rep - r0) : chunk);
     p.r_base = (uint32_t)r0;
     p.n_chunk = nc;
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
-    if ((s = mark(0)) != SLO_OK) return s;
+    if ((s = mark(0, st)) != SLO_OK) return s;
     CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * slo::kCtlWords, st));
     // lane groups: narrow (G >= min(C, B), up to four replicas per warp) by default — measured best from
     // 512-replica climb steps (one 8-GPU rank of C4) up to the full sweeps; a chunk of at most one replica per
     // SM runs each replica on a whole warp (C1: shortest chain); wide (G >= max(C, B)) only when forced
-    const uint32_t wide = h->group_policy == 3 ? 2u
-                          : h->group_policy == 2 ? 1u
-                          : h->group_policy == 1 ? 0u
-                          : nc <= (uint32_t)h->sm_count ? 2u : 0u;
+    const uint32_t wide = (h->group_policy == 3 ? 2u
+                           : h->group_policy == 2 ? 1u
+                           : h->group_policy == 1 ? 0u
+                           : nc <= (uint32_t)h->sm_count ? 2u : 0u) | (split ? 4u : 0u);   // bit 2: split path
     slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
                                                                     h->n_wl, wide, h->d_ctl);
     CUDA_TRY(h, cudaGetLastError());
     slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc, h->n_wl,
                                                               wide, h->d_ctl, h->d_lists);
     CUDA_TRY(h, cudaGetLastError());
-    if ((s = mark(1)) != SLO_OK) return s;
+    if ((s = mark(1, st)) != SLO_OK) return s;
     uint64_t blocks = (uint64_t)bps * h->sm_count;
     const uint64_t need = ((uint64_t)nc + 4u * h->warps_per_block - 1) / (4u * h->warps_per_block);
     if (blocks > need) blocks = need;
@@ -519,30 +527,32 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     const bool stop = (p.stop_n | p.stop_t) != 0;
     if (split) {   // K1g: every request's record at full width, then K1s: the batch chain over the records
       p.rec = h->d_rec;
-      const uint32_t tpr = (N + kGenTile - 1) / kGenTile;
-      uint64_t gblocks = (uint64_t)gen_bps * h->sm_count;
-      if (gblocks > (uint64_t)nc * tpr) gblocks = (uint64_t)nc * tpr;
-      slo::slo_gen_kernel<<<(unsigned)gblocks, slo::kGenThreads, 0, st>>>(p, h->d_rec);
-      CUDA_TRY(h, cudaGetLastError());
-      if ((s = mark(2)) != SLO_OK) return s;
       // K1s lane groups per warp: the fewest that still fit every replica of the chunk into the resident warp
       // slots (one wave) — the chain is latency-bound, so a small launch runs one replica per warp
       const uint64_t slots = (uint64_t)serve_bps * h->sm_count * h->warps_per_block;
       uint64_t gpw = (nc + slots - 1) / slots;
       if (gpw < 1) gpw = 1;
-      if (gpw > 4) gpw = 4;
-      slo::SimParams ps = p;
-      ps.gpw = (uint32_t)gpw;
-      ps.warp_bytes = (uint32_t)slo::serve_warp_bytes();
+      if (gpw > 8) gpw = 8;
+      const uint32_t tpr = (N + kGenTile - 1) / kGenTile;
+      uint64_t gblocks = (uint64_t)gen_bps * h->sm_count;
+      if (gblocks > (uint64_t)nc * tpr) gblocks = (uint64_t)nc * tpr;
       uint64_t sblocks = (uint64_t)serve_bps * h->sm_count;
       const uint64_t sneed = ((uint64_t)nc + gpw * h->warps_per_block - 1) / (gpw * h->warps_per_block);
       if (sblocks > sneed) sblocks = sneed;
       if (sblocks < 1) sblocks = 1;
+      if ((s = mark(2, st)) != SLO_OK) return s;
+      slo::slo_gen_kernel<<<(unsigned)gblocks, slo::kGenThreads, 0, st>>>(p, h->d_rec);
+      CUDA_TRY(h, cudaGetLastError());
+      if ((s = mark(3, st)) != SLO_OK || (s = mark(4, st)) != SLO_OK) return s;
+      slo::SimParams ps = p;
+      ps.gpw = (uint32_t)gpw;
+      ps.warp_bytes = (uint32_t)slo::serve_warp_bytes();
       stop ? slo::slo_serve_kernel_t<true><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps)
            : slo::slo_serve_kernel_t<false><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps);
       p.rec = nullptr;
     } else {
-      if ((s = mark(2)) != SLO_OK) return s;          // (no K1g: an empty interval)
+      if ((s = mark(2, st)) != SLO_OK || (s = mark(3, st)) != SLO_OK || (s = mark(4, st)) != SLO_OK)
+        return s;                                     // (no K1g: an empty interval)
       stop ? slo::slo_sim_kernel_t<true><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p)
            : slo::slo_sim_kernel_t<false><<<(unsigned)blocks, h->warps_per_block * 32, smem, st>>>(p);
     }
@@ -571,11 +581,11 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                               : slo::slo_sim_cont_kernel_t<false, false><<<cg, cb, cont_smem, st>>>(pc);
       CUDA_TRY(h, cudaGetLastError());
     }
-    if ((s = mark(3)) != SLO_OK) return s;
+    if ((s = mark(5, st)) != SLO_OK) return s;
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
     slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
     CUDA_TRY(h, cudaGetLastError());
-    if ((s = mark(4)) != SLO_OK) return s;
+    if ((s = mark(6, st)) != SLO_OK) return s;
   }
   return SLO_OK;
 }

@@ -11,7 +11,11 @@ constexpr int kDefaultWarpsPerBlock = 4;
 // K0 work lists: static batching by lane-group size G = 8, 16, 32 (>= min(C, B) narrow, >= max(C, B) wide, or
 // 32 for a lone replica; K1), then continuous batching by G = 8, 16, 32 >= min(C, B) (wide: >= B) (K1c), then
 // closed loops with think time (kind 4) by G = 8, 16, 32 >= max(C, B): static (K1t), continuous (K1c, think)
-constexpr int kLists = 12;
+// and (split path only) list 12: static batching with min(C, B) = 1, every batch a single request (K1s's scan),
+// list 13: static batching with G = 4 >= min(C, B) (K1s, eight replicas per warp)
+constexpr int kLists = 14;
+constexpr int kScanList = 12, kG4List = 13;
+// control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 constexpr int kCtlBucket = 32, kCtlWords = kCtlBucket + 2 * 16 * kLists;
 

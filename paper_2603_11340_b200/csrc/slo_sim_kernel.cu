@@ -316,6 +316,8 @@ __device__ __forceinline__ bool split_static(const slo_knobs& k, const DevWorklo
 #else
 #define GEN_PHILOX(c0, c1, c2, c3) philox(c0, c1, c2, c3, k0, k1)
 #endif
+__device__ __forceinline__ int gen_list(int q) { return q == 0 ? kScanList : q == 1 ? kG4List : q - 2; }
+
 #ifndef SLO_GEN_MINB
 #define SLO_GEN_MINB 3
 #endif
@@ -328,11 +330,18 @@ __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(cons
   // a block takes whole replicas when the launch has enough of them to fill the grid (the guide is then rebuilt
   // at most once per replica, and no block barrier falls between its tiles); a small launch splits replicas
   // into 2,048-request tiles so every block has work
+  // the replicas: this slice of the static split lists (K0's order: longest expected chains first, so the
+  // records K1s needs first are written first)
+  // (lists in K1s's order: scan, G = 4, 8, 16, 32)
+  uint32_t lo[6];
+  lo[0] = 0;
+  for (int q = 0; q < 5; ++q) lo[q + 1] = lo[q] + p.counts[gen_list(q)];
+  const uint32_t n_rep = lo[5];
   const uint32_t tpr0 = (N + TILE - 1) / TILE;
-  const uint32_t tpr = (uint64_t)p.n_chunk >= 2ull * gridDim.x ? 1u : tpr0;   // tiles per replica
+  const uint32_t tpr = (uint64_t)n_rep >= 2ull * gridDim.x ? 1u : tpr0;   // tiles per replica
   const uint32_t rounds = tpr == 1 ? tpr0 : 1u;                                  // 2,048-request rounds per tile
-  const uint64_t total = (uint64_t)p.n_chunk * tpr;
-  uint32_t cur = 0xFFFFFFFFu, gp = 0, kind = 0, wl = 0, gkey = 0xFFFFFFFFu;
+  const uint64_t total = (uint64_t)n_rep * tpr;
+  uint32_t cur = 0xFFFFFFFFu, gp = 0, kind = 0, wl = 0, gkey = 0xFFFFFFFFu, rl = 0;
   bool spec = false;                                   // gamma_eff > 0: a SPEC stream is consumed (S_i blocks)
   PhiloxKeys K = philox_keys(0, 0);
   uint32_t k0 = 0, k1 = 0;
@@ -341,10 +350,13 @@ __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(cons
   uint64_t g0 = 0;
   bool skip = true;
   for (uint64_t tt = blockIdx.x; tt < total; tt += gridDim.x) {
-    const uint32_t rl = (uint32_t)(tt / tpr), tile = (uint32_t)(tt - (uint64_t)rl * tpr);
-    if (rl != cur) {                                   // block-uniform: a new replica
-      cur = rl;
-      const uint32_t r = p.r_base + rl, ci = r / p.n_seeds;
+    const uint32_t en = (uint32_t)(tt / tpr), tile = (uint32_t)(tt - (uint64_t)en * tpr);
+    if (en != cur) {                                   // block-uniform: a new replica
+      cur = en;
+      const int q = en < lo[1] ? 0 : en < lo[2] ? 1 : en < lo[3] ? 2 : en < lo[4] ? 3 : 4;
+      const uint32_t r = p.lists[(size_t)gen_list(q) * p.n_chunk + (en - lo[q])];
+      rl = r - p.r_base;
+      const uint32_t ci = r / p.n_seeds;
       const slo_knobs k = p.cfg[ci];
       skip = !split_static(k, p.wl, p.n_wl);
       if (!skip) {
@@ -1036,6 +1048,147 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
 }
 
 // ------------------------------------------------------------------------------------------------
+// K1s scan mode (list 12): static batching with min(C, B) = 1.  Every batch is the single request at the head,
+// batch j is request j and completions come in index order, so with t_j = c_j:
+//   s_j = max(a_j, t_{j-C}) and t_form_j = max(t_{j-1}, s_j + w), w = max_wait if B > C (= 1) else 0, hence
+//   t_j = max(t_{j-1} + w, a_j + w) + D_j,  D_j = floor(f_j (pre_base + pre_tok P_j) / 10^6)
+//                                                + floor(f_j (alpha0 + alpha1) S_j / 10^6)
+// (t_{j-C} <= t_{j-1}; for B = 1 the max_wait term vanishes because s_{h+B-1} = s_h; for C = 1 < B the queue
+// never reaches B and the batch forms at s_h + max_wait).  x -> max(x + A, Bv) maps compose associatively,
+// (A1, B1) then (A2, B2) = (A1 + A2, max(B1 + A2, B2)), so a warp resolves 32 requests per step with a
+// 5-stage max-plus scan instead of 32 dependent batch iterations.  One replica per warp (G = 32).
+// ------------------------------------------------------------------------------------------------
+template <bool STOP>
+__device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
+  SGroup<32>& R = *reinterpret_cast<SGroup<32>*>(wsmem);  // arrival-process state (arrivals(), setup_replica())
+  const uint32_t N = p.warmup + p.seg;
+  const uint32_t count = p.counts[cls];
+  const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
+  for (;;) {
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(p.cursor + cls, 1u);
+    idx = __shfl_sync(FULL, idx, 0);
+    if (idx >= count) break;
+    const uint32_t r = list[idx];
+    const uint32_t ci = r / p.n_seeds;
+    const slo_knobs k = p.cfg[ci];                     // (K0 lists valid records only here)
+    const DevWorkload& W = p.wl[k.workload];
+    const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+    const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+    const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+    uint32_t gp;
+    __syncwarp();
+    if (lane == 0) R.wl = k.workload;
+    setup_replica<32, false>(R, W, k, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, gamma, gp, lane, FULL);
+    const uint32_t C = k.conc;
+    const uint64_t w = (k.max_num_seqs > k.conc) ? (uint64_t)k.max_wait_us : 0ull;
+    const bool closed = W.kind >= 3, spec = gamma > 0;
+    const uint32_t pre_base = W.t.pre_base_us, pre_tok = W.t.pre_tok_us, noise = W.t.noise_step_ppm;
+    uint64_t alpha0, alpha1;
+    step_coeffs(W.t, gamma, k.draft_width, alpha0, alpha1);
+    const uint64_t alpha = alpha0 + alpha1;           // d(1): one active sequence
+    const uint32_t rowoff = (r - p.r_base) * N;
+    const uint4* rec = p.rec + rowoff;
+    uint4 stg = (uint32_t)lane < N ? __ldcs(rec + lane) : uint4{0, 0, 0, 0};
+    uint64_t carry = 0;                                // t_{base - 1} (t_{-1} = 0: the idle server at t = 0)
+    uint64_t tprev = 0;                                // t of request (base - 32 + lane)
+    uint64_t a_w = 0, my_sum = 0, tlast = 0, tstar = 0;
+    uint32_t my_slo = 0, nmeas = 0, jstar = 0xFFFFFFFFu;
+    unsigned long long steps = 0, blocks = 0, dsteps = 0, batches = 0;
+    bool stopped = false;
+    for (uint32_t base = 0; base < N && !stopped; base += 32) {
+      const uint32_t i = base + (uint32_t)lane;
+      const bool valid = i < N;
+      const uint4 rc = stg;
+      if (base + 32u + (uint32_t)lane < N) stg = __ldcs(rec + base + 32u + lane);   // next step's records
+      const uint64_t x = valid ? (((uint64_t)rc.y << 32) | rc.x) : 0ull;
+      const uint64_t a = arrivals<32>(R, p.wl, R.wl, R.k0, R.k1, x, i, N, true, lane, lane);
+      const uint32_t P = rc.z & 0xFFFFu, S = rc.z >> 16;
+      const uint64_t f = noise_factor(rc.w, noise);
+      const uint64_t D = f * ((uint64_t)pre_base + (uint64_t)pre_tok * P) / 1000000u + f * (alpha * S) / 1000000u;
+      // inclusive max-plus scan of (A, Bv) = (w + D, a + w + D); invalid lanes carry the identity (0, 0)
+      uint64_t A = valid ? w + D : 0ull, Bv = valid ? a + w + D : 0ull;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t Ao = shfl_up64(A, d), Bo = shfl_up64(Bv, d);
+        if (lane >= d) {
+          const uint64_t nb = Bo + A;
+          Bv = nb > Bv ? nb : Bv;
+          A += Ao;
+        }
+      }
+      const uint64_t ca = carry + A;
+      const uint64_t t = ca > Bv ? ca : Bv;             // t_i = c_i
+      carry = shfl64(t, 31);                            // (invalid lanes keep the last valid t)
+      // issue instant s_i = max(a_i, t_{i-C}) (closed loops measure latency from it, §2.11)
+      const int src = lane - (int)C;
+      const uint64_t tc_in = shfl64(t, src & 31), tc_prev = shfl64(tprev, src & 31);
+      const uint64_t tC = i < C ? 0ull : (src >= 0 ? tc_in : tc_prev);
+      const uint64_t si = a > tC ? a : tC;
+      if (p.warmup >= base && p.warmup < base + 32u) a_w = shfl64(closed ? si : a, (int)(p.warmup - base));
+      const bool measured = valid && i >= p.warmup;
+      const uint64_t l = t - (closed ? si : a);
+      bool inc = true;
+      if constexpr (STOP) {                            // stop rule (§2.14): completion order = index order
+        const uint32_t need = p.stop_n ? p.stop_n : 1u;
+        const bool cand = measured && i - p.warmup + 1u >= need && t >= a_w + p.stop_t;
+        const uint32_t cm = __ballot_sync(FULL, cand);
+        if (cm) {
+          const int fl = __ffs(cm) - 1;
+          jstar = base + (uint32_t)fl;
+          tstar = shfl64(t, fl);
+          stopped = true;
+        }
+        inc = i <= jstar;
+      }
+      if (measured && inc) {
+        my_slo += (l <= p.slo_us);
+        my_slo |= (l > 0xFFFFFFFFull) ? 0x80000000u : 0u;
+        my_sum += l;
+        ++nmeas;
+      }
+      if (valid) p.lat[rowoff + i] = !inc ? 0xFFFFFFFFu : (l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l);
+      if (valid && inc) {                               // work counters: one batch per request
+        ++batches;
+        dsteps += S;
+        if (STOP) {
+          steps += S;
+          blocks += spec ? (S + 3u) >> 2 : 0u;
+        }
+      }
+      tprev = t;
+      tlast = carry;
+    }
+    if constexpr (STOP) {                              // never simulated past t*: sentinels for the rest
+      if (stopped) {
+        for (uint32_t j = (jstar & ~31u) + 32u + (uint32_t)lane; j < N; j += 32) p.lat[rowoff + j] = 0xFFFFFFFFu;
+      }
+    }
+    const uint32_t slo_met = __reduce_add_sync(FULL, my_slo & 0x7FFFFFFFu);
+    const uint64_t sum = warp_sum64(my_sum);
+    const bool sat = __any_sync(FULL, (my_slo >> 31) != 0);
+    const uint32_t n_meas = __reduce_add_sync(FULL, nmeas);
+    ct.batches += (uint32_t)batches;
+    ct.dsteps += (uint32_t)dsteps;
+    ct.steps += (uint32_t)steps;
+    ct.blocks += (uint32_t)blocks;
+    if (lane == 0) {
+      // the window ends at the last measured completion (t*, or t_{N-1}: completions are in index order)
+      const uint64_t Tw = (STOP && stopped ? tstar : tlast) - a_w;
+      const uint32_t fl = (sat ? 2u : 0u) | (STOP && !stopped ? 4u : 0u);
+      p.part[r] = slo_replica_result{0, slo_met, STOP ? n_meas : p.seg, fl, Tw < 1 ? 1 : Tw, sum};
+      if (p.stats) {
+        unsigned long long* st = (unsigned long long*)p.stats;
+        atomicAdd(st + 0, (unsigned long long)N);
+        atomicAdd(st + 4, (unsigned long long)(N + R.nphase));
+        atomicAdd(st + 5, 1ull);
+      }
+    }
+    if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u || ct.batches >= 0x40000000u) flush_counters(p, ct);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // K1c: continuous (iteration-level, vLLM-style) batching, DESIGN.md §2.12.
 //
 // A warp runs 32/G replicas at once, one per G-lane group with G >= min(C, B) (lane = one slot of the
@@ -1443,6 +1596,8 @@ __global__ void __maxnreg__(SLO_SERVE_MAXNREG) slo_serve_kernel_t(const SimParam
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
+  scan_mode<STOP>(p, kScanList, wsmem, lane, ct);   // min(C, B) = 1: a max-plus scan, 32 requests per step
+  serve_mode<4, STOP>(p, kG4List, wsmem, lane, ct);   // min(C, B) <= 4: eight replicas per warp
   serve_mode<8, STOP>(p, 0, wsmem, lane, ct);
   serve_mode<16, STOP>(p, 1, wsmem, lane, ct);
   serve_mode<32, STOP>(p, 2, wsmem, lane, ct);
@@ -1530,7 +1685,8 @@ size_t cont_warp_bytes() {
 }
 
 size_t serve_warp_bytes() {
-  size_t m = 4 * sizeof(SGroup<8>);
+  size_t m = 8 * sizeof(SGroup<4>);
+  if (4 * sizeof(SGroup<8>) > m) m = 4 * sizeof(SGroup<8>);
   if (2 * sizeof(SGroup<16>) > m) m = 2 * sizeof(SGroup<16>);
   if (sizeof(SGroup<32>) > m) m = sizeof(SGroup<32>);
   return m;
@@ -1549,11 +1705,24 @@ size_t group_warp_bytes() {
 // Expected cost ~ (batches per segment) x (cost per batch); a saturated replica runs ~N / min(C, B) batches
 // and a speculative batch costs ~3x a plain one.  bucket = floor(log2(beff^2)) (+3 ~ 2 log2 3 if not
 // speculative), so bucket 0 = most expensive; invalid records (no work) go last.
+#ifndef SLO_SCAN
+#define SLO_SCAN 1
+#endif
+#ifndef SLO_G4
+#define SLO_G4 1
+#endif
 __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWorkload* __restrict__ wl, uint32_t n_wl,
                                                uint32_t wide, uint32_t& bucket) {
+  const bool split = (wide & 4u) != 0;              // the split path (K1g + K1s) serves static batching
+  wide &= 3u;
   if (!knobs_valid(k, n_wl)) {
     bucket = 15;
     return 0;
+  }
+  // split path, min(C, B) = 1: every batch is one request, the chain a max-plus recursion (K1s scan_mode)
+  if (SLO_SCAN && split && !wl[k.workload].batching && wl[k.workload].kind != 4 && (k.conc == 1 || k.max_num_seqs == 1)) {
+    bucket = 0;
+    return (uint32_t)kScanList;
   }
   // static batching needs G >= min(C, B) lanes: a batch has b <= min(C, B) members, the issue window
   // only matters for them, and s_{h+B-1} is needed only when B <= C.  Narrow groups pack more replicas
@@ -1576,6 +1745,7 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
     const uint32_t cneed = wide ? (uint32_t)k.max_num_seqs : beff;
     return cneed <= 8 ? 3u : (cneed <= 16 ? 4u : 5u);
   }
+  if (SLO_G4 && split && need <= 4) return (uint32_t)kG4List;   // K1s: eight replicas per warp
   return need <= 8 ? 0u : (need <= 16 ? 1u : 2u);
 }
 

@@ -268,11 +268,12 @@ class Simulator:
         check(lib().slo_sim_profile(self.h, 1 if enable else 0), self.h)
 
     def profile_read(self) -> Dict:
-        """Summed ms of the recorded runs per kernel class {k0, k1g, sim, k1b} and the chunk count; clears them."""
-        ms = (C.c_double * 4)()
+        """Summed ms of the recorded runs: K0, K1g, the chain kernels, K1b and the simulation wall time (K1g and
+        the chains overlap when pipelined), and the chunk count; clears them."""
+        ms = (C.c_double * 5)()
         n = C.c_uint32(0)
         check(lib().slo_sim_profile_read(self.h, ms, C.byref(n)), self.h)
-        return {"k0_ms": ms[0], "gen_ms": ms[1], "sim_ms": ms[2], "k1b_ms": ms[3], "chunks": n.value}
+        return {"k0_ms": ms[0], "gen_ms": ms[1], "sim_ms": ms[2], "k1b_ms": ms[3], "wall_ms": ms[4], "chunks": n.value}
 
     def selftest(self, what: str, arg0: int = 0, arg1: int = 0, arg2: int = 0, stream=None) -> np.ndarray:
         """K6: exhaustive 2^32-input hashes / histograms of a transform (slo_selftest_transforms), as uint64."""
