@@ -390,7 +390,6 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   // 16 B of K1g records per request of the chunk
   if (split && (s = ensure(h, h->d_rec, h->rec_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
 
-  constexpr uint32_t kGenTile = slo::kGenThreads * slo::kGenPerThread;
   int gen_bps = 1, serve_bps = 1;
   const size_t serve_smem = slo::serve_warp_bytes() * h->warps_per_block;
   if (split) {
@@ -512,7 +511,9 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     const uint32_t wide = (h->group_policy == 3 ? 2u
                            : h->group_policy == 2 ? 1u
                            : h->group_policy == 1 ? 0u
-                           : nc <= (uint32_t)h->sm_count ? 2u : 0u) | (split ? 4u : 0u);   // bit 2: split path
+                           : nc <= (uint32_t)h->sm_count && !split ? 2u : 0u) | (split ? 4u : 0u);   // bit 2: split
+    // (a lone replica runs K1's inline generation fastest on a whole warp; K1s's chain is shortest on narrow
+    // groups, spread one replica per warp by gpw below)
     slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
                                                                     h->n_wl, wide, h->d_ctl);
     CUDA_TRY(h, cudaGetLastError());
@@ -533,9 +534,8 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       uint64_t gpw = (nc + slots - 1) / slots;
       if (gpw < 1) gpw = 1;
       if (gpw > 8) gpw = 8;
-      const uint32_t tpr = (N + kGenTile - 1) / kGenTile;
       uint64_t gblocks = (uint64_t)gen_bps * h->sm_count;
-      if (gblocks > (uint64_t)nc * tpr) gblocks = (uint64_t)nc * tpr;
+      if (gblocks > (uint64_t)nc * ((N + 255) / 256)) gblocks = (uint64_t)nc * ((N + 255) / 256);
       uint64_t sblocks = (uint64_t)serve_bps * h->sm_count;
       const uint64_t sneed = ((uint64_t)nc + gpw * h->warps_per_block - 1) / (gpw * h->warps_per_block);
       if (sblocks > sneed) sblocks = sneed;

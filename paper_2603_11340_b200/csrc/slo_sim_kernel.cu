@@ -324,7 +324,8 @@ __device__ __forceinline__ int gen_list(int q) { return q == 0 ? kScanList : q =
 __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(const SimParams p, uint4* __restrict__ rec) {
   __shared__ uint32_t s_tm1[16];
   __shared__ __align__(16) uint8_t s_guide[kGuideFine];
-  constexpr uint32_t TILE = kGenThreads * kGenPerThread;
+  // tile = rpt rounds of 256 requests: whole replicas per block in a large launch; a launch with fewer tiles of
+  // 2,048 requests than blocks takes one request per thread (C1: eight blocks instead of one)
   const uint32_t tid = threadIdx.x;
   const uint32_t N = p.warmup + p.seg;
   // a block takes whole replicas when the launch has enough of them to fill the grid (the guide is then rebuilt
@@ -337,9 +338,12 @@ __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(cons
   lo[0] = 0;
   for (int q = 0; q < 5; ++q) lo[q + 1] = lo[q] + p.counts[gen_list(q)];
   const uint32_t n_rep = lo[5];
+  const uint32_t big = kGenThreads * kGenPerThread;
+  const uint32_t rpt = (uint64_t)n_rep * ((N + big - 1) / big) >= gridDim.x ? (uint32_t)kGenPerThread : 1u;
+  const uint32_t TILE = kGenThreads * rpt;
   const uint32_t tpr0 = (N + TILE - 1) / TILE;
   const uint32_t tpr = (uint64_t)n_rep >= 2ull * gridDim.x ? 1u : tpr0;   // tiles per replica
-  const uint32_t rounds = tpr == 1 ? tpr0 : 1u;                                  // 2,048-request rounds per tile
+  const uint32_t rounds = tpr == 1 ? tpr0 * rpt : rpt;                     // 256-request rounds per tile
   const uint64_t total = (uint64_t)n_rep * tpr;
   uint32_t cur = 0xFFFFFFFFu, gp = 0, kind = 0, wl = 0, gkey = 0xFFFFFFFFu, rl = 0;
   bool spec = false;                                   // gamma_eff > 0: a SPEC stream is consumed (S_i blocks)
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(cons
     const DevWorkload& W = p.wl[wl];
     uint4* out = rec + (size_t)rl * N;
 #pragma unroll 1
-    for (uint32_t e = 0; e < rounds * (uint32_t)kGenPerThread; ++e) {
+    for (uint32_t e = 0; e < rounds; ++e) {
       const uint32_t i = tile * TILE + e * kGenThreads + tid;
       if (i >= N) break;
       // REQ block: arrival increment, lengths, noise word
@@ -942,19 +946,28 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
 
     // ---- (a6, a7) rank counting over the members' words: rank = #{m < b : w_m < w_li}, lts = the S of those
     // m; then sum_m min(S_m, S_li) = lts + S_li (b - rank) and the batch ends with the largest key (rank b - 1)
-    const uint32_t bmax = __reduce_max_sync(FULL, b);
     const uint32_t S = wj >> 18;
     uint32_t rank = 0, lts = 0, mrank = 0;
-#pragma unroll
-    for (int m = 0; m < G; ++m) {
-      if ((uint32_t)m >= bmax) break;
-      const uint32_t wm = __shfl_sync(FULL, wj, m, G);
-      const bool lt = (uint32_t)m < b && wm < wj;
+    uint32_t maxP = 0;
+    auto rank_step = [&](uint32_t m) {
+      const uint32_t wm = __shfl_sync(FULL, wj, (int)(m & (G - 1)), G);
+      const bool in = m < b, lt = in && wm < wj;
       rank += lt ? 1u : 0u;
       lts += lt ? wm >> 18 : 0u;
-      if (STOP) mrank += lt && h + (uint32_t)m >= p.warmup;   // measured completions before this one
+      if (G <= 8) maxP = max(maxP, in ? wm & 0x1FFFu : 0u);     // (wider groups: one reduction below)
+      if (STOP) mrank += lt && h + m >= p.warmup;   // measured completions before this one
+    };
+    if constexpr (G <= 8) {                            // straight-line (the shuffles do not wait for b)
+#pragma unroll
+      for (int m = 0; m < G; ++m) rank_step((uint32_t)m);
+    } else {                                           // four members per trip up to the warp's largest batch
+      const uint32_t bmax = __reduce_max_sync(FULL, b);
+      for (uint32_t m0 = 0; m0 < bmax; m0 += 4) {
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) rank_step(m0 + u);
+      }
+      maxP = gmax<G>(member ? wj & 0x1FFFu : 0u);
     }
-    const uint32_t maxP = gmax<G>(member ? wj & 0x1FFFu : 0u);
     const uint64_t f = R.f[h % RING];                  // the head's noise factor
     const uint64_t t0 = t_form + f * ((uint64_t)pre_base + (uint64_t)pre_tok * maxP) / 1000000u;
     const uint32_t summin = lts + S * (b - rank);
