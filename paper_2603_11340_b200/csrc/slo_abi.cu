@@ -382,7 +382,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   if (chunk > n_rep) chunk = n_rep;
   // static batching without think time runs the split path (K1g records, K1s chain) unless gen_policy = 1 asks
   // for K1's inline generation
-  const bool split = h->any_static_plain && h->gen_policy != 1;
+  const bool split = (h->any_static_plain || h->any_cont_plain) && h->gen_policy != 1;
   slo_status s;
   if ((s = ensure(h, h->d_lists, h->lists_cap, (size_t)slo::kLists * chunk, st)) != SLO_OK) return s;
   if (!d_lat && (s = ensure(h, h->d_lat, h->lat_cap, (size_t)chunk * N, st)) != SLO_OK) return s;
@@ -453,21 +453,27 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   if (h->any_cont || h->any_cont_think) {
     if (cont_smem > 48 * 1024)
     {
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
-      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)cont_smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)cont_smem));
+      CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cont_smem));
     }
     // occupancy is register-bound; give the group rings the whole carveout so smem never binds first
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel_t<false, false>, h->warps_per_block * 32,
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(h, cudaFuncSetAttribute(slo::slo_sim_cont_kernel_t<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cont_bps, slo::slo_sim_cont_kernel_t<false, false, false>, h->warps_per_block * 32,
                                                       cont_smem) != cudaSuccess || cont_bps < 1)
       cont_bps = 1;
     if (h->blocks_per_sm_opt > 0 && h->blocks_per_sm_opt < cont_bps) cont_bps = h->blocks_per_sm_opt;
@@ -547,8 +553,23 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       slo::SimParams ps = p;
       ps.gpw = (uint32_t)gpw;
       ps.warp_bytes = (uint32_t)slo::serve_warp_bytes();
-      stop ? slo::slo_serve_kernel_t<true><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps)
-           : slo::slo_serve_kernel_t<false><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps);
+      if (h->any_static_plain) {
+        stop ? slo::slo_serve_kernel_t<true><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps)
+             : slo::slo_serve_kernel_t<false><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps);
+        CUDA_TRY(h, cudaGetLastError());
+      }
+      if (h->any_cont_plain) {   // K1e: continuous batching with min(C, B) = 1, one replica per one-warp block
+        const size_t csm = slo::cscan_warp_bytes();
+        int occ = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slo::slo_cscan_kernel_t<false>, 32, csm) != cudaSuccess ||
+            occ < 1)
+          occ = 1;
+        uint64_t cb = (uint64_t)occ * h->sm_count;
+        if (cb > nc) cb = nc;
+        stop ? slo::slo_cscan_kernel_t<true><<<(unsigned)cb, 32, csm, st>>>(p)
+             : slo::slo_cscan_kernel_t<false><<<(unsigned)cb, 32, csm, st>>>(p);
+        CUDA_TRY(h, cudaGetLastError());
+      }
       p.rec = nullptr;
     } else {
       if ((s = mark(2, st)) != SLO_OK || (s = mark(3, st)) != SLO_OK || (s = mark(4, st)) != SLO_OK)
@@ -574,11 +595,16 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       pc.warp_bytes = (uint32_t)slo::cont_warp_bytes();
       const dim3 cg((unsigned)cblocks), cb(h->warps_per_block * 32);
       if (think)
-        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, true><<<cg, cb, cont_smem, st>>>(pc)
-                              : slo::slo_sim_cont_kernel_t<false, true><<<cg, cb, cont_smem, st>>>(pc);
-      else
-        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, false><<<cg, cb, cont_smem, st>>>(pc)
-                              : slo::slo_sim_cont_kernel_t<false, false><<<cg, cb, cont_smem, st>>>(pc);
+        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, true, false><<<cg, cb, cont_smem, st>>>(pc)
+                              : slo::slo_sim_cont_kernel_t<false, true, false><<<cg, cb, cont_smem, st>>>(pc);
+      else if (split) {   // lists 3-5 from K1g's records
+        pc.rec = h->d_rec;
+        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, false, true><<<cg, cb, cont_smem, st>>>(pc)
+                              : slo::slo_sim_cont_kernel_t<false, false, true><<<cg, cb, cont_smem, st>>>(pc);
+      } else {
+        (p.stop_n | p.stop_t) ? slo::slo_sim_cont_kernel_t<true, false, false><<<cg, cb, cont_smem, st>>>(pc)
+                              : slo::slo_sim_cont_kernel_t<false, false, false><<<cg, cb, cont_smem, st>>>(pc);
+      }
       CUDA_TRY(h, cudaGetLastError());
     }
     if ((s = mark(5, st)) != SLO_OK) return s;

@@ -12,12 +12,14 @@ constexpr int kDefaultWarpsPerBlock = 4;
 // 32 for a lone replica; K1), then continuous batching by G = 8, 16, 32 >= min(C, B) (wide: >= B) (K1c), then
 // closed loops with think time (kind 4) by G = 8, 16, 32 >= max(C, B): static (K1t), continuous (K1c, think)
 // and (split path only) list 12: static batching with min(C, B) = 1, every batch a single request (K1s's scan),
-// list 13: static batching with G = 4 >= min(C, B) (K1s, eight replicas per warp)
-constexpr int kLists = 14;
-constexpr int kScanList = 12, kG4List = 13;
+// list 13: static batching with G = 4 >= min(C, B) (K1s, eight replicas per warp), list 14: continuous batching
+// with min(C, B) = 1 (K1e's scan)
+constexpr int kLists = 15;
+constexpr int kScanList = 12, kG4List = 13, kCScanList = 14;
+constexpr int kGenLists = 9;   // K1g's lists: 12, 13, 0, 1, 2 (static), 14, 3, 4, 5 (continuous)
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
-constexpr int kCtlBucket = 32, kCtlWords = kCtlBucket + 2 * 16 * kLists;
+constexpr int kCtlBucket = 64, kCtlWords = kCtlBucket + 2 * 16 * kLists;
 
 struct DevWorkload {      // device copy of one slo_workload
   uint32_t kind, start_state;
@@ -56,11 +58,15 @@ struct SimParams {
 template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
 // K1s: the static-batching chain over K1g's request records (split path)
 template <bool STOP> __global__ void slo_serve_kernel_t(const SimParams p);
+// K1e: continuous batching with min(C, B) = 1 on the split path (a max-plus scan, one replica per warp)
+template <bool STOP> __global__ void slo_cscan_kernel_t(const SimParams p);
+size_t cscan_warp_bytes();
 // K1g: per-request records of the static-batching replicas (split path), one block per 2,048-request tile
 constexpr int kGenThreads = 256, kGenPerThread = 8;
 __global__ void slo_gen_kernel(const SimParams p, uint4* rec);
 // K1c: continuous batching (§2.12); THINK: the kind-4 (think-time) lists 9-11
-template <bool STOP, bool THINK> __global__ void slo_sim_cont_kernel_t(const SimParams p);
+// (SPLIT: lists 3-5 fed by K1g's records)
+template <bool STOP, bool THINK, bool SPLIT> __global__ void slo_sim_cont_kernel_t(const SimParams p);
 template <bool STOP> __global__ void slo_sim_think_kernel_t(const SimParams p); // K1t: think-time closed loop (§2.11)
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
                                           uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t wide,

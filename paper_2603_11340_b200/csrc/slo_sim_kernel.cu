@@ -302,7 +302,7 @@ __device__ __forceinline__ void generate(GR& R, const DevWorkload* __restrict__ 
 // walk and the batch chain.
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ bool split_static(const slo_knobs& k, const DevWorkload* __restrict__ wl, uint32_t n_wl) {
-  return knobs_valid(k, n_wl) && wl[k.workload].batching == 0 && wl[k.workload].kind != 4;
+  return knobs_valid(k, n_wl) && wl[k.workload].kind != 4;   // (K0 put it in one of K1g's lists)
 }
 
 #ifndef SLO_GEN_PAIR
@@ -316,7 +316,10 @@ __device__ __forceinline__ bool split_static(const slo_knobs& k, const DevWorklo
 #else
 #define GEN_PHILOX(c0, c1, c2, c3) philox(c0, c1, c2, c3, k0, k1)
 #endif
-__device__ __forceinline__ int gen_list(int q) { return q == 0 ? kScanList : q == 1 ? kG4List : q - 2; }
+// K1g's lists in K1s / K1e / K1c order: static scan, G = 4, 8, 16, 32; continuous scan, G = 8, 16, 32
+__device__ __forceinline__ int gen_list(int q) {
+  return q == 0 ? kScanList : q == 1 ? kG4List : q <= 4 ? q - 2 : q == 5 ? kCScanList : q - 3;
+}
 
 #ifndef SLO_GEN_MINB
 #define SLO_GEN_MINB 3
@@ -333,11 +336,10 @@ __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(cons
   // into 2,048-request tiles so every block has work
   // the replicas: this slice of the static split lists (K0's order: longest expected chains first, so the
   // records K1s needs first are written first)
-  // (lists in K1s's order: scan, G = 4, 8, 16, 32)
-  uint32_t lo[6];
+  uint32_t lo[kGenLists + 1];
   lo[0] = 0;
-  for (int q = 0; q < 5; ++q) lo[q + 1] = lo[q] + p.counts[gen_list(q)];
-  const uint32_t n_rep = lo[5];
+  for (int q = 0; q < kGenLists; ++q) lo[q + 1] = lo[q] + p.counts[gen_list(q)];
+  const uint32_t n_rep = lo[kGenLists];
   const uint32_t big = kGenThreads * kGenPerThread;
   const uint32_t rpt = (uint64_t)n_rep * ((N + big - 1) / big) >= gridDim.x ? (uint32_t)kGenPerThread : 1u;
   const uint32_t TILE = kGenThreads * rpt;
@@ -357,7 +359,8 @@ __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(cons
     const uint32_t en = (uint32_t)(tt / tpr), tile = (uint32_t)(tt - (uint64_t)en * tpr);
     if (en != cur) {                                   // block-uniform: a new replica
       cur = en;
-      const int q = en < lo[1] ? 0 : en < lo[2] ? 1 : en < lo[3] ? 2 : en < lo[4] ? 3 : 4;
+      int q = 0;
+      while (en >= lo[q + 1]) ++q;
       const uint32_t r = p.lists[(size_t)gen_list(q) * p.n_chunk + (en - lo[q])];
       rl = r - p.r_base;
       const uint32_t ci = r / p.n_seeds;
@@ -1070,8 +1073,13 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
 // never reaches B and the batch forms at s_h + max_wait).  x -> max(x + A, Bv) maps compose associatively,
 // (A1, B1) then (A2, B2) = (A1 + A2, max(B1 + A2, B2)), so a warp resolves 32 requests per step with a
 // 5-stage max-plus scan instead of 32 dependent batch iterations.  One replica per warp (G = 32).
+// CONT (list 14, continuous batching §2.12 with min(C, B) = 1): the running set never holds more than one
+// request, so request j runs alone — a prefill, then its S_j decode iterations it_j .. it_j + S_j - 1 of the
+// replica's decode counter (it_j = S_0 + .. + S_{j-1}, an exclusive scan) — and the same recursion holds with
+// w = 0 and D_j = floor(f_j (pre_base + pre_tok P_j) / 10^6) + sum_k floor(f_ITER(it_j + k) d(1) / 10^6): each
+// lane sums its request's iterations (one ITER Philox block each, the §2.12 draws).
 // ------------------------------------------------------------------------------------------------
-template <bool STOP>
+template <bool STOP, bool CONT = false>
 __device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   SGroup<32>& R = *reinterpret_cast<SGroup<32>*>(wsmem);  // arrival-process state (arrivals(), setup_replica())
   const uint32_t N = p.warmup + p.seg;
@@ -1094,7 +1102,7 @@ __device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* 
     if (lane == 0) R.wl = k.workload;
     setup_replica<32, false>(R, W, k, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, gamma, gp, lane, FULL);
     const uint32_t C = k.conc;
-    const uint64_t w = (k.max_num_seqs > k.conc) ? (uint64_t)k.max_wait_us : 0ull;
+    const uint64_t w = (!CONT && k.max_num_seqs > k.conc) ? (uint64_t)k.max_wait_us : 0ull;
     const bool closed = W.kind >= 3, spec = gamma > 0;
     const uint32_t pre_base = W.t.pre_base_us, pre_tok = W.t.pre_tok_us, noise = W.t.noise_step_ppm;
     uint64_t alpha0, alpha1;
@@ -1104,6 +1112,7 @@ __device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* 
     const uint4* rec = p.rec + rowoff;
     uint4 stg = (uint32_t)lane < N ? __ldcs(rec + lane) : uint4{0, 0, 0, 0};
     uint64_t carry = 0;                                // t_{base - 1} (t_{-1} = 0: the idle server at t = 0)
+    uint32_t itc = 0;                                  // CONT: decode iterations before this step's requests
     uint64_t tprev = 0;                                // t of request (base - 32 + lane)
     uint64_t a_w = 0, my_sum = 0, tlast = 0, tstar = 0;
     uint32_t my_slo = 0, nmeas = 0, jstar = 0xFFFFFFFFu;
@@ -1118,7 +1127,26 @@ __device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* 
       const uint64_t a = arrivals<32>(R, p.wl, R.wl, R.k0, R.k1, x, i, N, true, lane, lane);
       const uint32_t P = rc.z & 0xFFFFu, S = rc.z >> 16;
       const uint64_t f = noise_factor(rc.w, noise);
-      const uint64_t D = f * ((uint64_t)pre_base + (uint64_t)pre_tok * P) / 1000000u + f * (alpha * S) / 1000000u;
+      uint64_t D = f * ((uint64_t)pre_base + (uint64_t)pre_tok * P) / 1000000u;
+      if constexpr (CONT) {                             // S_j decode iterations alone, each with its ITER noise
+        uint32_t Sv = valid ? S : 0u, ex = Sv;          // exclusive scan of S over the lanes
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t o = __shfl_up_sync(FULL, ex, d);
+          if (lane >= d) ex += o;
+        }
+        const uint32_t it0 = itc + ex - Sv;
+        itc += __shfl_sync(FULL, ex, 31);
+        const uint32_t d1 = (uint32_t)alpha;            // d(1) < 2^31 (create-time check)
+        if (noise == 0) {
+          D += (uint64_t)d1 * Sv;
+        } else {
+          for (uint32_t q = 0; q < Sv; ++q)
+            D += (uint64_t)noise_factor(philox(it0 + q, 3, 0, 0, R.k0, R.k1).x, noise) * d1 / 1000000u;
+        }
+      } else {
+        D += f * (alpha * S) / 1000000u;
+      }
       // inclusive max-plus scan of (A, Bv) = (w + D, a + w + D); invalid lanes carry the identity (0, 0)
       uint64_t A = valid ? w + D : 0ull, Bv = valid ? a + w + D : 0ull;
 #pragma unroll
@@ -1161,9 +1189,10 @@ __device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* 
         ++nmeas;
       }
       if (valid) p.lat[rowoff + i] = !inc ? 0xFFFFFFFFu : (l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l);
-      if (valid && inc) {                               // work counters: one batch per request
+      if (valid && inc) {                               // work counters: one batch (prefill) per request
         ++batches;
         dsteps += S;
+        if (CONT && noise) blocks += S;                 // its ITER blocks
         if (STOP) {
           steps += S;
           blocks += spec ? (S + 3u) >> 2 : 0u;
@@ -1240,7 +1269,9 @@ struct alignas(16) CGroup {
 
 // THINK (kind 4, §2.11): the C pending user chains sit sorted in the lanes (lane l = request nq + l) and give
 // s_next and the prefill window in place of s_j = max(a_j, kappa_{j-C})
-template <int G, bool STOP, bool THINK>
+// SPLIT: the requests' attributes come from K1g's records (register-staged one refill ahead) instead of inline
+// generation (Philox REQ / SPEC blocks, lengths, S_i)
+template <int G, bool STOP, bool THINK, bool SPLIT = false>
 __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* wsmem, int lane, Counters& ct) {
   using CG = CGroup<G>;
   constexpr int RING = CG::RING, KRING = CG::KRING;
@@ -1264,6 +1295,32 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
   uint64_t origin = 0, my_sum = 0, my_cmax = 0;
   uint64_t pq = INF64;          // THINK: this lane's pending ready instant
   uint32_t pid = 0xFFFFFFFFu;   // THINK: its user chain id
+  uint4 stg{0, 0, 0, 0};        // SPLIT: K1g record of request gen + li, loaded one refill ahead
+  // requests [gen, gen + G) into the rings for the groups with `go` (all lanes execute)
+  auto refill = [&](bool go) {
+    if constexpr (SPLIT) {
+      const uint32_t i = gen + (uint32_t)li;
+      const bool valid = go && i < N;
+      const uint64_t x = valid ? (((uint64_t)stg.y << 32) | stg.x) : 0ull;
+      const uint64_t a = arrivals<G>(R, p.wl, R.wl, k0, k1, x, i, N, go, lane, li);
+      if (valid) {
+        R.a[i % RING] = a;
+        R.po[i % RING] = stg.z & 0xFFFFu;
+        R.w3[i % RING] = stg.w;
+        R.ss[i % RING] = (uint16_t)(stg.z >> 16);
+        if (i == p.warmup) R.a_w = a;
+      }
+      __syncwarp();
+      if (go) {
+        gen += G;
+        if (gen + (uint32_t)li < N) stg = __ldcs(p.rec + rowoff + gen + li);
+      }
+    } else {
+      generate<G>(R, p.wl, R.wl, p.tables, k0, k1, gen, N, p.warmup, go, lane, li);
+      if (go) gen += G;
+    }
+  };
+  constexpr uint32_t LOOK = SPLIT ? 2 * G : G;   // the split path refills one window ahead (record latency)
 
   for (;;) {
     __syncwarp();
@@ -1294,7 +1351,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             gamma = k.spec_on ? k.draft_len : 0u;
             uint32_t gp;
             if (li == 0) R.wl = k.workload;
-            setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
+            setup_replica<G, !SPLIT>(R, W, k, k0, k1, gamma, gp, li, gmask);
             C = k.conc;
             B = k.max_num_seqs;
             closed = W.kind >= 3;
@@ -1306,6 +1363,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             alpha0 = (uint32_t)R.alpha0;                 // d(n) = alpha0 + alpha1 n
             alpha1 = (uint32_t)R.alpha1;
             rowoff = (r - p.r_base) * N;
+            if constexpr (SPLIT) stg = (uint32_t)li < N ? __ldcs(p.rec + rowoff + li) : uint4{0, 0, 0, 0};
             t = 0;
             s_next = INF64;
             a_w = 0;
@@ -1329,8 +1387,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
     if (__any_sync(FULL, need_s)) {
       bool gn = need_s && gen < N && gen < nq + G;
       while (__any_sync(FULL, gn)) {
-        generate<G>(R, p.wl, R.wl, p.tables, k0, k1, gen, N, p.warmup, gn, lane, li);
-        if (gn) gen += G;
+        refill(need_s && gen < N && gen < nq + LOOK);
         gn = need_s && gen < N && gen < nq + G;
       }
       const uint64_t pq0 = gshfl64<G>(pq, 0);
@@ -1353,8 +1410,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
     if (__any_sync(FULL, pre)) {
       bool gn = pre && gen < N && gen < nq + G;          // the window [nq, nq + G) must be generated
       while (__any_sync(FULL, gn)) {
-        generate<G>(R, p.wl, R.wl, p.tables, k0, k1, gen, N, p.warmup, gn, lane, li);
-        if (gn) gen += G;
+        refill(pre && gen < N && gen < nq + LOOK);
         gn = pre && gen < N && gen < nq + G;
       }
       __syncwarp();
@@ -1484,8 +1540,10 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
             my_sum += l;
             my_cmax = t;
           }
-          ct.steps += stot;
-          ct.blocks += gamma > 0 ? (stot + 3u) >> 2 : 0u;
+          if (!SPLIT || STOP) {                          // (split, no stop rule: K1g counted them)
+            ct.steps += stot;
+            ct.blocks += gamma > 0 ? (stot + 3u) >> 2 : 0u;
+          }
           run = false;
         }
         if constexpr (THINK) {
@@ -1627,6 +1685,30 @@ __global__ void __maxnreg__(SLO_SERVE_MAXNREG) slo_serve_kernel_t(const SimParam
   }
 }
 
+// K1e: continuous batching with min(C, B) = 1 on the split path — scan_mode<CONT>, one replica per warp
+template <bool STOP>
+__global__ void __maxnreg__(SLO_SERVE_MAXNREG) slo_cscan_kernel_t(const SimParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * sizeof(SGroup<32>);
+  Counters ct{0, 0, 0, 0};
+  scan_mode<STOP, true>(p, kCScanList, wsmem, lane, ct);
+  if (p.stats) {
+    const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
+    const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
+    if (lane == 0) {
+      unsigned long long* st = (unsigned long long*)p.stats;
+      atomicAdd(st + 1, (unsigned long long)batches);
+      atomicAdd(st + 2, (unsigned long long)dsteps);
+      atomicAdd(st + 3, (unsigned long long)steps);
+      atomicAdd(st + 4, (unsigned long long)blocks);
+    }
+  }
+}
+size_t cscan_warp_bytes() { return sizeof(SGroup<32>); }
+template __global__ void slo_cscan_kernel_t<false>(const SimParams p);
+template __global__ void slo_cscan_kernel_t<true>(const SimParams p);
+
 // K1t: closed loops with think time (kind 4), launched only when a workload uses it
 template <bool STOP>
 __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_think_kernel_t(const SimParams p) {
@@ -1654,16 +1736,16 @@ __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_think_kernel_t(const SimParams 
 #ifndef SLO_CONT_MAXNREG
 #define SLO_CONT_MAXNREG 96
 #endif
-template <bool STOP, bool THINK>
+template <bool STOP, bool THINK, bool SPLIT>
 __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
   constexpr int l0 = THINK ? 9 : 3;   // THINK: the closed loops with think time (kind 4), lists 9-11
-  run_cont<8, STOP, THINK>(p, l0, wsmem, lane, ct);
-  run_cont<16, STOP, THINK>(p, l0 + 1, wsmem, lane, ct);
-  run_cont<32, STOP, THINK>(p, l0 + 2, wsmem, lane, ct);
+  run_cont<8, STOP, THINK, SPLIT>(p, l0, wsmem, lane, ct);
+  run_cont<16, STOP, THINK, SPLIT>(p, l0 + 1, wsmem, lane, ct);
+  run_cont<32, STOP, THINK, SPLIT>(p, l0 + 2, wsmem, lane, ct);
   if (p.stats) {
     const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
     const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
@@ -1685,10 +1767,12 @@ template __global__ void slo_serve_kernel_t<false>(const SimParams p);
 template __global__ void slo_serve_kernel_t<true>(const SimParams p);
 template __global__ void slo_sim_think_kernel_t<false>(const SimParams p);
 template __global__ void slo_sim_think_kernel_t<true>(const SimParams p);
-template __global__ void slo_sim_cont_kernel_t<false, false>(const SimParams p);
-template __global__ void slo_sim_cont_kernel_t<true, false>(const SimParams p);
-template __global__ void slo_sim_cont_kernel_t<false, true>(const SimParams p);
-template __global__ void slo_sim_cont_kernel_t<true, true>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<false, false, false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<true, false, false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<false, true, false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<true, true, false>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<false, false, true>(const SimParams p);
+template __global__ void slo_sim_cont_kernel_t<true, false, true>(const SimParams p);
 
 size_t cont_warp_bytes() {
   size_t m = 4 * sizeof(CGroup<8>);
@@ -1751,6 +1835,10 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
     const uint32_t tneed = wide == 2 ? 32u : max((uint32_t)k.conc, (uint32_t)k.max_num_seqs);
     const uint32_t base = wl[k.workload].batching ? 9u : 6u;
     return base + (tneed <= 8 ? 0u : (tneed <= 16 ? 1u : 2u));
+  }
+  if (split && wl[k.workload].batching && beff == 1) {   // split path, min(C, B) = 1: K1e's scan
+    bucket = 0;
+    return (uint32_t)kCScanList;
   }
   if (wl[k.workload].batching) {      // continuous batching, ~N*O/beff iterations: lane groups G >= min(C, B)
     // (at most min(C, B) requests run at once and a prefill admits at most that many; `wide`: G >= B)
