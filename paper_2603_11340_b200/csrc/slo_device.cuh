@@ -220,7 +220,7 @@ __device__ __forceinline__ void step_coeffs(const slo_timing& t, uint32_t gamma,
 // ---- batch noise factor: f = 10^6 + (b0 + b1 + b2 + b3 - 510) step ppm of a word's bytes
 // (step <= 1960, so f > 0); the head's w3 for a static batch or a prefill, an ITER word for a decode iteration
 __device__ __forceinline__ uint32_t noise_factor(uint32_t w, uint32_t step) {
-  const uint32_t bytesum = (w & 0xFF) + ((w >> 8) & 0xFF) + ((w >> 16) & 0xFF) + (w >> 24);
+  const uint32_t bytesum = (uint32_t)__dp4a(w, 0x01010101u, 0u);   // b0 + b1 + b2 + b3 in one IDP4A
   return (uint32_t)(1000000 + ((int32_t)bytesum - 510) * (int32_t)step);
 }
 

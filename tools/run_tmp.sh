@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_think.py -m gpu -q -x -k "continuous or stop_rule or think" > gpurun_out/t_cont.log 2>&1; tail -30 gpurun_out/t_cont.log | grep -E "passed|failed|Error|assert" | head -10
-python bench.py --workload c2c --no-cpu-baseline --steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernel_ms_per_step']; print('c2c', round(d['value']/1e9,3), round(d['ms_per_step'],3), 'gen', round(k['k1g_generate'],3), 'chain', round(k['chain'],3), 'k1b', round(k['k1b_select'],3))"
-python bench.py --workload c2c --no-cpu-baseline --steps 3 --gen-policy 1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernel_ms_per_step']; print('c2c inline', round(d['value']/1e9,3), round(d['ms_per_step'],3), 'gen', round(k['k1g_generate'],3), 'chain', round(k['chain'],3), 'k1b', round(k['k1b_select'],3))"
-python tools/c2c_subsets.py
+timeout 600 python -m pytest tests/test_gpu_exhaustive.py -m gpu -q -x -k noise 2>&1 | tail -1
+bash tools/ab.sh "base dp c80 c88" c2c
+bash tools/ab.sh "base dp" c2
