@@ -309,11 +309,15 @@ def main():
     k1_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k1_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     st_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    # K0 count + K0 classify + K1 simulate + K1b select + K2 aggregate (+ K2b for N>1 sweeps, K3 for the climb)
-    launches_per_step = 5 + (1 if (world > 1 and args.workload != "c4" and not strong) else 0) + \
+    # K0 count + K0 classify + simulation + K1b select + K2 aggregate (+ K2b for N>1 sweeps, K3 for the climb);
+    # simulation on the split path (gen_policy != 1): K1g + K1s (static) / K1g + K1c (continuous; K1e inside),
+    # inline: K1 (static) / K1c (continuous)
+    split = args.gen_policy != 1
+    cont = any(w.get("batching", 0) for w in cfg.workloads)
+    static = any(not w.get("batching", 0) for w in cfg.workloads)
+    n_sim = (1 + (1 if static else 0) + (1 if cont else 0)) if split else ((1 if static else 0) + (1 if cont else 0))
+    launches_per_step = 4 + n_sim + (1 if (world > 1 and args.workload != "c4" and not strong) else 0) + \
         (1 if args.workload == "c4" else 0)
-    if any(w.get("batching", 0) for w in cfg.workloads):
-        launches_per_step += 1                                          # K1c (continuous batching)
 
     # N > 1: the aggregate exchange through the peers' windows (K2x/K2w, NEXT-4), NCCL as the fallback
     xchg, exchange_desc = None, None
@@ -339,7 +343,7 @@ def main():
         graph = ClimbGraph(S, cfg, seeds, n_cand=n_cfg, exchange=args.exchange).capture()   # one graph per step
         out_eager = out                                                 # (the untimed per-kernel profile pass)
         out = graph.out                                                 # (replayed on the current stream)
-        launches_per_step = 6 + (1 if graph.xchg is not None else 0)    # K0 x2, K1, K1b, K2 (K2x+K2w), K3
+        launches_per_step = 5 + n_sim + (1 if graph.xchg is not None else 0)   # K0 x2, sim, K1b, K2 (K2x+K2w), K3
 
     def step(i=None):
         if graph is not None:
@@ -510,35 +514,76 @@ def main():
         pk = peaks()
         blocks = int(stats["philox_blocks"])
         peak_gops = 148 * 4 * 32 * pk["sm_max_mhz"] * 1e6 / 1e9      # lane-ops/s at 1 warp-instr/clk/SMSP
-        # the dominant kernel's own time: the simulation kernels' CUDA events over the timed launches
-        achieved_gops = blocks * OPS_PER_PHILOX_BLOCK / (t_sim / args.steps) / 1e9
         # K4: measured Philox4x32-10 throughput of this GPU at full occupancy (untimed, after the run)
         rng_peak_gops = S.philox_peak() * OPS_PER_PHILOX_BLOCK / 1e9
+        # the Philox blocks each kernel draws: K1g the REQ and SPEC blocks of every request; the chain kernels the
+        # ITER blocks of continuous batching (one per noisy decode iteration, §2.12) and the PHASE blocks of MMPP-2
+        iter_blocks = int(stats["decode_steps"]) if (cont and any(w["timing"]["noise_step_ppm"] for w in cfg.workloads)) else 0
+        gen_blocks = blocks - iter_blocks if t_gen > 0 else 0
+        chain_blocks = blocks - gen_blocks
+        # the dominant kernel (its own CUDA-event time over the timed launches) carries the roofline; a static chain
+        # kernel that dominates (latency-bound launches: C1, C4) draws no Philox blocks of its own, so there the
+        # simulation as a whole (K1g + K1s, its CUDA-event span) is the unit
+        dom_gen = t_gen >= t_chain
+        whole = not dom_gen and chain_blocks == 0
+        t_dom = (t_gen if dom_gen else (t_sim if whole else t_chain)) / args.steps
+        dom_blocks = gen_blocks if dom_gen else (blocks if whole else chain_blocks)
+        achieved_gops = dom_blocks * OPS_PER_PHILOX_BLOCK / t_dom / 1e9
+        sim_gops = blocks * OPS_PER_PHILOX_BLOCK / (t_sim / args.steps) / 1e9
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-                traffic = json.load(fh).get(args.workload)
+                traffic = json.load(fh).get(args.workload + (":k1g" if dom_gen else ":chain"))
         except Exception:
             pass
-        # BASELINE's "% SM issue / HBM peak": issue-slot utilisation of the dominant kernel from its committed
-        # ncu summary, and the HBM share of this run (ncu bytes per step over the live kernel time)
-        issue_util = None
-        try:
+        # BASELINE's "% SM issue / HBM peak": issue-slot utilisation of the kernels from their committed ncu
+        # summaries (profiles/r02_*_ncu.json), and the HBM share of this run (ncu bytes over the live kernel time)
+        def ncu_issue(tag):
             import glob
-            pat = "r0*_k1c_v*_c2c_ncu.json" if args.workload == "c2c" else "r0*_k1_v*_c2_ncu.json"
-            fs = sorted(glob.glob(os.path.join(ROOT, "profiles", pat)),
-                        key=lambda f: (os.path.basename(f)[:3], int(f.rsplit("_v", 1)[1].split("_")[0])))
-            if fs:
+            fs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r02_{tag}_ncu.json")))
+            if not fs:
+                return None
+            try:
                 with open(fs[-1]) as fh:
                     m = json.load(fh)["metrics"]
-                issue_util = {"pct_of_peak": float(m["sm__inst_issued.avg.pct_of_peak_sustained_active"][0]),
-                              "source": os.path.relpath(fs[-1], ROOT)}
-        except Exception:
-            issue_util = None
+                return {"pct_of_peak": float(m["sm__inst_issued.avg.pct_of_peak_sustained_active"][0]),
+                        "source": os.path.relpath(fs[-1], ROOT)}
+            except Exception:
+                return None
+        wl_tag = "c2c" if args.workload == "c2c" else "c2"
+        chain_tag = ("k1c" if cont else "k1s") if split else ("k1c" if cont else "k1")
         hbm = None
         if traffic:
-            gbs = traffic / (t_sim / args.steps) / 1e9
+            gbs = traffic / t_dom / 1e9
             hbm = {"gb_per_s": gbs, "peak_gb_per_s": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
+        gen_name = "K1g slo_gen_kernel (per-request generation: Philox REQ + SPEC blocks, E_q, lengths, S_i)"
+        chain_name = ("K1c slo_sim_cont_kernel_t (continuous-batching chains, K1e scans inside)" if cont else
+                      "K1s slo_serve_kernel_t (static-batching chains)") if split else \
+                     ("K1c slo_sim_cont_kernel_t" if cont else "K1 slo_sim_kernel_t (inline generation + chain)")
+        roofline = {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
+                    "frac": achieved_gops / peak_gops, "traffic": traffic,
+                    "kernel": (gen_name if dom_gen else (("the simulation: K1g + " + chain_name) if whole else chain_name))
+                              + ", its own CUDA-event time",
+                    "dominant_kernel_share_of_step": t_dom * args.steps / t_total,
+                    "issue_util_ncu": ncu_issue(("k1g_" + wl_tag) if dom_gen else (chain_tag + "_" + wl_tag)),
+                    "hbm": hbm,
+                    "note": "algorithmic int32 lane-ops = the Philox4x32-10 blocks the definition consumes (counted "
+                            "exactly by the kernels) that this kernel draws x 60; peak = 148 SM x 4 SMSP x 32 lanes x "
+                            "sm_max_mhz (issue limit)",
+                    "measured_rng_peak": rng_peak_gops,
+                    "frac_of_measured_rng_peak": achieved_gops / rng_peak_gops,
+                    "measured_rng_peak_note": "K4 slo_philox_peak: Philox blocks/s x 60 of a full-occupancy kernel "
+                                              "that only draws blocks (the RNG roofline of DESIGN.md §7)",
+                    "kernels": {
+                        "k1g": {"ms_per_step": 1000.0 * t_gen / args.steps, "philox_blocks": gen_blocks,
+                                "frac_of_measured_rng_peak": (gen_blocks * OPS_PER_PHILOX_BLOCK / (t_gen / args.steps)
+                                                              / 1e9 / rng_peak_gops) if t_gen > 0 else None,
+                                "issue_util_ncu": ncu_issue("k1g_" + wl_tag) if t_gen > 0 else None},
+                        "chain": {"kernel": chain_name, "ms_per_step": 1000.0 * t_chain / args.steps,
+                                  "philox_blocks": chain_blocks, "issue_util_ncu": ncu_issue(chain_tag + "_" + wl_tag)},
+                        "simulation": {"ms_per_step": 1000.0 * t_sim / args.steps, "achieved": sim_gops,
+                                       "frac": sim_gops / peak_gops,
+                                       "frac_of_measured_rng_peak": sim_gops / rng_peak_gops}}}
         line = {
             "metric": "simulated requests/s", "value": value, "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps,
@@ -562,19 +607,7 @@ def main():
             "work_per_step_per_gpu": {"philox_blocks": blocks, "batches": int(stats["batches"]),
                                       "member_steps": int(stats["member_steps"]),
                                       "decode_steps": int(stats["decode_steps"])},
-            "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
-                         "frac": achieved_gops / peak_gops, "traffic": traffic,
-                         "dominant_kernel_share_of_step": t_sim / t_total,
-                         "issue_util_ncu": issue_util, "hbm": hbm,
-                         "kernel": ("K1c slo_sim_cont_kernel_t (continuous-batching simulation), its own CUDA-event "
-                                    "time" if args.workload == "c2c" else
-                                    "K1 slo_sim_kernel_t (static-batching simulation), its own CUDA-event time"),
-                         "note": "algorithmic int32 lane-ops = Philox4x32-10 blocks the definition consumes x 60; "
-                                 "peak = 148 SM x 4 SMSP x 32 lanes x sm_max_mhz (issue limit)",
-                         "measured_rng_peak": rng_peak_gops,
-                         "frac_of_measured_rng_peak": achieved_gops / rng_peak_gops,
-                         "measured_rng_peak_note": "K4 slo_philox_peak: Philox blocks/s x 60 of a full-occupancy "
-                                                   "kernel that only draws blocks (the RNG roofline of DESIGN.md §7)"},
+            "roofline": roofline,
             "gpu_launches": launches_per_step * args.steps,
             **({"exchange_error": x_err} if world > 1 else {}),
             **({"pareto": pareto} if pareto is not None else {}),

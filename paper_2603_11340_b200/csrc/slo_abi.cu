@@ -558,18 +558,6 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
              : slo::slo_serve_kernel_t<false><<<(unsigned)sblocks, h->warps_per_block * 32, serve_smem, st>>>(ps);
         CUDA_TRY(h, cudaGetLastError());
       }
-      if (h->any_cont_plain) {   // K1e: continuous batching with min(C, B) = 1, one replica per one-warp block
-        const size_t csm = slo::cscan_warp_bytes();
-        int occ = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slo::slo_cscan_kernel_t<false>, 32, csm) != cudaSuccess ||
-            occ < 1)
-          occ = 1;
-        uint64_t cb = (uint64_t)occ * h->sm_count;
-        if (cb > nc) cb = nc;
-        stop ? slo::slo_cscan_kernel_t<true><<<(unsigned)cb, 32, csm, st>>>(p)
-             : slo::slo_cscan_kernel_t<false><<<(unsigned)cb, 32, csm, st>>>(p);
-        CUDA_TRY(h, cudaGetLastError());
-      }
       p.rec = nullptr;
     } else {
       if ((s = mark(2, st)) != SLO_OK || (s = mark(3, st)) != SLO_OK || (s = mark(4, st)) != SLO_OK)
@@ -588,7 +576,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     // K1c over the continuous-batching lists (one launch for lists 3-5, one for the think-time lists 9-11)
     for (uint32_t think = 0; think < 2; ++think) {
       if (!(think ? h->any_cont_think : h->any_cont_plain)) continue;
-      uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;
+      uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;   // (one replica per warp at most: the K1e scans)
       const uint64_t cneed = ((uint64_t)nc + h->warps_per_block - 1) / h->warps_per_block;
       if (cblocks > cneed) cblocks = cneed;
       pc = p;

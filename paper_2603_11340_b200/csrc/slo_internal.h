@@ -58,14 +58,11 @@ struct SimParams {
 template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
 // K1s: the static-batching chain over K1g's request records (split path)
 template <bool STOP> __global__ void slo_serve_kernel_t(const SimParams p);
-// K1e: continuous batching with min(C, B) = 1 on the split path (a max-plus scan, one replica per warp)
-template <bool STOP> __global__ void slo_cscan_kernel_t(const SimParams p);
-size_t cscan_warp_bytes();
 // K1g: per-request records of the static-batching replicas (split path), one block per 2,048-request tile
 constexpr int kGenThreads = 256, kGenPerThread = 8;
 __global__ void slo_gen_kernel(const SimParams p, uint4* rec);
 // K1c: continuous batching (§2.12); THINK: the kind-4 (think-time) lists 9-11
-// (SPLIT: lists 3-5 fed by K1g's records)
+// (SPLIT: lists 3-5 fed by K1g's records, and first list 14, continuous min(C, B) = 1, by the max-plus scan K1e)
 template <bool STOP, bool THINK, bool SPLIT> __global__ void slo_sim_cont_kernel_t(const SimParams p);
 template <bool STOP> __global__ void slo_sim_think_kernel_t(const SimParams p); // K1t: think-time closed loop (§2.11)
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,

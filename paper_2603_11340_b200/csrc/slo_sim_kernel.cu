@@ -1685,30 +1685,6 @@ __global__ void __maxnreg__(SLO_SERVE_MAXNREG) slo_serve_kernel_t(const SimParam
   }
 }
 
-// K1e: continuous batching with min(C, B) = 1 on the split path — scan_mode<CONT>, one replica per warp
-template <bool STOP>
-__global__ void __maxnreg__(SLO_SERVE_MAXNREG) slo_cscan_kernel_t(const SimParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int lane = threadIdx.x & 31;
-  uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * sizeof(SGroup<32>);
-  Counters ct{0, 0, 0, 0};
-  scan_mode<STOP, true>(p, kCScanList, wsmem, lane, ct);
-  if (p.stats) {
-    const uint64_t steps = warp_sum64(ct.steps), blocks = warp_sum64(ct.blocks);
-    const uint64_t batches = warp_sum64(ct.batches), dsteps = warp_sum64(ct.dsteps);
-    if (lane == 0) {
-      unsigned long long* st = (unsigned long long*)p.stats;
-      atomicAdd(st + 1, (unsigned long long)batches);
-      atomicAdd(st + 2, (unsigned long long)dsteps);
-      atomicAdd(st + 3, (unsigned long long)steps);
-      atomicAdd(st + 4, (unsigned long long)blocks);
-    }
-  }
-}
-size_t cscan_warp_bytes() { return sizeof(SGroup<32>); }
-template __global__ void slo_cscan_kernel_t<false>(const SimParams p);
-template __global__ void slo_cscan_kernel_t<true>(const SimParams p);
-
 // K1t: closed loops with think time (kind 4), launched only when a workload uses it
 template <bool STOP>
 __global__ void __maxnreg__(SLO_MAXNREG) slo_sim_think_kernel_t(const SimParams p) {
@@ -1743,6 +1719,9 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimPar
   uint8_t* wsmem = smem + (size_t)(threadIdx.x >> 5) * p.warp_bytes;
   Counters ct{0, 0, 0, 0};
   constexpr int l0 = THINK ? 9 : 3;   // THINK: the closed loops with think time (kind 4), lists 9-11
+  // split path: the min(C, B) = 1 replicas' max-plus scans first (K1e, one replica per warp; their chains are
+  // the longest), then the fast-forward lists
+  if constexpr (SPLIT && !THINK) scan_mode<STOP, true>(p, kCScanList, wsmem, lane, ct);
   run_cont<8, STOP, THINK, SPLIT>(p, l0, wsmem, lane, ct);
   run_cont<16, STOP, THINK, SPLIT>(p, l0 + 1, wsmem, lane, ct);
   run_cont<32, STOP, THINK, SPLIT>(p, l0 + 2, wsmem, lane, ct);
@@ -1775,7 +1754,8 @@ template __global__ void slo_sim_cont_kernel_t<false, false, true>(const SimPara
 template __global__ void slo_sim_cont_kernel_t<true, false, true>(const SimParams p);
 
 size_t cont_warp_bytes() {
-  size_t m = 4 * sizeof(CGroup<8>);
+  size_t m = sizeof(SGroup<32>);              // (the split path's continuous scan, K1e)
+  if (4 * sizeof(CGroup<8>) > m) m = 4 * sizeof(CGroup<8>);
   if (2 * sizeof(CGroup<16>) > m) m = 2 * sizeof(CGroup<16>);
   if (sizeof(CGroup<32>) > m) m = sizeof(CGroup<32>);
   return m;
