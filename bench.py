@@ -211,6 +211,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N>1 sweeps: strong = the BASELINE grid config-sharded over ranks (SURVEY §8(e)); "
                          "weak = every rank runs the full grid on its own seed block")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="latency-bound sweeps (<= 4 replicas per SM): stream launches instead of a CUDA-graph replay")
     ap.add_argument("--share-of", type=int, default=1,
                     help="N=1 only: time rank 0's share of a W-GPU partition of the workload on this one GPU (no "
                          "exchange) — the per-rank step of a W-GPU run, for strong-scaling analysis")
@@ -345,7 +347,24 @@ def main():
         out = graph.out                                                 # (replayed on the current stream)
         launches_per_step = 5 + n_sim + (1 if graph.xchg is not None else 0)   # K0 x2, sim, K1b, K2 (K2x+K2w), K3
 
+    # a latency-bound sweep (at most four replicas per SM: C1) replays one captured CUDA graph per step
+    # (dist.SweepGraph) instead of its seven stream launches; per-kernel times then come from an eager replay
+    sweep_graph = None
+    if graph is None and world == 1 and R <= 4 * info["sm_count"] and not args.no_graph:
+        from paper_2603_11340_b200.dist import SweepGraph
+        sweep_graph = SweepGraph(S, cands, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us).capture()
+        out_eager, out = out, sweep_graph.out                          # (the graph writes its own outputs)
+        launches_per_step = 4 + n_sim                                   # K0 x2, simulation, K1b, K2
+
     def step(i=None):
+        if sweep_graph is not None:
+            if i is not None:
+                k1_start[i].record(stream)
+            sweep_graph.graph.replay()
+            if i is not None:
+                k1_end[i].record(stream)
+                st_end[i].record(stream)
+            return
         if graph is not None:
             if i is not None:
                 k1_start[i].record(stream)
@@ -416,16 +435,16 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         extended = int(te.item())
     prof = None
-    if graph is None:
+    if graph is None and sweep_graph is None:
         prof = S.profile_read()    # exactly the timed steps' K0 / simulation / K1b launches
         S.profile(False)
     for _ in range(extended):
         step()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    if graph is not None:
+    if graph is not None or sweep_graph is not None:
         # the graph's launches record no events: time the same kernels on the same candidates eagerly
-        gc = graph.evaluated
+        gc = graph.evaluated if graph is not None else cands
         S.run_batch(gc, seeds_t, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out_eager, stream=stream)
         torch.cuda.synchronize()
         S.profile(True)
@@ -595,6 +614,8 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write, untimed); inputs are < 1 MB",
                        "parallelism": f"dp{world} over replicas ({'seed-sharded climb' if args.workload == 'c4' else ('config-sharded: config c on rank c mod N, all seeds local' if strong else 'weak: full grid, per-rank seed block')})",
                        "exchange": exchange_desc,
+                       "cuda_graph": ("ClimbGraph (one Alg. 1 step per replay)" if graph is not None else
+                                      "SweepGraph (one sweep step per replay)" if sweep_graph is not None else None),
                        "launch": {"blocks_per_sm": info["blocks_per_sm"], "warps_per_block": info["warps_per_block"],
                                   "regs_per_thread": info["regs_per_thread"]}},
             "replica_segments_per_s": (req_all // N) * args.steps / t_total,
@@ -602,8 +623,8 @@ def main():
             "kernel_ms_per_step": {"simulate": 1000.0 * t_sim / args.steps, "k1g_generate": 1000.0 * t_gen / args.steps,
                                    "chain": 1000.0 * t_chain / args.steps, "k1b_select": 1000.0 * t_k1b / args.steps,
                                    "source": "CUDA events around each launch (slo_sim_profile) on the launching "
-                                             "stream, " + ("the timed launches" if graph is None else
-                                                           "an eager replay of the graph's launches")},
+                                             "stream, " + ("the timed launches" if (graph is None and sweep_graph is None)
+                                                           else "an eager replay of the graph's launches")},
             "work_per_step_per_gpu": {"philox_blocks": blocks, "batches": int(stats["batches"]),
                                       "member_steps": int(stats["member_steps"]),
                                       "decode_steps": int(stats["decode_steps"])},

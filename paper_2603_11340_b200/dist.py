@@ -111,6 +111,42 @@ class PeerExchange:
             self.x = None
 
 
+class SweepGraph:
+    """One sweep step — K0/K1g/K1s (or K1/K1c)/K1b simulate and K2 aggregate — captured once in a CUDA graph
+    on a handle of its own (the graph holds pointers into that handle's scratch) and replayed: a latency-bound
+    launch (C1: one replica) then pays one graph launch instead of seven stream launches per step."""
+
+    def __init__(self, sim, knobs: torch.Tensor, seeds: torch.Tensor, segment_len: int, warmup_len: int = 0,
+                 slo_us: int = 1_200_000):
+        self.sim = sim.twin()
+        self.knobs, self.seeds = knobs, seeds
+        self.n_cfg, self.n_seeds = knobs.shape[0], seeds.shape[0]
+        self.args = (segment_len, warmup_len, slo_us)
+        self.out = self.sim.alloc_outputs(self.n_cfg * self.n_seeds, detail=True, stats=True)
+        self.agg = torch.empty((self.n_cfg, 32), dtype=torch.uint8, device=knobs.device)
+        self.stream = torch.cuda.Stream(device=knobs.device)
+        self.graph = None
+
+    def _step(self):
+        self.sim.run_batch(self.knobs, self.seeds, *self.args, out=self.out, stream=self.stream)
+        self.sim.aggregate(self.out["detail"], self.n_cfg, self.n_seeds, out=self.agg, stream=self.stream)
+
+    def capture(self):
+        """Warm up (allocates the library's scratch), then capture one step."""
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            self._step()
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._step()
+        return self
+
+    def close(self):
+        self.graph = None
+        self.sim.close()
+
+
 class ClimbGraph:
     """Alg. 1 with the whole step — K0/K1/K1b simulate, K2 aggregate, all-gather (N > 1), K3 climb — captured
     once in a CUDA graph and replayed (SV §8(f) NEXT-4): no host round trip between steps.  The candidate

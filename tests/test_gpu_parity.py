@@ -356,9 +356,10 @@ def _wls_cont():
             c(inputs.workload(kind=0, rate=200.0, timing=dict(inputs.LL_TIMING, noise_step_ppm=0), stream_id=5))]
 
 
+@pytest.mark.parametrize("gen", [1, 2], ids=["inline", "split"])
 @pytest.mark.parametrize("policy", [1, 2], ids=["narrow", "wide"])
 @pytest.mark.parametrize("block", range(6))
-def test_continuous_random_configs(S, orc, block, policy):
+def test_continuous_random_configs(S, orc, block, policy, gen):
     """Continuous batching: random knob records over every arrival kind (incl. the closed loop), noise on
     and off, speculation, several 32-request windows, ragged tails and warmup — every latency, p50/p95/p99,
     goodput and the work counters bit-exact against the oracle's iteration-level event loop."""
@@ -377,7 +378,7 @@ def test_continuous_random_configs(S, orc, block, policy):
     seeds = inputs.seeds(3, 31 * block)
     N = rng.choice([37, 333, 1000, 1234])
     warmup = rng.choice([0, 0, 17, 100])
-    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup, group_policy=policy)
+    g = _run_gpu(S, wls, ks, seeds, N, warmup=warmup, group_policy=policy, gen_policy=gen)
     tot = dict(batches=0, decode_steps=0, member_steps=0, philox_blocks=0)
     for ci, k in enumerate(ks):
         for si, sd in enumerate(seeds):
