@@ -1,14 +1,19 @@
 // slo_sim_kernel.cu — the simulation kernels of libslosim.
 //
-//  K0 slo_classify_kernel : sorts replicas into work lists by lane-group size G in {8, 16, 32} (static:
-//                           G >= min(C, B) narrow / max(C, B) wide / 32; continuous: G >= min(C, B) or B).
-//  K1 slo_sim_kernel      : persistent; a warp runs 32/G replicas at once, one per G-lane group, with every
-//                           collective (ballot, shuffle, scan, sort) scoped to the group. Per-group shared
-//                           memory holds rings of arrival times a_j, completion times kappa_k, packed (P, O),
-//                           decode step counts S_j, noise words, acceptance thresholds and the arrival-process
-//                           state. Every request's latency goes to an HBM scratch row.
-//  K1c slo_sim_cont_kernel: the same for continuous (iteration-level) batching, decode iterations
-//                           fast-forwarded to the next event.
+//  K0 slo_classify_kernel : sorts replicas into work lists by lane-group size and chain kind, each list in 16
+//                           cost buckets (longest expected chains first).
+//  The split path (default; slo_sim_opts.gen_policy):
+//  K1g slo_gen_kernel     : per-request generation at full width — Philox REQ block (arrival increment, P, O,
+//                           noise word) and the SPEC blocks that resolve the step count S_i — written as one
+//                           16-B record per request.
+//  K1s slo_serve_kernel   : the static-batching chain over the records; 32/G replicas per warp (G = 4 .. 32),
+//                           completion order and costs by rank counting, own-lane latencies; min(C, B) = 1 by
+//                           a 32-request max-plus scan (scan_mode).
+//  K1c slo_sim_cont_kernel: continuous (iteration-level) batching, decode iterations fast-forwarded to the next
+//                           event (SPLIT: over K1g's records; its warps first run K1e, the min(C, B) = 1 scans).
+//  The inline path (gen_policy = 1) and the think-time loops:
+//  K1 slo_sim_kernel      : persistent; a warp runs 32/G replicas at once, one per G-lane group, generation
+//                           inline, the batch order by a bitonic network.  K1t: its think-time instantiation.
 //  K1b slo_select_kernel  : per replica, the exact nearest-rank p99 (p50, p95) of the measured latencies by
 //                           an 8-bit radix select over the row (L2-resident; shared-memory staging is kept for
 //                           callers passing smem_vals > 0); writes p99 and goodput.
@@ -17,8 +22,9 @@
 // checked bit-exactly against the oracle):
 //   s_j = max(a_j, kappa_{j-C});  t_form = max(t_idle, s_h[, min(s_h + max_wait, s_{h+B-1})]);
 //   b = min(B, #{j in [h, h+C) : s_j <= t_form});
-//   Cum_m = alpha0 S_m + alpha1 sum_{m'} min(S_m', S_m); completion order = order of S_m;
-//   S_m depends on request m's own SPEC stream only, so it is resolved at generation (lane-parallel).
+//   Cum_m = alpha0 S_m + alpha1 sum_{m'} min(S_m', S_m); completion order = order of (S_m, m);
+//   S_m depends on request m's own SPEC stream only, so it is resolved at generation;
+//   min(C, B) = 1: t_j = max(t_{j-1} + w, a_j + w) + D_j, a max-plus scan.
 #include <cstdint>
 
 #include "slo_device.cuh"

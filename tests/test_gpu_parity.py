@@ -332,6 +332,28 @@ def test_climb_cuda_graph_matches_eager(S):
     s.close()
 
 
+def test_sweep_graph_matches_eager(S):
+    """dist.SweepGraph (bench.py's replay for latency-bound sweeps): the captured run + aggregation replayed gives
+    the same per-replica outputs and per-config aggregates, bit for bit, as the eager calls."""
+    from paper_2603_11340_b200.dist import SweepGraph
+    rng = random.Random(44)
+    wls = _wls()
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(12)] + [inputs.knobs(conc=8, max_num_seqs=16)]
+    seeds = inputs.seeds(3, 9)
+    s = S.Simulator(wls, device=0)
+    kt, st = S.knobs_tensor(ks), S.seeds_tensor(seeds)
+    out = s.run_batch(kt, st, 700, warmup_len=20, slo_us=900_000)
+    agg = s.aggregate(out["detail"], len(ks), len(seeds))
+    g = SweepGraph(s, kt, st, 700, 20, 900_000).capture()
+    for _ in range(3):
+        g.graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out["p99_us"], g.out["p99_us"]) and torch.equal(out["goodput"], g.out["goodput"])
+    assert torch.equal(out["detail"], g.out["detail"]) and torch.equal(agg, g.agg)
+    g.close()
+    s.close()
+
+
 def test_short_segment_window_ends_at_last_measured_completion(S, orc):
     """Segments shorter than a batch with warmup: the goodput window T ends at the last MEASURED completion
     (DESIGN.md §2.8), which can precede a warmup member's completion in the same final batch."""
