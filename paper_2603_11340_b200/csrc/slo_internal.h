@@ -13,10 +13,10 @@ constexpr int kDefaultWarpsPerBlock = 4;
 // closed loops with think time (kind 4) by G = 8, 16, 32 >= max(C, B): static (K1t), continuous (K1c, think)
 // and (split path only) list 12: static batching with min(C, B) = 1, every batch a single request (K1s's scan),
 // list 13: static batching with G = 4 >= min(C, B) (K1s, eight replicas per warp), list 14: continuous batching
-// with min(C, B) = 1 (K1e's scan)
-constexpr int kLists = 15;
-constexpr int kScanList = 12, kG4List = 13, kCScanList = 14;
-constexpr int kGenLists = 9;   // K1g's lists: 12, 13, 0, 1, 2 (static), 14, 3, 4, 5 (continuous)
+// with min(C, B) = 1 (K1e's scan), list 15: continuous batching with G = 4 >= min(C, B) (K1c)
+constexpr int kLists = 16;
+constexpr int kScanList = 12, kG4List = 13, kCScanList = 14, kCG4List = 15;
+constexpr int kGenLists = 10;  // K1g's lists: 12, 13, 0, 1, 2 (static), 14, 15, 3, 4, 5 (continuous)
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 // control words: list lengths [kLists], K1 cursors [kLists], K0 per-(list, bucket) counts and cursors
 constexpr int kCtlBucket = 64, kCtlWords = kCtlBucket + 2 * 16 * kLists;

@@ -322,9 +322,9 @@ __device__ __forceinline__ bool split_static(const slo_knobs& k, const DevWorklo
 #else
 #define GEN_PHILOX(c0, c1, c2, c3) philox(c0, c1, c2, c3, k0, k1)
 #endif
-// K1g's lists in K1s / K1e / K1c order: static scan, G = 4, 8, 16, 32; continuous scan, G = 8, 16, 32
+// K1g's lists in K1s / K1e / K1c order: static scan, G = 4, 8, 16, 32; continuous scan, G = 4, 8, 16, 32
 __device__ __forceinline__ int gen_list(int q) {
-  return q == 0 ? kScanList : q == 1 ? kG4List : q <= 4 ? q - 2 : q == 5 ? kCScanList : q - 3;
+  return q == 0 ? kScanList : q == 1 ? kG4List : q <= 4 ? q - 2 : q == 5 ? kCScanList : q == 6 ? kCG4List : q - 4;
 }
 
 #ifndef SLO_GEN_MINB
@@ -1727,7 +1727,10 @@ __global__ void __maxnreg__(SLO_CONT_MAXNREG) slo_sim_cont_kernel_t(const SimPar
   constexpr int l0 = THINK ? 9 : 3;   // THINK: the closed loops with think time (kind 4), lists 9-11
   // split path: the min(C, B) = 1 replicas' max-plus scans first (K1e, one replica per warp; their chains are
   // the longest), then the fast-forward lists
-  if constexpr (SPLIT && !THINK) scan_mode<STOP, true>(p, kCScanList, wsmem, lane, ct);
+  if constexpr (SPLIT && !THINK) {
+    scan_mode<STOP, true>(p, kCScanList, wsmem, lane, ct);
+    run_cont<4, STOP, THINK, SPLIT>(p, kCG4List, wsmem, lane, ct);
+  }
   run_cont<8, STOP, THINK, SPLIT>(p, l0, wsmem, lane, ct);
   run_cont<16, STOP, THINK, SPLIT>(p, l0 + 1, wsmem, lane, ct);
   run_cont<32, STOP, THINK, SPLIT>(p, l0 + 2, wsmem, lane, ct);
@@ -1761,6 +1764,7 @@ template __global__ void slo_sim_cont_kernel_t<true, false, true>(const SimParam
 
 size_t cont_warp_bytes() {
   size_t m = sizeof(SGroup<32>);              // (the split path's continuous scan, K1e)
+  if (8 * sizeof(CGroup<4>) > m) m = 8 * sizeof(CGroup<4>);
   if (4 * sizeof(CGroup<8>) > m) m = 4 * sizeof(CGroup<8>);
   if (2 * sizeof(CGroup<16>) > m) m = 2 * sizeof(CGroup<16>);
   if (sizeof(CGroup<32>) > m) m = sizeof(CGroup<32>);
@@ -1794,6 +1798,9 @@ size_t group_warp_bytes() {
 #ifndef SLO_G4
 #define SLO_G4 1
 #endif
+#ifndef SLO_CG4
+#define SLO_CG4 1
+#endif
 __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWorkload* __restrict__ wl, uint32_t n_wl,
                                                uint32_t wide, uint32_t& bucket) {
   const bool split = (wide & 4u) != 0;              // the split path (K1g + K1s) serves static batching
@@ -1825,6 +1832,10 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
   if (split && wl[k.workload].batching && beff == 1) {   // split path, min(C, B) = 1: K1e's scan
     bucket = 0;
     return (uint32_t)kCScanList;
+  }
+  if (SLO_CG4 && split && wl[k.workload].batching && !wide && beff <= 4) {   // K1c, eight replicas per warp
+    bucket = min(14u, (31u - __clz(beff)) + (spec ? 0u : 2u));
+    return (uint32_t)kCG4List;
   }
   if (wl[k.workload].batching) {      // continuous batching, ~N*O/beff iterations: lane groups G >= min(C, B)
     // (at most min(C, B) requests run at once and a prefill admits at most that many; `wide`: G >= B)
