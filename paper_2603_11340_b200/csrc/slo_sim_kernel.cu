@@ -226,6 +226,7 @@ template <int G, class GR>
 __device__ __forceinline__ uint64_t arrivals(GR& R, const DevWorkload* __restrict__ wls, uint32_t wl, uint32_t k0,
                                              uint32_t k1, uint64_t x, uint32_t i, uint32_t N, bool go, int lane,
                                              int li) {
+  __syncwarp();     // the previous call's R.last / phase-state writes are visible to every lane
   const uint32_t kind = go ? R.kind : 0u;
   const uint64_t last = go ? R.last : 0ull;
   const uint64_t sc = last + gscan64<G>(x, li);     // kind 0: a_i; kinds 1, 2: tau_i; kind 3: 0

@@ -1,2 +1,3 @@
-SLO_SIM_LIB=$PWD/paper_2603_11340_b200/libslosim_cg4.so timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "continuous" 2>&1 | tail -1
-bash tools/ab.sh "cg4 nocg4" c2c
+mkdir -p gpurun_out
+bash tools/sanitize.sh
+bash tools/ab.sh "x" c2 2>/dev/null; python bench.py --workload c2 --no-cpu-baseline --steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernel_ms_per_step']; print('c2', round(d['ms_per_step'],3), 'gen', round(k['k1g_generate'],3), 'chain', round(k['chain'],3))"

@@ -1,4 +1,5 @@
-"""Tiny run of every kernel (K0, K1, K1t and K1c in all three lane-group modes, K1b, K2, K2b, K3) for compute-sanitizer."""
+"""Tiny run of every kernel (K0, K1g, K1s incl. its scans, K1, K1t and K1c in all lane-group modes, K1b, K2, K2b,
+K3) for compute-sanitizer."""
 import random
 import sys
 
@@ -16,8 +17,11 @@ ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(24)] + [inputs.knob
 ks += [inputs.knobs(max_num_seqs=b, conc=c, workload=w, draft_len=4, spec_on=1) for b, c, w in
        ((4, 12, 4), (12, 3, 5), (32, 32, 6), (8, 8, 8), (32, 32, 9), (3, 5, 10), (12, 6, 9), (6, 20, 11),
                       (32, 32, 11))]
-for pol in (1, 2):   # narrow (G >= min(C, B)) and wide (G >= max(C, B)) lane groups
-    sp = sim.Simulator(wls, device=0, group_policy=pol)
+# min(C, B) = 1 (the K1s / K1e max-plus scans) and <= 4 (G = 4 groups), static and continuous
+ks += [inputs.knobs(max_num_seqs=b, conc=c, workload=w, draft_len=3, spec_on=1, max_wait_us=mw) for b, c, w, mw in
+       ((1, 9, 0, 0), (7, 1, 0, 20_000), (1, 1, 2, 0), (3, 4, 0, 0), (1, 5, 4, 0), (6, 1, 6, 0), (4, 2, 5, 0))]
+for pol, gen in ((1, 2), (2, 2), (1, 1)):   # narrow / wide lane groups, split (K1g + K1s / K1c) / inline K1
+    sp = sim.Simulator(wls, device=0, group_policy=pol, gen_policy=gen)
     sp.run_batch(sim.knobs_tensor(ks), sim.seeds_tensor(inputs.seeds(3)), 150, warmup_len=10, latencies=True,
                  stats=True)
     torch.cuda.synchronize()
