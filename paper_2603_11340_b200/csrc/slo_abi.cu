@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "slo_internal.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: host ranges around each launch phase (nsys / ncu timelines)
 
 static_assert(sizeof(slo_knobs) == 32, "slo_knobs must be 32 B");
 static_assert(sizeof(slo_replica_result) == 32, "slo_replica_result must be 32 B");
@@ -83,6 +84,11 @@ slo_status fail(slo_sim* h, slo_status s, const char* fmt, ...) {
     cudaError_t e_ = (call);                                                                \
     if (e_ != cudaSuccess) return fail((h), SLO_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
+
+struct NvtxRange {               // scoped NVTX range (free when no profiler is attached)
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
   int prev = -1;
@@ -509,6 +515,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     p.n_chunk = nc;
     p.lists = h->d_lists;
     p.lat = d_lat ? d_lat + r0 * N : h->d_lat;
+    NvtxRange chunk_range("slo_sim_run chunk");
     if ((s = mark(0, st)) != SLO_OK) return s;
     CUDA_TRY(h, cudaMemsetAsync(h->d_ctl, 0, sizeof(uint32_t) * slo::kCtlWords, st));
     // lane groups: narrow (G >= min(C, B), up to four replicas per warp) by default — measured best from
@@ -547,9 +554,12 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       if (sblocks > sneed) sblocks = sneed;
       if (sblocks < 1) sblocks = 1;
       if ((s = mark(2, st)) != SLO_OK) return s;
+      nvtxRangePushA("K1g generate");
       slo::slo_gen_kernel<<<(unsigned)gblocks, slo::kGenThreads, 0, st>>>(p, h->d_rec);
       CUDA_TRY(h, cudaGetLastError());
+      nvtxRangePop();
       if ((s = mark(3, st)) != SLO_OK || (s = mark(4, st)) != SLO_OK) return s;
+      NvtxRange chain_range("K1s chains");
       slo::SimParams ps = p;
       ps.gpw = (uint32_t)gpw;
       ps.warp_bytes = (uint32_t)slo::serve_warp_bytes();
@@ -574,6 +584,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       CUDA_TRY(h, cudaGetLastError());
     }
     // K1c over the continuous-batching lists (one launch for lists 3-5, one for the think-time lists 9-11)
+    NvtxRange cont_range("K1c continuous");
     for (uint32_t think = 0; think < 2; ++think) {
       if (!(think ? h->any_cont_think : h->any_cont_plain)) continue;
       uint64_t cblocks = (uint64_t)cont_bps * h->sm_count;   // (one replica per warp at most: the K1e scans)
@@ -597,7 +608,9 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     }
     if ((s = mark(5, st)) != SLO_OK) return s;
     const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
+    nvtxRangePushA("K1b select");
     slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
+    nvtxRangePop();
     CUDA_TRY(h, cudaGetLastError());
     if ((s = mark(6, st)) != SLO_OK) return s;
   }
