@@ -55,6 +55,7 @@ struct slo_sim {
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
   int regs = 0;
+  int sel_bps = 1;                  // K1b resident blocks per SM (its grid: sel_bps x SMs, one wave)
   bool pinned = false;              // scratch referenced by a captured CUDA graph: never regrown (ensure())
   // measurement hook (slo_sim_profile): events around each chunk's K0 | simulation kernels | K1b
   bool profile = false;
@@ -280,6 +281,9 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     return fail(nullptr, SLO_E_DEVICE, "create: no sm_100a kernel image for device %d", device);
   }
   h->regs = fa.numRegs;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->sel_bps, slo::slo_select_kernel, 256, 0) != cudaSuccess ||
+      h->sel_bps < 1)
+    h->sel_bps = 1;
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
@@ -486,8 +490,6 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   }
   // K1b reads each row from L2 (a just-written row stays there across the radix passes): staging rows of up
   // to 43 KB in shared memory capped residency at 5 blocks/SM and measured 1.5 % slower on C2
-  const uint32_t sel_vals = 0u;
-  const size_t sel_smem = (256u + sel_vals) * sizeof(uint32_t);
   if (d_stats) CUDA_TRY(h, cudaMemsetAsync(d_stats, 0, sizeof(slo_stats), st));
   bool prof = h->profile;
   if (prof) {                                     // no event marks inside a graph capture
@@ -607,9 +609,11 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
       CUDA_TRY(h, cudaGetLastError());
     }
     if ((s = mark(5, st)) != SLO_OK) return s;
-    const uint32_t sel_blocks = nc < (uint32_t)h->sm_count * 8u ? nc : (uint32_t)h->sm_count * 8u;
+    // one wave of resident blocks: a grid-stride second wave would start its rows late
+    const uint32_t sel_wave = (uint32_t)h->sm_count * (uint32_t)h->sel_bps;
+    const uint32_t sel_blocks = nc < sel_wave ? nc : sel_wave;
     nvtxRangePushA("K1b select");
-    slo::slo_select_kernel<<<sel_blocks, 256, sel_smem, st>>>(p, sel_vals);
+    slo::slo_select_kernel<<<sel_blocks, 256, 0, st>>>(p);
     nvtxRangePop();
     CUDA_TRY(h, cudaGetLastError());
     if ((s = mark(6, st)) != SLO_OK) return s;

@@ -70,7 +70,7 @@ __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkloa
                                           uint32_t* ctl);
 __global__ void slo_classify_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds, uint32_t r_base,
                                     uint32_t n_chunk, uint32_t n_wl, uint32_t wide, uint32_t* ctl, uint32_t* lists);
-__global__ void slo_select_kernel(const SimParams p, uint32_t smem_vals);
+__global__ void slo_select_kernel(const SimParams p);
 size_t group_warp_bytes();   // per-warp shared memory of K1
 size_t serve_warp_bytes();   // per-warp shared memory of K1s
 size_t cont_warp_bytes();    // per-warp shared memory of K1c

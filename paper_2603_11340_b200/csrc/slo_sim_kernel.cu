@@ -14,9 +14,9 @@
 //  The inline path (gen_policy = 1) and the think-time loops:
 //  K1 slo_sim_kernel      : persistent; a warp runs 32/G replicas at once, one per G-lane group, generation
 //                           inline, the batch order by a bitonic network.  K1t: its think-time instantiation.
-//  K1b slo_select_kernel  : per replica, the exact nearest-rank p99 (p50, p95) of the measured latencies by
-//                           an 8-bit radix select over the row (L2-resident; shared-memory staging is kept for
-//                           callers passing smem_vals > 0); writes p99 and goodput.
+//  K1b slo_select_kernel  : per replica, the exact nearest-rank p99 (p50, p95) of the measured latencies: a
+//                           log-scale histogram pass over the row, the selected bucket copied into shared
+//                           memory by a second pass and ranked there; writes p99 and goodput.
 //
 // The event loop is replaced by the closed forms of DESIGN.md §2.6 (equal to the event definition;
 // checked bit-exactly against the oracle):
@@ -29,6 +29,18 @@
 
 #include "slo_device.cuh"
 #include "slo_internal.h"
+
+#ifdef SLO_K1C_PROF   // profiling builds only (tools/k1c_prof.py): K1c pass statistics
+__device__ unsigned long long g_k1c_prof[16];
+#define KPROF(i, v) do { if (v) atomicAdd(&g_k1c_prof[i], (unsigned long long)(v)); } while (0)
+extern "C" int slo_debug_k1c_prof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_k1c_prof, sizeof(g_k1c_prof)) != cudaSuccess) return -1;
+  if (reset) { unsigned long long z[16] = {}; cudaMemcpyToSymbol(g_k1c_prof, z, sizeof(z)); }
+  return 0;
+}
+#else
+#define KPROF(i, v) do { } while (0)
+#endif
 
 namespace slo {
 
@@ -1353,6 +1365,9 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
     }
     if (!__any_sync(FULL, active)) break;
     __syncwarp();   // setup / previous iteration's ring writes before this iteration's reads
+    if (lane == 0) KPROF(0, 1u);
+    if (li == 0) KPROF(1, active ? 1u : 0u);
+    if (li == 0) KPROF(2, need_s ? 1u : 0u);
 
     // ---- s_next = s_{nq} for groups whose nq or gate changed; keep [nq, nq + G) generated
     if (__any_sync(FULL, need_s)) {
@@ -1379,6 +1394,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
 
     // ---- prefill iteration: admit the first k queued requests into free slots (§2.12)
     if (__any_sync(FULL, pre)) {
+      if (lane == 0) KPROF(10, 1u);
+      if (li == 0) KPROF(3, pre ? 1u : 0u);
       bool gn = pre && gen < N && gen < nq + G;          // the window [nq, nq + G) must be generated
       while (__any_sync(FULL, gn)) {
         refill(pre && gen < N && gen < nq + LOOK);
@@ -1453,6 +1470,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       const bool nz = dec && noise != 0;
       // noise window of 2G decode iterations: lane li holds positions li (fw) and G + li (fw2) after nzc used
       if (__any_sync(FULL, nz && nzc > (uint32_t)G)) {       // pooled shift-refill once half of it is used
+        if (lane == 0) KPROF(8, 1u);
         const uint32_t sA = (uint32_t)li + nzc, sB = (uint32_t)(G + li) + nzc;   // old positions of the new ones
         const uint32_t a0 = __shfl_sync(FULL, fw, (int)(sA & (G - 1)), G);
         const uint32_t b0 = __shfl_sync(FULL, fw2, (int)(sA & (G - 1)), G);
@@ -1490,6 +1508,14 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
       const uint32_t i0 = m0 ? 2u * (uint32_t)(__ffs(m0) - 1) : 0xFFFFu, i1 = m1 ? 2u * (uint32_t)(__ffs(m1) - 1) + 1u : 0xFFFFu;
       if (m0 | m1) K = min(i0, i1) + 1u;                  // the first such iteration end
       const uint64_t tK = gshfl64<G>(((K - 1u) & 1u) ? end1 : end0, (int)(((K - 1u) >> 1) & (G - 1)));
+      if (lane == 0) KPROF(11, 1u);
+      if (li == 0 && dec) {
+        KPROF(4, 1u);
+        KPROF(5, K);
+        KPROF(7, (m0 | m1) ? 1u : 0u);
+        KPROF(14, K == 2u * G ? 1u : 0u);
+        KPROF(13, nrun);
+      }
       bool fin = false;
       if (dec) {
         t += tK;
@@ -1500,8 +1526,14 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           fin = sleft == 0;
         }
       }
+#ifdef SLO_K1C_PROF
+      const uint32_t pf_fin = gballot<G>(fin, lane);
+      if (li == 0) KPROF(6, (dec && pf_fin) ? 1u : 0u);
+#endif
       if (__any_sync(FULL, fin)) {
         const uint32_t nf = __popc(gballot<G>(fin, lane));
+        if (lane == 0) KPROF(12, 1u);
+        if (li == 0) KPROF(9, nf);
         if (fin) {                                       // (a8) completion at t
           const uint64_t l = t - origin;
           p.lat[rowoff + mi] = l > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)l;
@@ -1578,6 +1610,10 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
 
     // ---- groups that finished their replica: outputs (p99 and goodput follow in K1b)
     const bool done = active && ndone >= N;
+#ifdef SLO_K1C_PROF
+    const uint32_t pf_act = __popc(__ballot_sync(FULL, active && li == 0));
+    if (lane == 0) KPROF(15, pf_act);
+#endif
     if (__any_sync(FULL, done)) {
       const uint32_t slo_met = gsum<G>(my_slo & 0x7FFFFFFFu);
       const uint64_t sum = gsum64<G>(my_sum);
@@ -1845,13 +1881,101 @@ __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, const Dev
 }
 
 // ------------------------------------------------------------------------------------------------
-// K1b: exact nearest-rank p99 by shared-memory radix select; goodput (Eq. 1)
+// K1b: exact nearest-rank p99 (p50, p95) by radix select; goodput (Eq. 1)
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint32_t smem_vals) {
-  extern __shared__ __align__(16) uint32_t sv[];   // [256 hist][smem_vals values]
-  uint32_t* hist = sv;
-  uint32_t* vals = sv + 256;
-  __shared__ uint32_t s_digit, s_kk;
+// Pass 1 histograms every value of the row by a log-scale digit (its highest set bit and the 4 bits below
+// it: 464 bins, monotone in the value, each bucket a contiguous range whose values share all bits above bit
+// t - 4, t = the highest set bit), which finds the bucket holding the wanted rank with a relative width of
+// 1/16.  Pass 2 copies that bucket's values into shared memory (when they fit, kSelCap; for LL rows the 99th
+// percentile's bucket holds a few dozen values): <= 256 of them are ranked by direct counting, more by 8-bit
+// radix passes in shared memory.  A bucket that does not fit continues with 8-bit radix passes over the row.
+constexpr uint32_t kSelCap = 1024, kLogBins = 512;
+
+__device__ __forceinline__ uint32_t log_bin(uint32_t v) {   // v < 16: v; else 16 + 16 (t - 4) + 4 bits below t
+  const uint32_t t = 31u - (uint32_t)__clz(v | 1u);
+  return v < 16u ? v : 16u * (t - 3u) + ((v >> (t - 4u)) & 15u);
+}
+
+// every value of a global row, 16-B loads two deep per thread when the row is 16-B aligned (the loop is
+// bound by load latency, not by bytes: a plain scalar loop keeps one load in flight per thread)
+template <class F>
+__device__ __forceinline__ void for_row(const uint32_t* __restrict__ row, uint32_t n, F f) {
+  const uint32_t bs = blockDim.x;
+  uint32_t e0 = 0;
+  if ((reinterpret_cast<uintptr_t>(row) & 15u) == 0) {
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+    const uint32_t n4 = n >> 2;
+    for (uint32_t e = threadIdx.x; e < n4; e += 2 * bs) {
+      const uint4 a = r4[e];
+      const bool hb = e + bs < n4;
+      const uint4 b = hb ? r4[e + bs] : uint4{0, 0, 0, 0};
+      f(a.x); f(a.y); f(a.z); f(a.w);
+      if (hb) { f(b.x); f(b.y); f(b.z); f(b.w); }
+    }
+    e0 = n4 << 2;
+  }
+  for (uint32_t e = e0 + threadIdx.x; e < n; e += bs) f(row[e]);
+}
+
+// warp 0: the bin holding the kk-th largest of hist[0, 8 * 32 * per) (per bins per lane, suffix sums over the
+// lanes); writes the bin, the rank inside it and its count
+template <int PER>
+__device__ __forceinline__ void find_bin(const uint32_t* hist, uint32_t kk, uint32_t* s_dig, uint32_t* s_kk,
+                                         uint32_t* s_cnt) {
+  const int lane = threadIdx.x;
+  uint32_t c[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    c[q] = hist[lane * PER + q];
+    sum += c[q];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_down_sync(FULL, incl, d);
+    if (lane + d < 32) incl += v;
+  }
+  if (incl >= kk && incl - sum < kk) {
+    uint32_t above = incl - sum, dg = 0, kn = 0, cnt = 0;
+#pragma unroll
+    for (int q = PER - 1; q >= 0; --q) {
+      if (kn == 0 && above + c[q] >= kk) {
+        dg = (uint32_t)(PER * lane + q);
+        kn = kk - above;
+        cnt = c[q];
+      }
+      above += c[q];
+    }
+    *s_dig = dg;
+    *s_kk = kn;
+    *s_cnt = cnt;
+  }
+}
+
+// one 8-bit radix pass: digit (v >> sh) & (2^w - 1) over the values of src whose bits >= sh + w equal those of
+// prefix; returns the digit holding the kk-th largest and updates kk to the rank inside it
+__device__ __forceinline__ uint32_t select_pass(const uint32_t* src, uint32_t n, uint32_t prefix, uint32_t sh,
+                                                uint32_t w, uint32_t& kk, uint32_t* hist, uint32_t* s_dig,
+                                                uint32_t* s_kk, uint32_t* s_cnt) {
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t hs = sh + w;                      // bits >= hs must match the prefix
+  const uint32_t dm = (1u << w) - 1u;
+  for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const uint32_t v = src[e];
+    if (hs >= 32 || (v >> hs) == (prefix >> hs)) atomicAdd(hist + ((v >> sh) & dm), 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) find_bin<8>(hist, kk, s_dig, s_kk, s_cnt);
+  __syncthreads();
+  kk = *s_kk;
+  return *s_dig;
+}
+
+__global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p) {
+  __shared__ uint32_t hist[kLogBins];
+  __shared__ uint32_t cand[kSelCap];
+  __shared__ uint32_t s_digit, s_kk, s_cnt, s_m, s_res;
   const uint32_t N = p.warmup + p.seg;
   const uint32_t n = p.seg;                        // row length (stop rule: uncounted entries hold UINT32_MAX)
 
@@ -1869,61 +1993,64 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p, uint
       continue;
     }
     const uint32_t* row = p.lat + (size_t)t * N + p.warmup;
-    const bool staged = n <= smem_vals;
-    if (staged) {
-      for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) vals[e] = row[e];
-    }
     uint32_t res[3];
     const uint32_t nq = (p.p50 || p.p95) ? 3u : 1u;
     for (uint32_t qi = 0; qi < nq; ++qi) {          // p99, then p50 and p95 (nearest rank, ceil(q n))
-    // nearest rank among the nm counted latencies; the n - nm uncounted ones are UINT32_MAX (the top), so the
-    // rq-th smallest counted value is the (n - rq + 1)-th largest of the row
-    const uint32_t nm = pr.n_measured;
-    const uint32_t rq = (uint32_t)(((qi == 0 ? 99ull : qi == 1 ? 50ull : 95ull) * nm + 99ull) / 100ull);
-    uint32_t prefix = 0, kk = n - rq + 1;
-    for (int shift = 24; shift >= 0; shift -= 8) {
+      // nearest rank among the nm counted latencies; the n - nm uncounted ones are UINT32_MAX (the top), so
+      // the rq-th smallest counted value is the (n - rq + 1)-th largest of the row
+      const uint32_t nm = pr.n_measured;
+      const uint32_t rq = (uint32_t)(((qi == 0 ? 99ull : qi == 1 ? 50ull : 95ull) * nm + 99ull) / 100ull);
+      uint32_t kk = n - rq + 1;
+      // pass 1: log-scale histogram of the row
       hist[threadIdx.x] = 0;
+      hist[threadIdx.x + 256] = 0;
+      if (threadIdx.x == 0) s_m = 0;
       __syncthreads();
-      const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-      for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
-        const uint32_t v = staged ? vals[e] : row[e];
-        if ((v & hmask) == prefix) atomicAdd(hist + ((v >> shift) & 255u), 1u);
-      }
+      for_row(row, n, [&](uint32_t v) { atomicAdd(hist + log_bin(v), 1u); });
       __syncthreads();
-      if (threadIdx.x < 32) {  // warp 0: suffix sums over 8 bins per lane, find the digit
-        const int lane = threadIdx.x;
-        uint32_t c[8], sum = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          c[q] = hist[lane * 8 + q];
-          sum += c[q];
-        }
-        uint32_t incl = sum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t v = __shfl_down_sync(FULL, incl, d);
-          if (lane + d < 32) incl += v;
-        }
-        if (incl >= kk && incl - sum < kk) {
-          uint32_t above = incl - sum, dg = 0, kn = 0;
-#pragma unroll
-          for (int q = 7; q >= 0; --q) {
-            if (kn == 0 && above + c[q] >= kk) {
-              dg = 8u * lane + q;
-              kn = kk - above;
-            }
-            above += c[q];
-          }
-          s_digit = dg;
-          s_kk = kn;
-        }
-      }
+      if (threadIdx.x < 32) find_bin<16>(hist, kk, &s_digit, &s_kk, &s_cnt);
       __syncthreads();
-      prefix |= s_digit << shift;
+      const uint32_t b = s_digit, m = s_cnt;
       kk = s_kk;
+      uint32_t result;
+      if (b < 16u) {                                 // an exact value
+        result = b;
+      } else {
+        const uint32_t tb = b / 16u + 3u;            // the bucket's highest set bit
+        const uint32_t lo = (16u | (b & 15u)) << (tb - 4u);   // its values: bits >= tb - 4 equal lo's
+        uint32_t hi = tb - 4u;                       // bits [0, hi) still to select
+        uint32_t prefix = lo;
+        if (m <= kSelCap) {                          // pass 2: the bucket's values into shared memory
+          for_row(row, n, [&](uint32_t v) {
+            if ((v >> hi) == (lo >> hi)) cand[atomicAdd(&s_m, 1u)] = v;
+          });
+          __syncthreads();
+          if (m <= blockDim.x) {                     // rank by counting: (greater, equal and earlier) = kk - 1
+            if (threadIdx.x < m) {
+              const uint32_t v = cand[threadIdx.x];
+              uint32_t above = 0;
+              for (uint32_t j = 0; j < m; ++j) {
+                const uint32_t u = cand[j];
+                above += (u > v || (u == v && j < threadIdx.x)) ? 1u : 0u;
+              }
+              if (above == kk - 1u) s_res = v;
+            }
+            __syncthreads();
+            prefix = s_res;
+            hi = 0;
+          }
+        }
+        const uint32_t* src = m <= kSelCap ? cand : row;
+        const uint32_t ns = m <= kSelCap ? m : n;
+        while (hi > 0) {                             // the remaining digits, 8 bits at a time
+          const uint32_t sh = hi >= 8u ? hi - 8u : 0u;
+          prefix |= select_pass(src, ns, prefix, sh, hi - sh, kk, hist, &s_digit, &s_kk, &s_cnt) << sh;
+          hi = sh;
+        }
+        result = prefix;
+      }
+      res[qi] = result;
       __syncthreads();
-    }
-    res[qi] = prefix;
     }
     const uint32_t prefix = res[0];
     if (threadIdx.x == 0) {
