@@ -321,6 +321,20 @@ enum { SLO_SELFTEST_EXP = 0, SLO_SELFTEST_LENGTH = 1, SLO_SELFTEST_ACCEPT = 2, S
 slo_status slo_selftest_transforms(slo_sim* h, uint32_t what, uint32_t arg0, uint32_t arg1, uint32_t arg2,
                                    uint64_t* d_out, uint32_t out_len, void* stream);
 
+/* K1b on caller rows (SV §8(a) a9; "p99", S:123 / S:165 nearest rank): for each of n_rows contiguous rows
+ * of row_len u32 values (device, [n_rows][row_len], row r at d_rows + r * row_len), the exact nearest-rank
+ * order statistics among its first-counted values: with m = d_n_measured ? min(d_n_measured[r], row_len) :
+ * row_len counted values and the row_len - m others equal to UINT32_MAX (the convention the simulation's stop
+ * rule uses, §2.14), p_q = the ceil(q m)-th smallest value of the row (q = 0.99, 0.50, 0.95; m = 0 gives the
+ * row's largest value, UINT32_MAX under that convention).  d_p99_us is required ([n_rows]); d_p50_us and
+ * d_p95_us are optional (NULL: not computed).  The same kernel and code path as slo_sim_run_batch's select step;
+ * enqueued on `stream`, results valid after it completes.  Uses handle scratch (32 B + 8 B per row).
+ * Errors: SLO_E_INVAL (null handle / rows / d_p99_us, n_rows == 0, row_len == 0), SLO_E_RANGE (n_rows * row_len
+ * >= 2^40), SLO_E_NOMEM, SLO_E_CUDA. */
+slo_status slo_select_rows(slo_sim* h, const uint32_t* d_rows, uint32_t n_rows, uint32_t row_len,
+                           const uint32_t* d_n_measured, uint32_t* d_p99_us, uint32_t* d_p50_us, uint32_t* d_p95_us,
+                           void* stream);
+
 const char* slo_status_string(slo_status s);
 const char* slo_last_error(const slo_sim* h); /* detail of the last failing call on h (NULL h: global) */
 

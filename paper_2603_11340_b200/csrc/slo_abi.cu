@@ -56,6 +56,8 @@ struct slo_sim {
   size_t scratch_bytes = 0;
   int regs = 0;
   int sel_bps = 1;                  // K1b resident blocks per SM (its grid: sel_bps x SMs, one wave)
+  double* d_sel_gp = nullptr;       // slo_select_rows: the goodput K1b writes (unused)
+  size_t sel_gp_cap = 0;
   bool pinned = false;              // scratch referenced by a captured CUDA graph: never regrown (ensure())
   // measurement hook (slo_sim_profile): events around each chunk's K0 | simulation kernels | K1b
   bool profile = false;
@@ -123,6 +125,15 @@ bool table_ok(const uint32_t* cw, uint32_t ncw, uint32_t lo) {
   for (uint32_t i = 1; i < ncw; ++i)
     if (cw[i] < cw[i - 1]) return false;
   return true;
+}
+
+// slo_select_rows: the replica records K1b reads (n_measured; window 1 so its goodput division is defined)
+__global__ void select_rows_part_kernel(slo_replica_result* part, uint32_t n, uint32_t row_len,
+                                        const uint32_t* __restrict__ nm) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t m = nm ? (nm[r] < row_len ? nm[r] : row_len) : row_len;
+  part[r] = slo_replica_result{0, 0, m, 0, 1, 0};
 }
 
 }  // namespace
@@ -342,6 +353,7 @@ slo_status slo_sim_destroy(slo_sim* h) {
     if (h->d_rec) cudaFree(h->d_rec);
     if (h->d_scratch) cudaFree(h->d_scratch);
     if (h->d_pareto) cudaFree(h->d_pareto);
+    if (h->d_sel_gp) cudaFree(h->d_sel_gp);
     for (auto& m : h->ev_marks)
       for (cudaEvent_t e : m) cudaEventDestroy(e);
     for (cudaEvent_t e : h->ev_free) cudaEventDestroy(e);
@@ -925,6 +937,37 @@ slo_status slo_selftest_transforms(slo_sim* h, uint32_t what, uint32_t arg0, uin
   CUDA_TRY(h, cudaMemsetAsync(d_out, 0, (size_t)need * sizeof(uint64_t), st));
   const size_t smem = (size_t)a.nbins * sizeof(uint32_t);
   slo::slo_selftest_kernel<<<4096, 256, smem, st>>>(a, h->d_tables, d_out);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+slo_status slo_select_rows(slo_sim* h, const uint32_t* d_rows, uint32_t n_rows, uint32_t row_len,
+                           const uint32_t* d_n_measured, uint32_t* d_p99_us, uint32_t* d_p50_us, uint32_t* d_p95_us,
+                           void* stream) {
+  if (!h || !d_rows || !d_p99_us || n_rows == 0 || row_len == 0)
+    return fail(h, SLO_E_INVAL, "select_rows: null pointer or empty rows");
+  if ((uint64_t)n_rows * row_len >= (1ull << 40)) return fail(h, SLO_E_RANGE, "select_rows: rows too large");
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  slo_status s;
+  if ((s = ensure(h, h->d_part, h->part_cap, (size_t)n_rows, st)) != SLO_OK) return s;
+  if ((s = ensure(h, h->d_sel_gp, h->sel_gp_cap, (size_t)n_rows, st)) != SLO_OK) return s;
+  select_rows_part_kernel<<<(n_rows + 255) / 256, 256, 0, st>>>(h->d_part, n_rows, row_len, d_n_measured);
+  CUDA_TRY(h, cudaGetLastError());
+  slo::SimParams p{};
+  p.lat = const_cast<uint32_t*>(d_rows);
+  p.part = h->d_part;
+  p.p99 = d_p99_us;
+  p.p50 = d_p50_us;
+  p.p95 = d_p95_us;
+  p.goodput = h->d_sel_gp;
+  p.n_rep = n_rows;
+  p.r_base = 0;
+  p.n_chunk = n_rows;
+  p.warmup = 0;
+  p.seg = row_len;
+  const uint32_t wave = (uint32_t)h->sm_count * (uint32_t)h->sel_bps;
+  slo::slo_select_kernel<<<n_rows < wave ? n_rows : wave, 256, 0, st>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   return SLO_OK;
 }

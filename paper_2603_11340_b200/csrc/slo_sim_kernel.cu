@@ -1999,7 +1999,8 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p) {
       // nearest rank among the nm counted latencies; the n - nm uncounted ones are UINT32_MAX (the top), so
       // the rq-th smallest counted value is the (n - rq + 1)-th largest of the row
       const uint32_t nm = pr.n_measured;
-      const uint32_t rq = (uint32_t)(((qi == 0 ? 99ull : qi == 1 ? 50ull : 95ull) * nm + 99ull) / 100ull);
+      uint32_t rq = (uint32_t)(((qi == 0 ? 99ull : qi == 1 ? 50ull : 95ull) * nm + 99ull) / 100ull);
+      if (rq == 0) rq = n;                           // no counted value (slo_select_rows): the row's largest
       uint32_t kk = n - rq + 1;
       // pass 1: log-scale histogram of the row
       hist[threadIdx.x] = 0;

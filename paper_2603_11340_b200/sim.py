@@ -284,6 +284,22 @@ class Simulator:
         torch.cuda.synchronize(self.device)
         return out.cpu().numpy().view(np.uint64)
 
+    def select_rows(self, rows: torch.Tensor, n_measured: Optional[torch.Tensor] = None, percentiles: bool = False,
+                    stream=None) -> Dict:
+        """K1b on caller rows (slo_select_rows): nearest-rank p99 (and p50/p95) of each row of a contiguous
+        [n_rows, row_len] int32/uint32 device tensor.  Asynchronous on `stream`."""
+        assert rows.dim() == 2 and rows.is_contiguous() and rows.element_size() == 4
+        n_rows, row_len = rows.shape
+        dev = rows.device
+        out = {"p99_us": torch.empty(n_rows, dtype=torch.int32, device=dev)}
+        if percentiles:
+            out["p50_us"] = torch.empty(n_rows, dtype=torch.int32, device=dev)
+            out["p95_us"] = torch.empty(n_rows, dtype=torch.int32, device=dev)
+        check(lib().slo_select_rows(self.h, rows.data_ptr(), n_rows, row_len, _ptr(n_measured),
+                                    out["p99_us"].data_ptr(), _ptr(out.get("p50_us")), _ptr(out.get("p95_us")),
+                                    _stream_ptr(stream)), self.h)
+        return out
+
     def philox_peak(self, iters: int = 2048, repeats: int = 3) -> float:
         """K4: measured Philox4x32-10 blocks/s at full occupancy (the RNG roofline)."""
         sm = self.info()["sm_count"]
