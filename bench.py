@@ -189,6 +189,47 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------------------------
+def climb_time_to_solution(S, cfg, seeds, graph, steps=500):
+    """BASELINE config 4 is a 500-step climb: its time with the plain device climb (ClimbGraph, one step per
+    replay, every step simulates its 32 candidates) and with the lookahead climb (LookaheadClimbGraph, SV §8(f)
+    NEXT-4: two steps per replay from U(K) = {K} u N(K) u N(N(K)), records measured last round cached).  CUDA
+    events on the replay streams; the two must end in the same climb state."""
+    import torch
+    from paper_2603_11340_b200.dist import LookaheadClimbGraph
+    la = LookaheadClimbGraph(S, cfg, seeds, n_cand=graph.n_cand).capture()
+
+    def timed(stream, body):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        body()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    graph.cands.copy_(graph.init_cands)
+    graph.state.copy_(graph.init_state)
+    tp = timed(graph.stream, lambda: [graph.graph.replay() for _ in range(steps)])
+    la.reset()
+    sims = []
+
+    def rounds():
+        for _ in range(steps // 2):
+            la.graph.replay()
+    tl = timed(la.stream, rounds)
+    same = bool(torch.equal(graph.state, la.state))
+    la.reset()
+    for _ in range(4):
+        la.run(1)
+        torch.cuda.synchronize()
+        sims.append(la.simulated())
+    la.close()
+    return {"steps": steps, "plain_ms": tp, "lookahead_ms": tl, "final_state_equal": same,
+            "lookahead_records_simulated_rounds_1_4": sims,
+            "note": "plain: 32 candidates simulated every step; lookahead: U(K) minus the cache per two steps "
+                    "(a converged climb simulates nothing); not the timed metric of this line"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -644,6 +685,8 @@ def main():
                                     "value_1core": v1,
                                     "sample_1core": f"{reps1} replicas ({reqs1} requests), same order, {dt1:.1f} s "
                                                     f"in one process (1 core)"}
+        if args.workload == "c4" and graph is not None and world == 1:
+            line["time_to_solution"] = climb_time_to_solution(S, cfg, seeds, graph)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()                         # no rank still reads a peer window

@@ -335,6 +335,31 @@ slo_status slo_select_rows(slo_sim* h, const uint32_t* d_rows, uint32_t n_rows, 
                            const uint32_t* d_n_measured, uint32_t* d_p99_us, uint32_t* d_p50_us, uint32_t* d_p95_us,
                            void* stream);
 
+/* Lookahead climb (SV §8(f) NEXT-4 "neighbour-of-neighbour lookahead"; Alg. 1).  A round takes two
+ * Alg. 1 steps from one batch of simulations: U(K) = {K} u N(K) u (union over c in N(K) of N(c)) holds every
+ * candidate the next two steps can score, whichever way the first step moves (<= 272 records for the wide-32
+ * stencil), and a record's aggregate depends only on the record and the seeds (its Philox key is (seed, config
+ * key), §2.1), so records the previous round measured are taken from its table (the cache) and only the rest
+ * are simulated.  The trajectory is the plain climb's (slo_hillclimb_step with n_cand candidates) step for step.
+ * d_table: SLO_LOOKAHEAD_TABLE_BYTES of device memory, zero-filled before the first round (empty cache).
+ *   slo_lookahead_prepare: builds U(state.K), looks it up in the cache and writes the records to simulate into
+ *     d_sim[0 .. SLO_LOOKAHEAD_CAP) (the rest padded with invalid records, conc = 0: no simulation work); the
+ *     caller then runs slo_sim_run_batch on d_sim x seeds and slo_aggregate into SLO_LOOKAHEAD_CAP aggregates
+ *     (n_parts rank parts of them, [part][SLO_LOOKAHEAD_CAP], for a seed-sharded multi-GPU climb);
+ *   slo_lookahead_step: assembles U's aggregates (cache or the new parts, summed), takes two steps on *d_state
+ *     (n_cand in [2, 32], the plain climb's candidate count), writes the state after each into d_traj[0..2)
+ *     and keeps U's table as the next round's cache.
+ * Enqueued on `stream` (graph-capturable: fixed launch sizes).  Errors: SLO_E_INVAL (null pointers, bad space or
+ * score parameters, n_cand / n_parts out of range), SLO_E_CUDA.  A U larger than the capacity (not reachable
+ * with the built-in stencils) is recorded in the table's 4th word. */
+#define SLO_LOOKAHEAD_CAP 320
+#define SLO_LOOKAHEAD_TABLE_BYTES 34576
+slo_status slo_lookahead_prepare(slo_sim* h, const slo_space* space, const slo_climb_state* d_state, void* d_table,
+                                 slo_knobs* d_sim, void* stream);
+slo_status slo_lookahead_step(slo_sim* h, const slo_space* space, const slo_score_params* sp, void* d_table,
+                              const slo_config_agg* d_aggs, uint32_t n_parts, uint32_t n_cand,
+                              slo_climb_state* d_state, slo_climb_state* d_traj, void* stream);
+
 const char* slo_status_string(slo_status s);
 const char* slo_last_error(const slo_sim* h); /* detail of the last failing call on h (NULL h: global) */
 

@@ -23,7 +23,8 @@ EXPORTS = ("slo_sim_create", "slo_sim_destroy", "slo_sim_get_info", "slo_sim_run
            "slo_sim_run_batch_host", "slo_aggregate", "slo_aggregate_reduce", "slo_neighbors",
            "slo_hillclimb_step", "slo_exchange_create", "slo_exchange_open", "slo_aggregate_exchange",
            "slo_exchange_error", "slo_exchange_destroy", "slo_philox_peak", "slo_pareto_front", "slo_status_string",
-           "slo_last_error", "slo_selftest_transforms", "slo_sim_profile", "slo_sim_profile_read", "slo_select_rows")
+           "slo_last_error", "slo_selftest_transforms", "slo_sim_profile", "slo_sim_profile_read", "slo_select_rows",
+           "slo_lookahead_prepare", "slo_lookahead_step")
 SELFTEST = {"exp": 0, "length": 1, "accept": 2, "noise": 3, "accept2": 4}   # SLO_SELFTEST_* (include/slo_sim.h)
 EXCHANGE_HANDLE_BYTES = 64
 
@@ -145,6 +146,9 @@ def lib():
         L.slo_sim_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint32)]
         L.slo_selftest_transforms.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, vp, C.c_uint32, vp]
         L.slo_select_rows.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp]
+        L.slo_lookahead_prepare.argtypes = [vp, C.POINTER(slo_space), vp, vp, vp, vp]
+        L.slo_lookahead_step.argtypes = [vp, C.POINTER(slo_space), C.POINTER(slo_score_params), vp, vp, C.c_uint32,
+                                         C.c_uint32, vp, vp, vp]
         L.slo_status_string.argtypes = [C.c_int32]
         L.slo_status_string.restype = C.c_char_p
         L.slo_last_error.argtypes = [vp]

@@ -782,6 +782,35 @@ slo_status slo_hillclimb_step(slo_sim* h, const slo_space* space, const slo_scor
   return SLO_OK;
 }
 
+static_assert(sizeof(slo::LookTable) == SLO_LOOKAHEAD_TABLE_BYTES, "SLO_LOOKAHEAD_TABLE_BYTES");
+
+slo_status slo_lookahead_prepare(slo_sim* h, const slo_space* space, const slo_climb_state* d_state, void* d_table,
+                                 slo_knobs* d_sim, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "lookahead_prepare: null handle");
+  if (!space_ok(space) || !d_state || !d_table || !d_sim) return fail(h, SLO_E_INVAL, "lookahead_prepare: bad arguments");
+  DeviceGuard g(h->device);
+  slo::slo_lookahead_prepare_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(*space, d_state, (slo::LookTable*)d_table,
+                                                                         d_sim);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
+slo_status slo_lookahead_step(slo_sim* h, const slo_space* space, const slo_score_params* sp, void* d_table,
+                              const slo_config_agg* d_aggs, uint32_t n_parts, uint32_t n_cand,
+                              slo_climb_state* d_state, slo_climb_state* d_traj, void* stream) {
+  if (!h) return fail(nullptr, SLO_E_INVAL, "lookahead_step: null handle");
+  if (!space_ok(space) || !sp || !d_table || !d_aggs || !d_state || !d_traj || n_cand < 2 || n_cand > 32 ||
+      n_parts == 0)
+    return fail(h, SLO_E_INVAL, "lookahead_step: bad arguments");
+  if (sp->lambda_milli < 0 || sp->delta_micro < 0 || sp->viol_mult < 1 || sp->ema_beta_q16 > 65536 || sp->reserved)
+    return fail(h, SLO_E_INVAL, "lookahead_step: bad score parameters");
+  DeviceGuard g(h->device);
+  slo::slo_lookahead_step_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*space, *sp, (slo::LookTable*)d_table, d_aggs,
+                                                                    n_parts, n_cand, d_state, d_traj);
+  CUDA_TRY(h, cudaGetLastError());
+  return SLO_OK;
+}
+
 // ---- peer exchange (NEXT-4) ----------------------------------------------------------------------
 struct slo_exchange {
   slo_sim* h = nullptr;

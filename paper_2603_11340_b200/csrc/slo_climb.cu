@@ -276,25 +276,17 @@ __device__ static inline int64_t score_micro(const slo_config_agg& a, const slo_
   return (int64_t)gp - (int64_t)pen - hw_cost_micro(k, sp);
 }
 
-__global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs* cands, uint32_t n_cand,
-                                 const slo_config_agg* aggs, uint32_t n_parts, slo_climb_state* state,
-                                 int64_t* scores) {
+// one Alg. 1 step on one warp: lane k < n_cand holds candidate k's pooled aggregate `a` (cands[0] = state.K);
+// scores (Eq. 3), argmax over k >= 1 (lowest index on ties), move rule, best-so-far; lane 0 writes the state
+// and next[0..n_cand) = [K', neighbours(K'), padding]
+__device__ static void climb_core(const slo_space& space, const slo_score_params& sp, const slo_knobs* cands,
+                                  uint32_t n_cand, const slo_config_agg& a, slo_climb_state* state, slo_knobs* next,
+                                  int64_t* scores) {
   const int lane = threadIdx.x & 31;
-  __shared__ slo_knobs next[32];
-  slo_knobs mine{};
-  slo_config_agg a{0, 0, 0, 0, 0};
   int64_t s = INT64_MIN;
   int64_t ema_new = -1;
   if ((uint32_t)lane < n_cand) {
-    mine = cands[lane];
-    for (uint32_t p = 0; p < n_parts; ++p) {
-      const slo_config_agg x = aggs[(size_t)p * n_cand + lane];
-      a.sum_p99_us += x.sum_p99_us;
-      a.sum_slo_met += x.sum_slo_met;
-      a.sum_window_us += x.sum_window_us;
-      a.n_seeds += x.n_seeds;
-      a.flags |= x.flags;
-    }
+    const slo_knobs mine = cands[lane];
     int64_t ema = -1;
     if (lane == 0 && sp.ema_beta_q16 > 0 && a.n_seeds > 0 && !(a.flags & 1u)) {  // EMA of p99
       const uint64_t sample = a.sum_p99_us / a.n_seeds;
@@ -357,16 +349,190 @@ __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs
     next[0] = K;
     uint32_t nn = 1 + neighbors_of(space, K, next + 1, n_cand > 0 ? n_cand - 1 : 0);
     st.n_next = nn;
-    for (uint32_t i = nn; i < n_cand; ++i) {
-      slo_knobs pad{};
-      pad.conc = 0;       // invalid => sentinel outputs, no simulation work
-      pad.workload = 0;
-      next[i] = pad;
-    }
+    for (uint32_t i = nn; i < n_cand; ++i) next[i] = slo_knobs{};   // conc = 0: invalid, no simulation work
     *state = st;
   }
   __syncwarp();
+}
+
+__global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs* cands, uint32_t n_cand,
+                                 const slo_config_agg* aggs, uint32_t n_parts, slo_climb_state* state,
+                                 int64_t* scores) {
+  const int lane = threadIdx.x & 31;
+  __shared__ slo_knobs next[32];
+  slo_config_agg a{0, 0, 0, 0, 0};
+  if ((uint32_t)lane < n_cand) {
+    for (uint32_t p = 0; p < n_parts; ++p) {
+      const slo_config_agg x = aggs[(size_t)p * n_cand + lane];
+      a.sum_p99_us += x.sum_p99_us;
+      a.sum_slo_met += x.sum_slo_met;
+      a.sum_window_us += x.sum_window_us;
+      a.n_seeds += x.n_seeds;
+      a.flags |= x.flags;
+    }
+  }
+  climb_core(space, sp, cands, n_cand, a, state, next, scores);
   if ((uint32_t)lane < n_cand) cands[lane] = next[lane];
+}
+
+// ------------------------------------------------------------------------------------------------
+// Lookahead climb (SV §8(f) NEXT-4): one round evaluates U(K) = {K} u N(K) u (union of N(c), c in N(K)) — every
+// candidate the next two Alg. 1 steps can look at, whatever the first step decides — minus what the previous
+// round's U already measured (a candidate's aggregate is a function of its knob record and the seeds only:
+// its Philox key is (seed, config key)), then takes two steps from the table.  The trajectory equals the plain
+// climb's step for step.
+// ------------------------------------------------------------------------------------------------
+__device__ static inline uint32_t knob_hash(const slo_knobs& k) {
+  const uint32_t* x = reinterpret_cast<const uint32_t*>(&k);
+  uint32_t h = 0x811C9DC5u;
+  for (int i = 0; i < 8; ++i) h = (h ^ x[i]) * 0x01000193u;
+  return h;
+}
+
+constexpr int kLookRaw = 1024;   // [K], N(K) (<= 31), N(c) for each c (31 x 31): 993 slots
+
+// block-wide exclusive prefix sum of a 0/1 flag (blockDim.x = 1024); returns the total via *tot
+__device__ static inline uint32_t block_excl(bool f, uint32_t* warp_tot, uint32_t* tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t m = __ballot_sync(FULL, f);
+  if (lane == 0) warp_tot[w] = __popc(m);
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t v = warp_tot[lane];
+    uint32_t incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += o;
+    }
+    warp_tot[lane] = incl - v;
+    if (lane == 31) *tot = incl;
+  }
+  __syncthreads();
+  const uint32_t r = warp_tot[w] + __popc(m & ((1u << lane) - 1u));
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) slo_lookahead_prepare_kernel(slo_space space, const slo_climb_state* state,
+                                                                      LookTable* T, slo_knobs* sim) {
+  __shared__ slo_knobs raw[kLookRaw];
+  __shared__ uint32_t rh[kLookRaw];
+  __shared__ uint32_t cnt[32];
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t s_tot;
+  const uint32_t t = threadIdx.x;
+  if (t == 0) {
+    raw[0] = state->K;
+    cnt[0] = neighbors_of(space, raw[0], raw + 1, 31);
+  }
+  __syncthreads();
+  const uint32_t nb = cnt[0];
+  if (t >= 1 && t <= nb) cnt[t] = neighbors_of(space, raw[t], raw + 32 + (t - 1) * 31, 31);
+  __syncthreads();
+  // slot t holds a candidate: 0 = K, 1..nb = N(K), 32 + 31 (i - 1) + j = the j-th neighbour of raw[i]
+  bool valid = t <= nb;
+  if (t >= 32) {
+    const uint32_t i = 1 + (t - 32) / 31, j = (t - 32) % 31;
+    valid = i <= nb && j < cnt[i];
+  }
+  const uint32_t h = valid ? knob_hash(raw[t]) : 0u;
+  rh[t] = h;
+  __syncthreads();
+  bool first = valid;
+  for (uint32_t u = 0; first && u < t; ++u) {
+    bool vu = u <= nb;
+    if (u >= 32) {
+      const uint32_t i = 1 + (u - 32) / 31, j = (u - 32) % 31;
+      vu = i <= nb && j < cnt[i];
+    }
+    if (vu && rh[u] == h && knobs_equal(raw[u], raw[t])) first = false;
+  }
+  const uint32_t pos = block_excl(first, warp_tot, &s_tot);
+  const uint32_t n_new = s_tot < kLookCap ? s_tot : kLookCap;
+  if (first && pos < kLookCap) {
+    T->new_k[pos] = raw[t];
+    T->new_h[pos] = h;
+  }
+  if (t == 0) {
+    T->n_new = n_new;
+    if (s_tot > kLookCap) T->overflow = s_tot;
+  }
+  __syncthreads();
+  // measured last round?  map[i] >= 0: the old table's entry; < 0: simulation list entry -map - 1
+  const uint32_t n_old = T->n_old;
+  int32_t m = -1;
+  if (t < n_new) {
+    const slo_knobs k = T->new_k[t];
+    const uint32_t hk = T->new_h[t];
+    for (uint32_t j = 0; j < n_old; ++j)
+      if (T->old_h[j] == hk && knobs_equal(T->old_k[j], k)) {
+        m = (int32_t)j;
+        break;
+      }
+  }
+  const bool miss = t < n_new && m < 0;
+  const uint32_t sp_ = block_excl(miss, warp_tot, &s_tot);
+  if (t < n_new) T->map[t] = miss ? -(int32_t)sp_ - 1 : m;
+  if (miss) sim[sp_] = T->new_k[t];
+  if (t >= s_tot && t < kLookCap) sim[t] = slo_knobs{};   // padding: conc = 0, invalid, no simulation work
+  if (t == 0) T->n_sim = s_tot;
+}
+
+__global__ void slo_lookahead_step_kernel(slo_space space, slo_score_params sp, LookTable* T,
+                                          const slo_config_agg* aggs, uint32_t n_parts, uint32_t n_cand,
+                                          slo_climb_state* state, slo_climb_state* traj) {
+  const int lane = threadIdx.x & 31;
+  __shared__ slo_knobs cands[32], next[32];
+  __shared__ slo_config_agg tab[kLookCap];
+  const uint32_t n_new = T->n_new;
+  for (uint32_t i = lane; i < n_new; i += 32) {          // the round's table: last round's or just simulated
+    const int32_t m = T->map[i];
+    slo_config_agg a{0, 0, 0, 0, 0};
+    if (m >= 0) {
+      a = T->old_a[m];
+    } else {
+      const uint32_t c = (uint32_t)(-m - 1);
+      for (uint32_t p = 0; p < n_parts; ++p) {
+        const slo_config_agg x = aggs[(size_t)p * kLookCap + c];
+        a.sum_p99_us += x.sum_p99_us;
+        a.sum_slo_met += x.sum_slo_met;
+        a.sum_window_us += x.sum_window_us;
+        a.n_seeds += x.n_seeds;
+        a.flags |= x.flags;
+      }
+    }
+    tab[i] = a;
+  }
+  if (lane == 0) {                                       // [K, neighbours(K), padding]: the plain climb's list
+    cands[0] = state->K;
+    const uint32_t nn = 1 + neighbors_of(space, cands[0], cands + 1, n_cand - 1);
+    for (uint32_t i = nn; i < n_cand; ++i) cands[i] = slo_knobs{};
+  }
+  __syncwarp();
+  for (int st = 0; st < 2; ++st) {
+    slo_config_agg a{0, 0, 0, 0, 1u};                    // not in U: a padding record (invalid, INT64_MIN)
+    if ((uint32_t)lane < n_cand) {
+      const slo_knobs k = cands[lane];
+      const uint32_t hk = knob_hash(k);
+      if (k.conc != 0)
+        for (uint32_t j = 0; j < n_new; ++j)
+          if (T->new_h[j] == hk && knobs_equal(T->new_k[j], k)) {
+            a = tab[j];
+            break;
+          }
+    }
+    climb_core(space, sp, cands, n_cand, a, state, next, nullptr);
+    if (lane == 0) traj[st] = *state;
+    if ((uint32_t)lane < n_cand) cands[lane] = next[lane];
+    __syncwarp();
+  }
+  for (uint32_t i = lane; i < n_new; i += 32) {          // this round's table is the next round's cache
+    T->old_k[i] = T->new_k[i];
+    T->old_h[i] = T->new_h[i];
+    T->old_a[i] = tab[i];
+  }
+  if (lane == 0) T->n_old = n_new;
 }
 
 }  // namespace slo

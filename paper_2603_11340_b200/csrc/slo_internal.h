@@ -82,6 +82,21 @@ __global__ void slo_climb_kernel(slo_space space, slo_score_params sp, slo_knobs
                                  const slo_config_agg* aggs, uint32_t n_parts, slo_climb_state* state,
                                  int64_t* scores);
 
+// lookahead climb (NEXT-4, slo_climb.cu): the round's candidate table U and last round's (the cache)
+constexpr uint32_t kLookCap = SLO_LOOKAHEAD_CAP;
+struct LookTable {
+  uint32_t n_old, n_new, n_sim, overflow;     // overflow: |U| when it exceeded kLookCap (0 otherwise)
+  uint32_t old_h[kLookCap], new_h[kLookCap];  // knob hashes
+  int32_t map[kLookCap];                      // U entry i: >= 0 cached (old index), < 0 simulated (list -map - 1)
+  slo_knobs old_k[kLookCap], new_k[kLookCap];
+  slo_config_agg old_a[kLookCap];
+};
+__global__ void slo_lookahead_prepare_kernel(slo_space space, const slo_climb_state* state, LookTable* T,
+                                             slo_knobs* sim);
+__global__ void slo_lookahead_step_kernel(slo_space space, slo_score_params sp, LookTable* T,
+                                          const slo_config_agg* aggs, uint32_t n_parts, uint32_t n_cand,
+                                          slo_climb_state* state, slo_climb_state* traj);
+
 // peer exchange (NEXT-4): window = [flags 2 x kXMaxRanks u64][inbox 2 parities x world x n_cfg slo_config_agg]
 constexpr uint32_t kXMaxRanks = 16;
 constexpr size_t kXHeader = 2 * kXMaxRanks * sizeof(uint64_t);

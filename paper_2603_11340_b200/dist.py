@@ -282,6 +282,93 @@ class ClimbGraph:
         return h_traj
 
 
+class LookaheadClimbGraph:
+    """Alg. 1 two steps per round (SV §8(f) NEXT-4 neighbour-of-neighbour lookahead, slo_lookahead_*): a round
+    simulates U(K) = {K} u N(K) u N(N(K)) minus what the previous round measured (the cache), then takes two
+    steps from the table.  Same trajectory as ClimbGraph; the whole round — prepare, K0/K1/K1b over the
+    SLO_LOOKAHEAD_CAP-record list (invalid padding records cost nothing), K2, all-gather (N > 1, seed-sharded),
+    two steps — is one CUDA graph."""
+
+    CAP = 320                                             # SLO_LOOKAHEAD_CAP
+    TABLE_BYTES = 34576                                   # SLO_LOOKAHEAD_TABLE_BYTES
+
+    def __init__(self, sim, cfg, seeds: List[int], n_cand: int = 32, sp=None):
+        from . import sim as S
+        sim = sim.twin()                                   # the graph holds this handle's scratch
+        self.sim, self.cfg = sim, cfg
+        self.space = cfg.extra["space"]
+        self.sp = dict(sp if sp is not None else cfg.extra["score"])
+        dev = torch.device("cuda", sim.device)
+        self.n_cand, self.n_seeds = n_cand, len(seeds)
+        self.state = sim.climb_state(cfg.knobs[0])
+        self.init_state = self.state.clone()
+        self.table = torch.zeros(self.TABLE_BYTES, dtype=torch.uint8, device=dev)
+        self.sim_list = torch.zeros((self.CAP, 32), dtype=torch.uint8, device=dev)
+        self.seeds = S.seeds_tensor(seeds, device=dev)
+        self.out = sim.alloc_outputs(self.CAP * len(seeds), detail=True, stats=True)
+        self.agg = torch.empty((self.CAP, 32), dtype=torch.uint8, device=dev)
+        _, self.w = world()
+        self.parts = (torch.empty((self.w * self.CAP, 32), dtype=torch.uint8, device=dev) if self.w > 1 else self.agg)
+        self.traj = torch.empty((2, self.state.numel()), dtype=torch.uint8, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.graph = None
+
+    def _round(self):
+        c, st = self.cfg, self.stream
+        self.sim.lookahead_prepare(self.space, self.state, self.table, self.sim_list, stream=st)
+        self.sim.run_batch(self.sim_list, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out, stream=st)
+        self.sim.aggregate(self.out["detail"], self.CAP, self.n_seeds, out=self.agg, stream=st)
+        if self.w > 1:
+            dist.all_gather_into_tensor(self.parts, self.agg)
+        self.sim.lookahead_step(self.space, self.sp, self.table, self.parts, self.w, self.n_cand, self.state,
+                                self.traj, stream=st)
+
+    def reset(self):
+        self.state.copy_(self.init_state)
+        self.table.zero_()
+
+    def capture(self):
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            self._round()
+        self.stream.synchronize()
+        self.reset()
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._round()
+        return self
+
+    def close(self):
+        self.graph = None
+        self.sim.close()
+
+    def run(self, rounds: int):
+        if self.graph is None:
+            self.capture()
+        for _ in range(rounds):
+            self.graph.replay()
+        return self.state
+
+    def states(self, rounds: int) -> torch.Tensor:
+        """Replay `rounds` rounds and return the climb state after every step: uint8 [2 rounds, 104] (host)."""
+        if self.graph is None:
+            self.capture()
+        h = torch.empty((rounds, 2, self.state.numel()), dtype=torch.uint8).pin_memory()
+        st = self.stream
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for i in range(rounds):
+                self.graph.replay()
+                h[i].copy_(self.traj, non_blocking=True)
+        st.synchronize()
+        return h.view(2 * rounds, -1)
+
+    def simulated(self) -> int:
+        """Records the last round simulated (the rest came from the cache)."""
+        return int(self.table[8:12].view(torch.int32).item())
+
+
 def hillclimb(sim, cfg, steps: int, seeds: List[int], n_cand: int = 32, stream=None):
     """Device-resident Alg. 1 over `steps` iterations on this rank's seed slice; returns the final state.
 

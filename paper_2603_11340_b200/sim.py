@@ -339,6 +339,19 @@ class Simulator:
         cands = [K] + nb + [PAD_KNOBS] * (n_cand - 1 - len(nb))
         return knobs_tensor(cands, device=torch.device("cuda", self.device))
 
+    def lookahead_prepare(self, space: Dict, state: torch.Tensor, table: torch.Tensor, sim_list: torch.Tensor,
+                          stream=None) -> None:
+        """Lookahead climb round, part 1 (slo_lookahead_prepare): U(K) minus the cache -> sim_list."""
+        check(lib().slo_lookahead_prepare(self.h, C.byref(space_struct(space)), state.data_ptr(), table.data_ptr(),
+                                          sim_list.data_ptr(), _stream_ptr(stream)), self.h)
+
+    def lookahead_step(self, space: Dict, sp: Dict, table: torch.Tensor, aggs: torch.Tensor, n_parts: int,
+                       n_cand: int, state: torch.Tensor, traj: torch.Tensor, stream=None) -> None:
+        """Lookahead climb round, part 2 (slo_lookahead_step): two Alg. 1 steps from U's aggregates."""
+        check(lib().slo_lookahead_step(self.h, C.byref(space_struct(space)), C.byref(score_struct(sp)),
+                                       table.data_ptr(), aggs.data_ptr(), n_parts, n_cand, state.data_ptr(),
+                                       traj.data_ptr(), _stream_ptr(stream)), self.h)
+
     def hillclimb_step(self, space: Dict, sp: Dict, cands: torch.Tensor, aggs: torch.Tensor, n_parts: int,
                        state: torch.Tensor, scores: Optional[torch.Tensor] = None, stream=None) -> None:
         """K3: Alg. 1 step on the device; rewrites `cands` in place with the next candidate list."""

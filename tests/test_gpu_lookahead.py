@@ -1,0 +1,59 @@
+"""Lookahead climb (SV §8(f) NEXT-4; slo_lookahead_prepare / slo_lookahead_step, dist.LookaheadClimbGraph): two
+Alg. 1 steps per round from U(K) = {K} u N(K) u N(N(K)), records measured last round taken from the cache.
+Its trajectory must equal the plain device climb's (dist.ClimbGraph, itself checked step by step against
+oracle/climb.py in test_gpu_parity.py) bit for bit: every field of the climb state after every step."""
+import dataclasses
+
+import pytest
+import torch
+
+from paper_2603_11340_b200 import inputs, sim
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {"live-wide32": (inputs.SPACE_WIDE32, dict(inputs.SCORE_DEFAULTS)),
+            "sim-controller": (inputs.SPACE_WIDE32, dict(inputs.SCORE_SIM)),
+            "sim-space": (inputs.SPACE_SIM, dict(inputs.SCORE_SIM, strict_alg1=0)),
+            "live-stencil": (inputs.SPACE_LIVE, dict(inputs.SCORE_DEFAULTS, delta_micro=0))}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_lookahead_trajectory_equals_plain_climb(variant):
+    from paper_2603_11340_b200.dist import ClimbGraph, LookaheadClimbGraph
+    space, sp = VARIANTS[variant]
+    cfg = inputs.config_c4(n_seeds=4, segment_len=400)
+    cfg = dataclasses.replace(cfg, extra=dict(cfg.extra, space=space, score=sp))
+    seeds = inputs.seeds(4, 77)
+    s = sim.Simulator(cfg.workloads, device=0)
+    rounds = 6
+    g = ClimbGraph(s, cfg, seeds, n_cand=32).capture()
+    nb = g.state.numel()
+    h_traj = torch.empty((2 * rounds, nb), dtype=torch.uint8).pin_memory()
+    g.run_host(2 * rounds, g.init_cands.cpu().pin_memory(), g.init_state.cpu().pin_memory(), h_traj)
+    la = LookaheadClimbGraph(s, cfg, seeds, n_cand=32).capture()
+    got = la.states(rounds)
+    assert torch.equal(got, h_traj), variant
+    # the cache: a later round simulates only what the previous round's table lacks
+    assert 0 <= la.simulated() <= la.CAP
+    g.close()
+    la.close()
+    s.close()
+
+
+def test_lookahead_cache_converged_climb_simulates_nothing():
+    """Once K stops moving, U(K) is the previous round's table: a round simulates no record at all and the
+    trajectory still matches the plain climb."""
+    from paper_2603_11340_b200.dist import LookaheadClimbGraph
+    cfg = inputs.config_c4(n_seeds=2, segment_len=300)
+    sp = dict(inputs.SCORE_DEFAULTS, delta_micro=10**15, slo_us=4_000_000_000)   # never moves, never violated
+    cfg = dataclasses.replace(cfg, extra=dict(cfg.extra, score=sp))
+    s = sim.Simulator(cfg.workloads, device=0)
+    la = LookaheadClimbGraph(s, cfg, inputs.seeds(2, 5), n_cand=32).capture()
+    la.run(1)
+    torch.cuda.synchronize()
+    first = la.simulated()
+    la.run(1)
+    torch.cuda.synchronize()
+    assert first > 32 and la.simulated() == 0
+    la.close()
+    s.close()
