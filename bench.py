@@ -600,7 +600,8 @@ def main():
         # summaries (profiles/r02_*_ncu.json), and the HBM share of this run (ncu bytes over the live kernel time)
         def ncu_issue(tag):
             import glob
-            fs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r02_{tag}_ncu.json")))
+            fs = (sorted(glob.glob(os.path.join(ROOT, "profiles", f"r02_{tag}_ncu.json"))) +
+                  sorted(glob.glob(os.path.join(ROOT, "profiles", f"r02b_{tag}_ncu.json"))))
             if not fs:
                 return None
             try:
