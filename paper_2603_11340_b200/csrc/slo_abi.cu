@@ -21,6 +21,10 @@ static_assert(sizeof(slo_arrivals) == 40, "slo_arrivals must be 40 B");
 static_assert(sizeof(slo_climb_state) == 104, "slo_climb_state must be 104 B");
 static_assert(sizeof(slo_score_params) == 80, "slo_score_params must be 80 B");
 
+// K1b block size by row length: short rows take smaller blocks (their per-row histogram scans and barriers, not
+// the loads, dominate; C5s's 2,000-value rows: 6.1 ms at 256 threads, 4.7 at 128, 4.2 at 64)
+static int sel_threads_for(uint32_t n) { return n <= 2048u ? 64 : (n <= 4096u ? 128 : 256); }
+
 struct slo_sim {
   int device = 0;
   int sm_count = 0;
@@ -55,7 +59,7 @@ struct slo_sim {
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
   int regs = 0;
-  int sel_bps = 1;                  // K1b resident blocks per SM (its grid: sel_bps x SMs, one wave)
+  int sel_bps[3] = {1, 1, 1};       // K1b resident blocks per SM at 64 / 128 / 256 threads (grid: one wave)
   double* d_sel_gp = nullptr;       // slo_select_rows: the goodput K1b writes (unused)
   size_t sel_gp_cap = 0;
   bool pinned = false;              // scratch referenced by a captured CUDA graph: never regrown (ensure())
@@ -292,9 +296,10 @@ slo_status slo_sim_create(int device, const slo_workload* wl, uint32_t n_wl, con
     return fail(nullptr, SLO_E_DEVICE, "create: no sm_100a kernel image for device %d", device);
   }
   h->regs = fa.numRegs;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->sel_bps, slo::slo_select_kernel, 256, 0) != cudaSuccess ||
-      h->sel_bps < 1)
-    h->sel_bps = 1;
+  for (int i = 0; i < 3; ++i)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->sel_bps[i], slo::slo_select_kernel, 64 << i, 0) !=
+            cudaSuccess || h->sel_bps[i] < 1)
+      h->sel_bps[i] = 1;
   cudaError_t e;
   if ((e = cudaMalloc(&h->d_wl, sizeof(slo::DevWorkload) * n_wl)) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tables, sizeof(uint32_t) * tables.size())) != cudaSuccess ||
@@ -622,10 +627,12 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     }
     if ((s = mark(5, st)) != SLO_OK) return s;
     // one wave of resident blocks: a grid-stride second wave would start its rows late
-    const uint32_t sel_wave = (uint32_t)h->sm_count * (uint32_t)h->sel_bps;
+    // (fewer rows than SMs: latency-bound, every row takes a full 256-thread block)
+    const uint32_t sel_threads = nc < (uint32_t)h->sm_count ? 256u : (uint32_t)sel_threads_for(p.seg);
+    const uint32_t sel_wave = (uint32_t)h->sm_count * (uint32_t)h->sel_bps[sel_threads == 64 ? 0 : (sel_threads == 128 ? 1 : 2)];
     const uint32_t sel_blocks = nc < sel_wave ? nc : sel_wave;
     nvtxRangePushA("K1b select");
-    slo::slo_select_kernel<<<sel_blocks, 256, 0, st>>>(p);
+    slo::slo_select_kernel<<<sel_blocks, sel_threads, 0, st>>>(p);
     nvtxRangePop();
     CUDA_TRY(h, cudaGetLastError());
     if ((s = mark(6, st)) != SLO_OK) return s;
@@ -995,8 +1002,9 @@ slo_status slo_select_rows(slo_sim* h, const uint32_t* d_rows, uint32_t n_rows, 
   p.n_chunk = n_rows;
   p.warmup = 0;
   p.seg = row_len;
-  const uint32_t wave = (uint32_t)h->sm_count * (uint32_t)h->sel_bps;
-  slo::slo_select_kernel<<<n_rows < wave ? n_rows : wave, 256, 0, st>>>(p);
+  const uint32_t thr = n_rows < (uint32_t)h->sm_count ? 256u : (uint32_t)sel_threads_for(row_len);
+  const uint32_t wave = (uint32_t)h->sm_count * (uint32_t)h->sel_bps[thr == 64 ? 0 : (thr == 128 ? 1 : 2)];
+  slo::slo_select_kernel<<<n_rows < wave ? n_rows : wave, thr, 0, st>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   return SLO_OK;
 }

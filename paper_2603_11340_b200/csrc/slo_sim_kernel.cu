@@ -1957,7 +1957,7 @@ __device__ __forceinline__ void find_bin(const uint32_t* hist, uint32_t kk, uint
 __device__ __forceinline__ uint32_t select_pass(const uint32_t* src, uint32_t n, uint32_t prefix, uint32_t sh,
                                                 uint32_t w, uint32_t& kk, uint32_t* hist, uint32_t* s_dig,
                                                 uint32_t* s_kk, uint32_t* s_cnt) {
-  hist[threadIdx.x] = 0;
+  for (uint32_t i = threadIdx.x; i < 256u; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   const uint32_t hs = sh + w;                      // bits >= hs must match the prefix
   const uint32_t dm = (1u << w) - 1u;
@@ -2003,8 +2003,7 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p) {
       if (rq == 0) rq = n;                           // no counted value (slo_select_rows): the row's largest
       uint32_t kk = n - rq + 1;
       // pass 1: log-scale histogram of the row
-      hist[threadIdx.x] = 0;
-      hist[threadIdx.x + 256] = 0;
+      for (uint32_t i = threadIdx.x; i < kLogBins; i += blockDim.x) hist[i] = 0;
       if (threadIdx.x == 0) s_m = 0;
       __syncthreads();
       for_row(row, n, [&](uint32_t v) { atomicAdd(hist + log_bin(v), 1u); });
