@@ -189,42 +189,60 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------------------------
+def inputs_seeds(n, offset):
+    from paper_2603_11340_b200 import inputs
+    return inputs.seeds(n, offset)
+
+
 def climb_time_to_solution(S, cfg, seeds, graph, steps=500):
     """BASELINE config 4 is a 500-step climb: its time with the plain device climb (ClimbGraph, one step per
     replay, every step simulates its 32 candidates) and with the lookahead climb (LookaheadClimbGraph, SV §8(f)
     NEXT-4: two steps per replay from U(K) = {K} u N(K) u N(N(K)), records measured last round cached).  CUDA
     events on the replay streams; the two must end in the same climb state."""
     import torch
-    from paper_2603_11340_b200.dist import LookaheadClimbGraph
+    from paper_2603_11340_b200 import sim
+    from paper_2603_11340_b200.dist import LookaheadClimbGraph, final_rerun
     la = LookaheadClimbGraph(S, cfg, seeds, n_cand=graph.n_cand).capture()
+    fresh = inputs_seeds(len(seeds), 1_000_000)           # Alg. 1's final re-run of K_best (P:168) on a fresh block
 
-    def timed(stream, body):
+    def timed(stream, body):                             # replays and re-run all on `stream`
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        body()
-        e1.record(stream)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            body()
+            e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
+    fresh_t = sim.seeds_tensor(fresh, device=graph.state.device)
+    res = {"plain": final_rerun(S, cfg, graph.state, fresh_t), "look": final_rerun(S, cfg, graph.state, fresh_t)}
+    torch.cuda.synchronize()                              # (outputs allocated outside the timed region)
     graph.cands.copy_(graph.init_cands)
     graph.state.copy_(graph.init_state)
-    tp = timed(graph.stream, lambda: [graph.graph.replay() for _ in range(steps)])
+
+    def plain():
+        for _ in range(steps):
+            graph.graph.replay()
+        final_rerun(S, cfg, graph.state, fresh_t, out=res["plain"], stream=graph.stream)
+    tp = timed(graph.stream, plain)
     la.reset()
     sims = []
 
     def rounds():
         for _ in range(steps // 2):
             la.graph.replay()
+        final_rerun(S, cfg, la.state, fresh_t, out=res["look"], stream=la.stream)
     tl = timed(la.stream, rounds)
-    same = bool(torch.equal(graph.state, la.state))
+    same = bool(torch.equal(graph.state, la.state)) and bool(torch.equal(res["plain"]["agg"], res["look"]["agg"]))
     la.reset()
     for _ in range(4):
         la.run(1)
         torch.cuda.synchronize()
         sims.append(la.simulated())
     la.close()
-    return {"steps": steps, "plain_ms": tp, "lookahead_ms": tl, "final_state_equal": same,
+    return {"steps": steps, "final_rerun": f"K_best on {len(fresh)} fresh seeds (inside both timings)",
+            "plain_ms": tp, "lookahead_ms": tl, "final_state_equal": same,
             "lookahead_records_simulated_rounds_1_4": sims,
             "note": "plain: 32 candidates simulated every step; lookahead: U(K) minus the cache per two steps "
                     "(a converged climb simulates nothing); not the timed metric of this line"}

@@ -386,7 +386,7 @@ __device__ static inline uint32_t knob_hash(const slo_knobs& k) {
   const uint32_t* x = reinterpret_cast<const uint32_t*>(&k);
   uint32_t h = 0x811C9DC5u;
   for (int i = 0; i < 8; ++i) h = (h ^ x[i]) * 0x01000193u;
-  return h;
+  return h ? h : 1u;                                     // 0 marks an empty slot
 }
 
 constexpr int kLookRaw = 1024;   // [K], N(K) (<= 31), N(c) for each c (31 x 31): 993 slots
@@ -417,7 +417,8 @@ __device__ static inline uint32_t block_excl(bool f, uint32_t* warp_tot, uint32_
 __global__ void __launch_bounds__(1024) slo_lookahead_prepare_kernel(slo_space space, const slo_climb_state* state,
                                                                       LookTable* T, slo_knobs* sim) {
   __shared__ slo_knobs raw[kLookRaw];
-  __shared__ uint32_t rh[kLookRaw];
+  __shared__ __align__(16) uint32_t rh[kLookRaw];        // slot hashes, 0 = empty slot (valid hashes are != 0)
+  __shared__ uint32_t oh[kLookCap];                      // the cache's hashes
   __shared__ uint32_t cnt[32];
   __shared__ uint32_t warp_tot[32];
   __shared__ uint32_t s_tot;
@@ -438,15 +439,18 @@ __global__ void __launch_bounds__(1024) slo_lookahead_prepare_kernel(slo_space s
   }
   const uint32_t h = valid ? knob_hash(raw[t]) : 0u;
   rh[t] = h;
+  const uint32_t n_old = T->n_old;
+  for (uint32_t j = t; j < n_old; j += blockDim.x) oh[j] = T->old_h[j];
   __syncthreads();
   bool first = valid;
-  for (uint32_t u = 0; first && u < t; ++u) {
-    bool vu = u <= nb;
-    if (u >= 32) {
-      const uint32_t i = 1 + (u - 32) / 31, j = (u - 32) % 31;
-      vu = i <= nb && j < cnt[i];
+  for (uint32_t u0 = 0; first && u0 < t; u0 += 4) {      // an equal record in an earlier slot? (4 hashes a load)
+    const uint4 q = *reinterpret_cast<const uint4*>(rh + u0);
+    const uint32_t hq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t u = u0 + (uint32_t)k;
+      if (u < t && hq[k] == h && knobs_equal(raw[u], raw[t])) first = false;
     }
-    if (vu && rh[u] == h && knobs_equal(raw[u], raw[t])) first = false;
   }
   const uint32_t pos = block_excl(first, warp_tot, &s_tot);
   const uint32_t n_new = s_tot < kLookCap ? s_tot : kLookCap;
@@ -460,13 +464,12 @@ __global__ void __launch_bounds__(1024) slo_lookahead_prepare_kernel(slo_space s
   }
   __syncthreads();
   // measured last round?  map[i] >= 0: the old table's entry; < 0: simulation list entry -map - 1
-  const uint32_t n_old = T->n_old;
   int32_t m = -1;
   if (t < n_new) {
     const slo_knobs k = T->new_k[t];
     const uint32_t hk = T->new_h[t];
     for (uint32_t j = 0; j < n_old; ++j)
-      if (T->old_h[j] == hk && knobs_equal(T->old_k[j], k)) {
+      if (oh[j] == hk && knobs_equal(T->old_k[j], k)) {
         m = (int32_t)j;
         break;
       }
@@ -485,7 +488,9 @@ __global__ void slo_lookahead_step_kernel(slo_space space, slo_score_params sp, 
   const int lane = threadIdx.x & 31;
   __shared__ slo_knobs cands[32], next[32];
   __shared__ slo_config_agg tab[kLookCap];
+  __shared__ uint32_t nh[kLookCap];
   const uint32_t n_new = T->n_new;
+  for (uint32_t i = lane; i < n_new; i += 32) nh[i] = T->new_h[i];
   for (uint32_t i = lane; i < n_new; i += 32) {          // the round's table: last round's or just simulated
     const int32_t m = T->map[i];
     slo_config_agg a{0, 0, 0, 0, 0};
@@ -517,7 +522,7 @@ __global__ void slo_lookahead_step_kernel(slo_space space, slo_score_params sp, 
       const uint32_t hk = knob_hash(k);
       if (k.conc != 0)
         for (uint32_t j = 0; j < n_new; ++j)
-          if (T->new_h[j] == hk && knobs_equal(T->new_k[j], k)) {
+          if (nh[j] == hk && knobs_equal(T->new_k[j], k)) {
             a = tab[j];
             break;
           }

@@ -147,6 +147,20 @@ class SweepGraph:
         self.sim.close()
 
 
+def final_rerun(sim, cfg, state: torch.Tensor, seeds, out=None, stream=None) -> dict:
+    """Alg. 1's last line ("Re-run one segment at K_best and report final metrics"; "re-measures it
+    at the end"): simulate K_best — read straight from the device climb state (bytes 32..64 of slo_climb_state)
+    — on `seeds` (a list or a device seeds tensor; a fresh seed block gives an independent segment) and return
+    its per-seed p99 / goodput and the pooled aggregate ("agg"), on the device (asynchronous on `stream`; `out`
+    from a previous call is reused)."""
+    from . import sim as S
+    kb = state.view(-1)[32:64].view(1, 32)
+    st = seeds if isinstance(seeds, torch.Tensor) else S.seeds_tensor(seeds, device=state.device)
+    out = sim.run_batch(kb, st, cfg.segment_len, cfg.warmup_len, cfg.slo_us, out=out, stream=stream)
+    out["agg"] = sim.aggregate(out["detail"], 1, st.shape[0], out=out.get("agg"), stream=stream)
+    return out
+
+
 class ClimbGraph:
     """Alg. 1 with the whole step — K0/K1/K1b simulate, K2 aggregate, all-gather (N > 1), K3 climb — captured
     once in a CUDA graph and replayed (SV §8(f) NEXT-4): no host round trip between steps.  The candidate

@@ -57,3 +57,28 @@ def test_lookahead_cache_converged_climb_simulates_nothing():
     assert first > 32 and la.simulated() == 0
     la.close()
     s.close()
+
+
+def test_final_rerun_of_k_best_matches_oracle():
+    """Alg. 1's final re-run of K_best on a fresh seed block, read from the device climb state, equals the
+    oracle's replicas of the same record on the same seeds."""
+    import oracle
+    from paper_2603_11340_b200._lib import CLIMB_DTYPE
+    from paper_2603_11340_b200.dist import LookaheadClimbGraph, final_rerun
+    cfg = inputs.config_c4(n_seeds=3, segment_len=300)
+    s = sim.Simulator(cfg.workloads, device=0)
+    la = LookaheadClimbGraph(s, cfg, inputs.seeds(3, 21), n_cand=32).capture()
+    la.run(3)
+    fresh = inputs.seeds(4, 900)
+    out = final_rerun(s, cfg, la.state, fresh)
+    torch.cuda.synchronize()
+    kb = sim.unpack_knobs(sim.unpack(la.state, CLIMB_DTYPE)[0]["K_best"].reshape(1))[0]
+    oracle.build()
+    exp = [oracle.run(cfg.workloads, kb, sd, cfg.segment_len, warmup_len=cfg.warmup_len, slo_us=cfg.slo_us)
+           for sd in fresh]
+    got_p99 = out["p99_us"].cpu().tolist()
+    assert got_p99 == [e["p99_us"] for e in exp]
+    gp = out["goodput"].cpu().tolist()
+    assert gp == [e["goodput"] for e in exp]
+    la.close()
+    s.close()

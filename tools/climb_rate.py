@@ -36,12 +36,13 @@ la.reset()
 assert torch.equal(la.states(20), h), "lookahead trajectory differs from the plain climb"
 
 
-def timed(stream, body):
+def timed(stream, body):            # replays on `stream` (CUDAGraph.replay launches on the current stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    body()
-    e1.record(stream)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        body()
+        e1.record(stream)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1)
 

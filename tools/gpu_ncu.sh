@@ -15,4 +15,5 @@ cap k1s_c2 slo_serve 3 "--steps 1 --warmup 3"
 cap k1c_c2c slo_sim_cont 1 "--workload c2c --steps 1 --warmup 1"
 cap k1s_c4s8 slo_serve 5 "--workload c4 --share-of 8 --eager-climb --steps 1 --warmup 3"
 cap k1s_c1 slo_serve 5 "--workload c1 --steps 1 --warmup 3"
+cap k1b_c2 slo_select 3 "--steps 1 --warmup 3"
 ls -la gpurun_out

@@ -12,3 +12,5 @@ N="ncu --clock-control none --target-processes application-only"
 timeout 600 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches_c2c.csv python bench.py --workload c2c --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 ls -la gpurun_out
+python tools/climb_rate.py > gpurun_out/climb_rate_c4.json 2>&1
+python tools/climb_rate.py --seeds 16 > gpurun_out/climb_rate_c4_share8.json 2>&1
