@@ -1,5 +1,5 @@
-"""Tiny run of every kernel (K0, K1g, K1s incl. its scans, K1, K1t and K1c in all lane-group modes, K1b, K2, K2b,
-K3) for compute-sanitizer."""
+"""Tiny run of every kernel (K0, K1g, K1s incl. its scans, K1, K1t and K1c in all lane-group modes, K1b at every
+block size and on caller rows, K2, K2b, K3, the lookahead climb's K3L) for compute-sanitizer."""
 import random
 import sys
 
@@ -41,5 +41,24 @@ st = s.climb_state(cfg.knobs[0])
 o2 = s.run_batch(cands, sim.seeds_tensor(cfg.seeds()), 100)
 a2 = s.aggregate(o2["detail"], 32, 2)
 s.hillclimb_step(cfg.extra["space"], cfg.extra["score"], cands, a2, 1, st)
+torch.cuda.synchronize()
+# K1b on caller rows: 64 / 128 / 256-thread blocks (row lengths 700 / 3000 / 5000; more rows than SMs), and a
+# bucket above the shared-memory capacity
+for n, R in ((700, 300), (3000, 200), (5000, 160)):
+    g = torch.Generator().manual_seed(n)
+    rows = torch.randint(0, 1 << 22, (R, n), generator=g, dtype=torch.int64)
+    rows[: R // 2, : n // 2] = 1_000_000
+    s.select_rows(rows.to(torch.int32).cuda(), percentiles=True)
+torch.cuda.synchronize()
+# the lookahead climb: prepare (U(K), cache lookup) -> simulate -> aggregate -> two steps, twice (cache hits)
+table = torch.zeros(34576, dtype=torch.uint8, device="cuda")
+sim_list = torch.zeros((320, 32), dtype=torch.uint8, device="cuda")
+traj = torch.empty((2, 104), dtype=torch.uint8, device="cuda")
+st2 = s.climb_state(cfg.knobs[0])
+for _ in range(2):
+    s.lookahead_prepare(cfg.extra["space"], st2, table, sim_list)
+    o3 = s.run_batch(sim_list, sim.seeds_tensor(cfg.seeds()), 100)
+    a3 = s.aggregate(o3["detail"], 320, 2)
+    s.lookahead_step(cfg.extra["space"], cfg.extra["score"], table, a3, 1, 32, st2, traj)
 torch.cuda.synchronize()
 print("sanitize run ok")
