@@ -178,7 +178,10 @@ typedef struct {
    * pre_base + pre_tok >= 3 and dec_base + dec_seq >= 3 and ver_base + ver_seq + ver_tok >= 3 (every batch and
    * iteration then lasts >= 1 us under any noise factor >= 0.4004), else SLO_E_INVAL. */
   uint32_t stop_min_completions, stop_min_time_us;
-  uint32_t reserved[2];         /* must be 0                                                              */
+  /* device u32 or NULL: only configs [0, *d_live_configs) are simulated; replicas of later configs are skipped
+   * entirely (nothing written for them, not counted) — a graph-captured caller with a fixed n_configs and a
+   * count known only on the device (the lookahead climb's simulation list) pays nothing for its padding */
+  const uint32_t* d_live_configs;
 } slo_run_args;
 slo_status slo_sim_run(slo_sim* h, const slo_run_args* args, void* stream);
 

@@ -77,7 +77,7 @@ class slo_run_args(C.Structure):
                 ("slo_us", C.c_uint32), ("d_p99_us", C.c_void_p), ("d_goodput", C.c_void_p),
                 ("d_detail", C.c_void_p), ("d_latencies", C.c_void_p), ("d_stats", C.c_void_p),
                 ("d_p50_us", C.c_void_p), ("d_p95_us", C.c_void_p), ("stop_min_completions", C.c_uint32),
-                ("stop_min_time_us", C.c_uint32), ("reserved", C.c_uint32 * 2)]
+                ("stop_min_time_us", C.c_uint32), ("d_live_configs", C.c_void_p)]
 
 
 class slo_space(C.Structure):

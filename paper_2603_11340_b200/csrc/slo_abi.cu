@@ -397,7 +397,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
                              uint32_t n_seeds, uint32_t segment_len, uint32_t warmup_len, uint32_t slo_us,
                              uint32_t* d_p99, double* d_goodput, slo_replica_result* d_detail, uint32_t* d_lat,
                              slo_stats* d_stats, uint32_t* d_p50, uint32_t* d_p95, cudaStream_t st,
-                             uint32_t stop_n = 0, uint32_t stop_t = 0) {
+                             uint32_t stop_n = 0, uint32_t stop_t = 0, const uint32_t* d_live = nullptr) {
   const uint32_t n_rep = (uint32_t)((uint64_t)n_configs * n_seeds);
   const uint32_t N = warmup_len + segment_len;
   // replicas per launch chunk: the latency rows of a chunk stay within the budget (a caller-provided
@@ -460,6 +460,7 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
   p.crn = h->crn;
   p.stop_n = stop_n;
   p.stop_t = stop_t;
+  p.live = d_live;
   p.warp_bytes = (uint32_t)slo::group_warp_bytes();
   const size_t smem = (size_t)p.warp_bytes * h->warps_per_block;
   if (smem > 48 * 1024)
@@ -547,10 +548,10 @@ static slo_status launch_sim(slo_sim* h, const slo_knobs* d_configs, uint32_t n_
     // (a lone replica runs K1's inline generation fastest on a whole warp; K1s's chain is shortest on narrow
     // groups, spread one replica per warp by gpw below)
     slo::slo_classify_count_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc,
-                                                                    h->n_wl, wide, h->d_ctl);
+                                                                    h->n_wl, wide, h->d_ctl, d_live);
     CUDA_TRY(h, cudaGetLastError());
     slo::slo_classify_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_configs, h->d_wl, n_seeds, (uint32_t)r0, nc, h->n_wl,
-                                                              wide, h->d_ctl, h->d_lists);
+                                                              wide, h->d_ctl, h->d_lists, d_live);
     CUDA_TRY(h, cudaGetLastError());
     if ((s = mark(1, st)) != SLO_OK) return s;
     uint64_t blocks = (uint64_t)bps * h->sm_count;
@@ -655,8 +656,6 @@ slo_status slo_sim_run(slo_sim* h, const slo_run_args* a, void* stream) {
   if (!h) return fail(nullptr, SLO_E_INVAL, "run: null handle");
   if (!a || !a->d_configs || !a->d_seeds || !a->d_p99_us || !a->d_goodput)
     return fail(h, SLO_E_INVAL, "run: null pointer");
-  for (int i = 0; i < 2; ++i)
-    if (a->reserved[i]) return fail(h, SLO_E_INVAL, "run: reserved must be 0");
   slo_status s = check_run_args(h, a->n_configs, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us);
   if (s != SLO_OK) return s;
   if (a->stop_min_completions || a->stop_min_time_us) {
@@ -673,7 +672,7 @@ slo_status slo_sim_run(slo_sim* h, const slo_run_args* a, void* stream) {
   DeviceGuard g(h->device);
   return launch_sim(h, a->d_configs, a->n_configs, a->d_seeds, a->n_seeds, a->segment_len, a->warmup_len, a->slo_us,
                     a->d_p99_us, a->d_goodput, a->d_detail, a->d_latencies, a->d_stats, a->d_p50_us, a->d_p95_us,
-                    (cudaStream_t)stream, a->stop_min_completions, a->stop_min_time_us);
+                    (cudaStream_t)stream, a->stop_min_completions, a->stop_min_time_us, a->d_live_configs);
 }
 
 slo_status slo_sim_run_batch(slo_sim* h, const slo_knobs* d_configs, uint32_t n_configs, const uint64_t* d_seeds,
@@ -998,6 +997,8 @@ slo_status slo_select_rows(slo_sim* h, const uint32_t* d_rows, uint32_t n_rows, 
   p.p95 = d_p95_us;
   p.goodput = h->d_sel_gp;
   p.n_rep = n_rows;
+  p.n_seeds = 1;
+  p.n_cfg = n_rows;
   p.r_base = 0;
   p.n_chunk = n_rows;
   p.warmup = 0;

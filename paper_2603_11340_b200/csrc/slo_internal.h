@@ -53,6 +53,7 @@ struct SimParams {
   uint32_t warp_bytes, gpw;    // per-warp shared memory; K1s: lane groups per warp in use (1..4)
   uint32_t stop_n, stop_t;     // segment stop rule, 0, 0 = off
   const uint4* rec;            // split path: [n_chunk][N] request records written by K1g (nullptr: inline)
+  const uint32_t* live;        // nullable: only configs [0, *live) are simulated (slo_run_args.d_live_configs)
 };
 
 template <bool STOP> __global__ void slo_sim_kernel_t(const SimParams p);       // K1 (STOP: §2.14 stop rule)
@@ -67,9 +68,10 @@ template <bool STOP, bool THINK, bool SPLIT> __global__ void slo_sim_cont_kernel
 template <bool STOP> __global__ void slo_sim_think_kernel_t(const SimParams p); // K1t: think-time closed loop (§2.11)
 __global__ void slo_classify_count_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds,
                                           uint32_t r_base, uint32_t n_chunk, uint32_t n_wl, uint32_t wide,
-                                          uint32_t* ctl);
+                                          uint32_t* ctl, const uint32_t* live);
 __global__ void slo_classify_kernel(const slo_knobs* cfg, const DevWorkload* wl, uint32_t n_seeds, uint32_t r_base,
-                                    uint32_t n_chunk, uint32_t n_wl, uint32_t wide, uint32_t* ctl, uint32_t* lists);
+                                    uint32_t n_chunk, uint32_t n_wl, uint32_t wide, uint32_t* ctl, uint32_t* lists,
+                                    const uint32_t* live);
 __global__ void slo_select_kernel(const SimParams p);
 size_t group_warp_bytes();   // per-warp shared memory of K1
 size_t serve_warp_bytes();   // per-warp shared memory of K1s

@@ -1850,9 +1850,10 @@ __device__ __forceinline__ uint32_t work_class(const slo_knobs& k, const DevWork
 
 __global__ void slo_classify_count_kernel(const slo_knobs* __restrict__ cfg, const DevWorkload* __restrict__ wl,
                                           uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk, uint32_t n_wl,
-                                          uint32_t wide, uint32_t* __restrict__ ctl) {
+                                          uint32_t wide, uint32_t* __restrict__ ctl, const uint32_t* __restrict__ live) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_chunk) return;
+  if (live && (r_base + t) / n_seeds >= *live) return;     // a skipped config: no work list, no outputs
   uint32_t bucket;
   const uint32_t cls = work_class(cfg[(r_base + t) / n_seeds], wl, n_wl, wide, bucket);
   atomicAdd(ctl + kCtlBucket + cls * 16 + bucket, 1u);     // per (class, bucket) counts
@@ -1860,7 +1861,8 @@ __global__ void slo_classify_count_kernel(const slo_knobs* __restrict__ cfg, con
 
 __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, const DevWorkload* __restrict__ wl,
                                     uint32_t n_seeds, uint32_t r_base, uint32_t n_chunk, uint32_t n_wl,
-                                    uint32_t wide, uint32_t* __restrict__ ctl, uint32_t* __restrict__ lists) {
+                                    uint32_t wide, uint32_t* __restrict__ ctl, uint32_t* __restrict__ lists,
+                                    const uint32_t* __restrict__ live) {
   __shared__ uint32_t off[16 * kLists];
   if (threadIdx.x < kLists) {                      // exclusive offsets of the buckets inside each list
     uint32_t acc = 0;
@@ -1874,6 +1876,7 @@ __global__ void slo_classify_kernel(const slo_knobs* __restrict__ cfg, const Dev
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_chunk) return;
   const uint32_t r = r_base + t;
+  if (live && r / n_seeds >= *live) return;
   uint32_t bucket;
   const uint32_t cls = work_class(cfg[r / n_seeds], wl, n_wl, wide, bucket);
   const uint32_t pos = off[cls * 16 + bucket] + atomicAdd(ctl + kCtlBucket + 16 * kLists + cls * 16 + bucket, 1u);
@@ -1979,8 +1982,10 @@ __global__ void __launch_bounds__(256) slo_select_kernel(const SimParams p) {
   const uint32_t N = p.warmup + p.seg;
   const uint32_t n = p.seg;                        // row length (stop rule: uncounted entries hold UINT32_MAX)
 
+  const uint32_t live_cfg = p.live ? *p.live : 0xFFFFFFFFu;
   for (uint32_t t = blockIdx.x; t < p.n_chunk; t += gridDim.x) {
     const uint32_t r = p.r_base + t;
+    if (p.live && r / p.n_seeds >= live_cfg) continue;   // a skipped config (slo_run_args.d_live_configs)
     const slo_replica_result pr = p.part[r];
     if (pr.flags & 1u) {
       if (threadIdx.x == 0) {

@@ -330,7 +330,9 @@ class LookaheadClimbGraph:
     def _round(self):
         c, st = self.cfg, self.stream
         self.sim.lookahead_prepare(self.space, self.state, self.table, self.sim_list, stream=st)
-        self.sim.run_batch(self.sim_list, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out, stream=st)
+        # only the table's n_sim records are simulated (its 3rd word): the padding costs nothing
+        self.sim.run_batch(self.sim_list, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out, stream=st,
+                           live_configs_ptr=self.table.data_ptr() + 8)
         self.sim.aggregate(self.out["detail"], self.CAP, self.n_seeds, out=self.agg, stream=st)
         if self.w > 1:
             dist.all_gather_into_tensor(self.parts, self.agg)

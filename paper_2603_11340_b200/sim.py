@@ -182,7 +182,7 @@ class Simulator:
     def run_batch(self, configs: torch.Tensor, seeds: torch.Tensor, segment_len: int, warmup_len: int = 0,
                   slo_us: int = 1_200_000, detail: bool = True, latencies: bool = False, stats: bool = False,
                   percentiles: bool = False, out: Optional[Dict] = None, stream=None, stop_n_min: int = 0,
-                  stop_t_min_us: int = 0) -> Dict:
+                  stop_t_min_us: int = 0, live_configs_ptr: int = 0) -> Dict:
         """K0/K1/K1b over n_configs x n_seeds replicas (config-major).  Asynchronous on `stream`."""
         n_cfg = configs.shape[0]
         n_seeds = seeds.shape[0]
@@ -196,6 +196,7 @@ class Simulator:
         a.d_detail, a.d_latencies, a.d_stats = _ptr(out.get("detail")), _ptr(out.get("latencies")), _ptr(out.get("stats"))
         a.d_p50_us, a.d_p95_us = _ptr(out.get("p50_us")), _ptr(out.get("p95_us"))
         a.stop_min_completions, a.stop_min_time_us = stop_n_min, stop_t_min_us
+        a.d_live_configs = live_configs_ptr or None     # device u32: only configs [0, value) simulated
         check(lib().slo_sim_run(self.h, C.byref(a), _stream_ptr(stream)), self.h)
         return out
 

@@ -82,3 +82,31 @@ def test_final_rerun_of_k_best_matches_oracle():
     assert gp == [e["goodput"] for e in exp]
     la.close()
     s.close()
+
+
+def test_live_configs_skip_padding():
+    """slo_run_args.d_live_configs: configs [0, L) give exactly a plain run's outputs, later configs' outputs are
+    not touched and their replicas are not counted (static, continuous and mixed knobs)."""
+    import random
+    from paper_2603_11340_b200._lib import STATS_DTYPE
+    rng = random.Random(8)
+    wls = [inputs.preset_ll(), inputs.continuous(inputs.preset_ll()), inputs.preset_stress(kind=1)]
+    ks = [inputs.random_knobs(rng, n_wl=len(wls)) for _ in range(20)]
+    seeds = inputs.seeds(3, 4)
+    s = sim.Simulator(wls, device=0)
+    dev = torch.device("cuda", 0)
+    kt, st = sim.knobs_tensor(ks, device=dev), sim.seeds_tensor(seeds, device=dev)
+    for L in (0, 1, 7, 20):
+        live = torch.tensor([L], dtype=torch.int32, device=dev)
+        out = s.alloc_outputs(len(ks) * 3, stats=True)
+        out["p99_us"].fill_(-7)
+        out["goodput"].fill_(-7.0)
+        s.run_batch(kt, st, 400, warmup_len=20, out=out, live_configs_ptr=live.data_ptr(), stats=True)
+        ref = s.run_batch(kt[:max(L, 1)], st, 400, warmup_len=20, stats=True)
+        torch.cuda.synchronize()
+        n = 3 * L
+        assert torch.equal(out["p99_us"][:n], ref["p99_us"][:n]) and torch.equal(out["goodput"][:n], ref["goodput"][:n])
+        assert bool((out["p99_us"][n:] == -7).all()) and bool((out["goodput"][n:] == -7.0).all())
+        req = int(sim.unpack(out["stats"], STATS_DTYPE)[0]["requests"])
+        assert req == n * 420, (L, req)
+    s.close()
