@@ -327,14 +327,19 @@ class LookaheadClimbGraph:
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
 
-    def _round(self):
+    def _round(self, host_gather: bool = False):
         c, st = self.cfg, self.stream
         self.sim.lookahead_prepare(self.space, self.state, self.table, self.sim_list, stream=st)
         # only the table's n_sim records are simulated (its 3rd word): the padding costs nothing
         self.sim.run_batch(self.sim_list, self.seeds, c.segment_len, c.warmup_len, c.slo_us, out=self.out, stream=st,
                            live_configs_ptr=self.table.data_ptr() + 8)
         self.sim.aggregate(self.out["detail"], self.CAP, self.n_seeds, out=self.agg, stream=st)
-        if self.w > 1:
+        if self.w > 1 and host_gather:                     # eager over a host backend (gloo): stage through host
+            st.synchronize()
+            parts = torch.empty(tuple(self.parts.shape), dtype=torch.uint8)
+            dist.all_gather_into_tensor(parts, self.agg.cpu())
+            self.parts.copy_(parts)
+        elif self.w > 1:
             dist.all_gather_into_tensor(self.parts, self.agg)
         self.sim.lookahead_step(self.space, self.sp, self.table, self.parts, self.w, self.n_cand, self.state,
                                 self.traj, stream=st)
@@ -365,6 +370,18 @@ class LookaheadClimbGraph:
         for _ in range(rounds):
             self.graph.replay()
         return self.state
+
+    def run_eager(self, rounds: int) -> torch.Tensor:
+        """The rounds without a graph (a multi-rank run over a host backend such as gloo, whose collectives a CUDA
+        graph cannot capture); returns the state after every step, uint8 [2 rounds, 104] (host)."""
+        host = self.w > 1 and dist.get_backend() != "nccl"
+        h = torch.empty((rounds, 2, self.state.numel()), dtype=torch.uint8)
+        with torch.cuda.stream(self.stream):
+            for i in range(rounds):
+                self._round(host_gather=host)
+                h[i].copy_(self.traj.cpu())
+        self.stream.synchronize()
+        return h.view(2 * rounds, -1)
 
     def states(self, rounds: int) -> torch.Tensor:
         """Replay `rounds` rounds and return the climb state after every step: uint8 [2 rounds, 104] (host)."""

@@ -110,3 +110,29 @@ def test_live_configs_skip_padding():
         req = int(sim.unpack(out["stats"], STATS_DTYPE)[0]["requests"])
         assert req == n * 420, (L, req)
     s.close()
+
+
+def test_lookahead_seed_sharded_two_ranks(tmp_path):
+    """Two ranks (gloo, sharing the box's GPU) each simulate half of the seeds of every round's records; the
+    all-gathered parts summed by K3L-step give every step's state bit for bit equal to one process over all
+    seeds (integer sums: the pooled aggregates do not depend on the split)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from paper_2603_11340_b200.dist import LookaheadClimbGraph
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    rounds, out = 3, tmp_path / "la.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29541", os.path.join(root, "tests", "lookahead_worker.py"),
+           str(out), str(rounds)]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=420)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    got = json.load(open(out))["states"]
+    cfg = inputs.config_c4(n_seeds=8, segment_len=400)
+    s = sim.Simulator(cfg.workloads, device=0)
+    la = LookaheadClimbGraph(s, cfg, cfg.seeds(), n_cand=32).capture()
+    ref = la.states(rounds)
+    assert [ref[i].numpy().tobytes().hex() for i in range(ref.shape[0])] == got
+    la.close()
+    s.close()
