@@ -14,3 +14,4 @@ timeout 600 $N --metrics gpu__time_duration.sum --csv --log-file gpurun_out/laun
 ls -la gpurun_out
 python tools/climb_rate.py > gpurun_out/climb_rate_c4.json 2>&1
 python tools/climb_rate.py --seeds 16 > gpurun_out/climb_rate_c4_share8.json 2>&1
+python bench.py --workload c5 --no-cpu-baseline --steps 2 --warmup 1 > gpurun_out/bench_c5.json 2>gpurun_out/bench_c5.err
