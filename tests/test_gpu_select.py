@@ -91,3 +91,20 @@ def test_select_rows_many_rows_one_wave(S):
     torch.cuda.synchronize()
     got = out["p99_us"].cpu().numpy().view(np.uint32).astype(np.uint64)
     np.testing.assert_array_equal(got, expected(rows, nm, 99))
+
+
+@pytest.mark.parametrize("n", [700, 3000, 5001])
+def test_select_rows_block_sizes(S, n):
+    """More rows than SMs, so K1b takes its row-length block size (64 / 128 / 256 threads for these lengths);
+    every adversarial family repeated over 300 rows."""
+    rng = np.random.default_rng(50 + n)
+    fam = families(rng, n)
+    rows = np.concatenate([fam] * (300 // len(fam) + 1))[:300]
+    rows[::7] = rng.integers(0, 2**32, (len(rows[::7]), n), dtype=np.uint64)
+    nm = np.full(len(rows), n, dtype=np.uint64)
+    t = torch.from_numpy(rows.astype(np.uint32).view(np.int32)).to(torch.device("cuda", 0))
+    out = S.select_rows(t, percentiles=True)
+    torch.cuda.synchronize()
+    for key, q in (("p99_us", 99), ("p50_us", 50), ("p95_us", 95)):
+        got = out[key].cpu().numpy().view(np.uint32).astype(np.uint64)
+        np.testing.assert_array_equal(got, expected(rows, nm, q), err_msg=f"{key} n={n}")
