@@ -955,9 +955,12 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
       maxP = gmax<G>(member ? wj & 0x1FFFu : 0u);
     }
     const uint64_t f = R.f[h % RING];                  // the head's noise factor
-    const uint64_t t0 = t_form + f * ((uint64_t)pre_base + (uint64_t)pre_tok * maxP) / 1000000u;
+    // f times the cost coefficients (known at the batch head, off the rank -> completion chain); the sums are
+    // the same integers as f (pre_base + pre_tok maxP) and f (alpha0 S + alpha1 summin)
+    const uint64_t fpb = f * pre_base, fpt = f * pre_tok, fa0 = f * alpha0, fa1 = f * alpha1;
+    const uint64_t t0 = t_form + (fpb + fpt * maxP) / 1000000u;
     const uint32_t summin = lts + S * (b - rank);
-    const uint64_t c = t0 + f * (alpha0 * S + alpha1 * summin) / 1000000u;
+    const uint64_t c = t0 + (fa0 * S + fa1 * summin) / 1000000u;
     if (member) R.kap[(h + rank) % KRING] = c;
     const uint32_t lastm = gballot<G>(member && rank + 1u == b, lane);
     const int ll = lastm ? __ffs(lastm) - 1 : 0;

@@ -10,9 +10,11 @@ top = int(sys.argv[7]) if len(sys.argv) > 7 else 60
 rows = list(csv.reader(open(csvp)))
 hdr = rows[1]
 ie, ad = hdr.index("Instructions Executed"), hdr.index("Address")
+sc = hdr.index("Warp Stall Sampling (All Samples)") if "Warp Stall Sampling (All Samples)" in hdr else None
 data = [r for r in rows[2:] if len(r) > ie]
 base = int(data[0][ad], 16)
 cnt = {int(r[ad], 16) - base: float(r[ie] or 0) for r in data}
+stl = {int(r[ad], 16) - base: float(r[sc] or 0) for r in data} if sc is not None else {}
 # parse the function's section of nvdisasm -gi output
 lines = open(disp).read().split("\n")
 start = next(i for i, l in enumerate(lines) if l.startswith(".text." + fn + ":"))
@@ -39,13 +41,16 @@ for l in lines[start + 1:]:
                 key = ln
         attr[off] = (key, frames[0] if frames else None, m.group(2).split()[0] if m.group(2).split() else "?")
 tot = sum(cnt.values())
-by_line, by_inner = defaultdict(float), defaultdict(float)
+by_line, by_inner, by_stall = defaultdict(float), defaultdict(float), defaultdict(float)
 for off, c in cnt.items():
     k, inner, op = attr.get(off, (None, None, "?"))
     by_line[k] += c
     by_inner[inner] += c
+    by_stall[k] += stl.get(off, 0.0)
+tst = sum(stl.values()) or 1.0
 src = open([p for p in [fname] if p][0] if False else "/root/repo/paper_2603_11340_b200/csrc/" + fname).read().split("\n")
 print(f"total warp instructions {tot:.4e}")
-for k, v in sorted(by_line.items(), key=lambda x: -x[1])[:top]:
+key = (lambda x: -by_stall[x[0]]) if "--by-stall" in sys.argv else (lambda x: -x[1])
+for k, v in sorted(by_line.items(), key=key)[:top]:
     txt = src[k - 1].strip()[:100] if k else "(outside)"
-    print(f"{100 * v / tot:6.2f}%  {k}  {txt}")
+    print(f"{100 * v / tot:6.2f}% inst {100 * by_stall[k] / tst:6.2f}% stall  {k}  {txt}")
