@@ -346,9 +346,11 @@ slo_status slo_select_rows(slo_sim* h, const uint32_t* d_rows, uint32_t n_rows, 
  * are simulated.  The trajectory is the plain climb's (slo_hillclimb_step with n_cand candidates) step for step.
  * d_table: SLO_LOOKAHEAD_TABLE_BYTES of device memory, zero-filled before the first round (empty cache).
  *   slo_lookahead_prepare: builds U(state.K), looks it up in the cache and writes the records to simulate into
- *     d_sim[0 .. SLO_LOOKAHEAD_CAP) (the rest padded with invalid records, conc = 0: no simulation work); the
- *     caller then runs slo_sim_run_batch on d_sim x seeds and slo_aggregate into SLO_LOOKAHEAD_CAP aggregates
- *     (n_parts rank parts of them, [part][SLO_LOOKAHEAD_CAP], for a seed-sharded multi-GPU climb);
+ *     d_sim[0 .. SLO_LOOKAHEAD_CAP) (the rest padded with invalid records, conc = 0) and their count into the
+ *     table's 3rd u32 word (byte offset 8); the caller then runs slo_sim_run on d_sim x seeds with
+ *     d_live_configs = d_table + 8 bytes (the padding is then skipped entirely; slo_sim_run_batch also works,
+ *     simulating the padding as invalid records) and slo_aggregate into SLO_LOOKAHEAD_CAP aggregates (n_parts rank
+ *     parts of them, [part][SLO_LOOKAHEAD_CAP], for a seed-sharded multi-GPU climb);
  *   slo_lookahead_step: assembles U's aggregates (cache or the new parts, summed), takes two steps on *d_state
  *     (n_cand in [2, 32], the plain climb's candidate count), writes the state after each into d_traj[0..2)
  *     and keeps U's table as the next round's cache.
