@@ -381,6 +381,7 @@ class LookaheadClimbGraph:
                 self._round(host_gather=host)
                 h[i].copy_(self.traj.cpu())
         self.stream.synchronize()
+        self.check()
         return h.view(2 * rounds, -1)
 
     def states(self, rounds: int) -> torch.Tensor:
@@ -395,7 +396,15 @@ class LookaheadClimbGraph:
                 self.graph.replay()
                 h[i].copy_(self.traj, non_blocking=True)
         st.synchronize()
+        self.check()
         return h.view(2 * rounds, -1)
+
+    def check(self) -> None:
+        """Raise if a round's U(K) exceeded the table's capacity (the table's 4th word; not reachable with the
+        built-in stencils: tests/test_lookahead_cpu.py bounds |U| by 272)."""
+        over = int(self.table[12:16].view(torch.int32).item())
+        if over:
+            raise RuntimeError(f"lookahead: |U(K)| = {over} exceeds the capacity {self.CAP}")
 
     def simulated(self) -> int:
         """Records the last round simulated (the rest came from the cache)."""
