@@ -825,60 +825,64 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
   bool active = false, exhausted = (uint32_t)g >= p.gpw, closed = false, spec = false;
   uint4 stg{0, 0, 0, 0};                               // K1g record of request gen + li, loaded ahead
 
+  bool acq = true;
   for (;;) {
     __syncwarp();
     // ---- acquire replicas for idle groups
-    bool want = !active && !exhausted;
-    while (__any_sync(FULL, want)) {
-      uint32_t idx = 0;
-      if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
-      idx = gshfl<G>(idx, 0);
-      if (want) {
-        if (idx >= count) {
-          exhausted = true;
-        } else {
-          r = list[idx];
-          const uint32_t ci = r / p.n_seeds;
-          const slo_knobs k = p.cfg[ci];
-          if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
-            if (li == 0) {
-              p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
-              if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
-            }
+    if (acq) {   // acquisition and the exit test only after a replica finished (warp-uniform)
+      bool want = !active && !exhausted;
+      while (__any_sync(FULL, want)) {
+        uint32_t idx = 0;
+        if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
+        idx = gshfl<G>(idx, 0);
+        if (want) {
+          if (idx >= count) {
+            exhausted = true;
           } else {
-            const DevWorkload& W = p.wl[k.workload];
-            const uint64_t seed = p.seeds[r - ci * p.n_seeds];
-            const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
-            const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
-            uint32_t gp;
-            if (li == 0) {
-              R.wl = k.workload;
-              R.cnt_incl = 0;
+            r = list[idx];
+            const uint32_t ci = r / p.n_seeds;
+            const slo_knobs k = p.cfg[ci];
+            if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
+              if (li == 0) {
+                p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+                if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+              }
+            } else {
+              const DevWorkload& W = p.wl[k.workload];
+              const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+              const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+              const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+              uint32_t gp;
+              if (li == 0) {
+                R.wl = k.workload;
+                R.cnt_incl = 0;
+              }
+              setup_replica<G, false>(R, W, k, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, gamma, gp, li, gmask);
+              C = k.conc;
+              B = k.max_num_seqs;
+              mw = k.max_wait_us;
+              spec = gamma > 0;
+              closed = W.kind >= 3;
+              pre_base = W.t.pre_base_us;
+              pre_tok = W.t.pre_tok_us;
+              noise = W.t.noise_step_ppm;
+              step_coeffs(W.t, gamma, k.draft_width, alpha0, alpha1);   // d(n) = alpha0 + alpha1 n (R10, R28)
+              rowoff = (r - p.r_base) * N;
+              stg = (uint32_t)li < N ? __ldcs(p.rec + rowoff + li) : uint4{0, 0, 0, 0};
+              h = 0;
+              gen = 0;
+              t_idle = 0;
+              my_slo = 0;
+              my_sum = 0;
+              active = true;
             }
-            setup_replica<G, false>(R, W, k, (uint32_t)seed, (uint32_t)(seed >> 32) ^ cfgkey, gamma, gp, li, gmask);
-            C = k.conc;
-            B = k.max_num_seqs;
-            mw = k.max_wait_us;
-            spec = gamma > 0;
-            closed = W.kind >= 3;
-            pre_base = W.t.pre_base_us;
-            pre_tok = W.t.pre_tok_us;
-            noise = W.t.noise_step_ppm;
-            step_coeffs(W.t, gamma, k.draft_width, alpha0, alpha1);   // d(n) = alpha0 + alpha1 n (R10, R28)
-            rowoff = (r - p.r_base) * N;
-            stg = (uint32_t)li < N ? __ldcs(p.rec + rowoff + li) : uint4{0, 0, 0, 0};
-            h = 0;
-            gen = 0;
-            t_idle = 0;
-            my_slo = 0;
-            my_sum = 0;
-            active = true;
           }
         }
+        want = !active && !exhausted;
       }
-      want = !active && !exhausted;
+      if (!__any_sync(FULL, active)) break;
+      acq = false;
     }
-    if (!__any_sync(FULL, active)) break;
     __syncwarp();
 
     // ---- (a2) keep [h, h + G) in the ring, up to 2G ahead: scan of the increments, bursty time change
@@ -1043,6 +1047,7 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
         }
       }
       if (fin) active = false;
+      acq = true;                                       // (the only way a group goes idle)
     }
     if (STOP && ct.steps >= 0x40000000u) flush_counters(p, ct);  // rare
   }
@@ -1308,65 +1313,69 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
   };
   constexpr uint32_t LOOK = SPLIT ? 2 * G : G;   // the split path refills one window ahead (record latency)
 
+  bool acq = true;
   for (;;) {
     __syncwarp();
     // ---- acquire replicas for idle groups
-    bool want = !active && !exhausted;
-    while (__any_sync(FULL, want)) {
-      uint32_t idx = 0;
-      if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
-      idx = gshfl<G>(idx, 0);
-      if (want) {
-        if (idx >= count) {
-          exhausted = true;
-        } else {
-          r = list[idx];
-          const uint32_t ci = r / p.n_seeds;
-          const slo_knobs k = p.cfg[ci];
-          if (!knobs_valid(k, p.n_wl)) {   // (K0 puts invalid records in list 0; kept for safety)
-            if (li == 0) {
-              p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
-              if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
-            }
+    if (acq) {   // acquisition and the exit test only after a replica finished (warp-uniform)
+      bool want = !active && !exhausted;
+      while (__any_sync(FULL, want)) {
+        uint32_t idx = 0;
+        if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
+        idx = gshfl<G>(idx, 0);
+        if (want) {
+          if (idx >= count) {
+            exhausted = true;
           } else {
-            const DevWorkload& W = p.wl[k.workload];
-            const uint64_t seed = p.seeds[r - ci * p.n_seeds];
-            const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
-            k0 = (uint32_t)seed;
-            k1 = (uint32_t)(seed >> 32) ^ cfgkey;
-            gamma = k.spec_on ? k.draft_len : 0u;
-            uint32_t gp;
-            if (li == 0) R.wl = k.workload;
-            setup_replica<G, !SPLIT>(R, W, k, k0, k1, gamma, gp, li, gmask);
-            C = k.conc;
-            B = k.max_num_seqs;
-            closed = W.kind >= 3;
-            if constexpr (THINK) {                       // the first C chains are ready at t = 0
-              pq = ((uint32_t)li < C && (uint32_t)li < N) ? 0ull : INF64;
-              pid = (uint32_t)li;
+            r = list[idx];
+            const uint32_t ci = r / p.n_seeds;
+            const slo_knobs k = p.cfg[ci];
+            if (!knobs_valid(k, p.n_wl)) {   // (K0 puts invalid records in list 0; kept for safety)
+              if (li == 0) {
+                p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+                if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+              }
+            } else {
+              const DevWorkload& W = p.wl[k.workload];
+              const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+              const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+              k0 = (uint32_t)seed;
+              k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+              gamma = k.spec_on ? k.draft_len : 0u;
+              uint32_t gp;
+              if (li == 0) R.wl = k.workload;
+              setup_replica<G, !SPLIT>(R, W, k, k0, k1, gamma, gp, li, gmask);
+              C = k.conc;
+              B = k.max_num_seqs;
+              closed = W.kind >= 3;
+              if constexpr (THINK) {                       // the first C chains are ready at t = 0
+                pq = ((uint32_t)li < C && (uint32_t)li < N) ? 0ull : INF64;
+                pid = (uint32_t)li;
+              }
+              noise = W.t.noise_step_ppm;
+              alpha0 = (uint32_t)R.alpha0;                 // d(n) = alpha0 + alpha1 n
+              alpha1 = (uint32_t)R.alpha1;
+              rowoff = (r - p.r_base) * N;
+              if constexpr (SPLIT) stg = (uint32_t)li < N ? __ldcs(p.rec + rowoff + li) : uint4{0, 0, 0, 0};
+              t = 0;
+              s_next = INF64;
+              a_w = 0;
+              nq = ndone = gen = it = nrun = npre = 0;
+              nzc = 2 * G;                                 // noise window empty: filled at the first decode
+              run = false;
+              my_slo = 0;
+              my_sum = 0;
+              my_cmax = 0;
+              need_s = true;
+              active = true;
             }
-            noise = W.t.noise_step_ppm;
-            alpha0 = (uint32_t)R.alpha0;                 // d(n) = alpha0 + alpha1 n
-            alpha1 = (uint32_t)R.alpha1;
-            rowoff = (r - p.r_base) * N;
-            if constexpr (SPLIT) stg = (uint32_t)li < N ? __ldcs(p.rec + rowoff + li) : uint4{0, 0, 0, 0};
-            t = 0;
-            s_next = INF64;
-            a_w = 0;
-            nq = ndone = gen = it = nrun = npre = 0;
-            nzc = 2 * G;                                 // noise window empty: filled at the first decode
-            run = false;
-            my_slo = 0;
-            my_sum = 0;
-            my_cmax = 0;
-            need_s = true;
-            active = true;
           }
         }
+        want = !active && !exhausted;
       }
-      want = !active && !exhausted;
+      if (!__any_sync(FULL, active)) break;
+      acq = false;
     }
-    if (!__any_sync(FULL, active)) break;
     __syncwarp();   // setup / previous iteration's ring writes before this iteration's reads
     if (lane == 0) KPROF(0, 1u);
     if (li == 0) KPROF(1, active ? 1u : 0u);
@@ -1637,6 +1646,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         }
       }
       if (done) active = false;
+      acq = true;                                       // (the only way a group goes idle)
       if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u || ct.blocks >= 0x40000000u) flush_counters(p, ct);
     }
   }
