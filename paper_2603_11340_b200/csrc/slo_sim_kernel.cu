@@ -555,56 +555,60 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   uint64_t pq = INF64;        // THINK: this lane's pending ready instant
   uint32_t pid = 0xFFFFFFFFu; // THINK: its user chain id
 
+  bool acq = true;
   for (;;) {
     __syncwarp();   // every lane is past the previous iteration's reads of its group's record
     // ---- acquire replicas for idle groups
-    bool want = !active && !exhausted;
-    while (__any_sync(FULL, want)) {
-      uint32_t idx = 0;
-      if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
-      idx = gshfl<G>(idx, 0);
-      if (want) {
-        if (idx >= count) {
-          exhausted = true;
-        } else {
-          r = list[idx];
-          const uint32_t ci = r / p.n_seeds;
-          const slo_knobs k = p.cfg[ci];
-          if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
-            if (li == 0) {
-              p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
-              if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
-            }
+    if (acq) {   // acquisition and the exit test only after a replica finished (warp-uniform)
+      bool want = !active && !exhausted;
+      while (__any_sync(FULL, want)) {
+        uint32_t idx = 0;
+        if (want && li == 0) idx = atomicAdd(p.cursor + cls, 1u);
+        idx = gshfl<G>(idx, 0);
+        if (want) {
+          if (idx >= count) {
+            exhausted = true;
           } else {
-            const DevWorkload& W = p.wl[k.workload];
-            const uint64_t seed = p.seeds[r - ci * p.n_seeds];
-            const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
-            const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
-            const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
-            uint32_t gp;
-            if (li == 0) {
-              R.knob = make_uint4(k.conc, k.max_num_seqs, k.max_wait_us, gamma);
-              R.wl = k.workload;
-              R.cnt_incl = 0;
+            r = list[idx];
+            const uint32_t ci = r / p.n_seeds;
+            const slo_knobs k = p.cfg[ci];
+            if (!knobs_valid(k, p.n_wl)) {  // sentinel outputs
+              if (li == 0) {
+                p.part[r] = slo_replica_result{0xFFFFFFFFu, 0, 0, 1u, 0, 0};
+                if (p.stats) atomicAdd((unsigned long long*)&p.stats->replicas, 1ull);
+              }
+            } else {
+              const DevWorkload& W = p.wl[k.workload];
+              const uint64_t seed = p.seeds[r - ci * p.n_seeds];
+              const uint32_t cfgkey = p.crn ? W.stream_id : fnv1a_knobs(k);
+              const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ cfgkey;
+              const uint32_t gamma = k.spec_on ? k.draft_len : 0u;
+              uint32_t gp;
+              if (li == 0) {
+                R.knob = make_uint4(k.conc, k.max_num_seqs, k.max_wait_us, gamma);
+                R.wl = k.workload;
+                R.cnt_incl = 0;
+              }
+              setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
+              rowoff = (r - p.r_base) * N;           // < 2^32: a chunk's rows are capped by the scratch budget
+              h = 0;
+              gen = 0;
+              t_idle = 0;
+              my_slo = 0;
+              my_sum = 0;
+              if constexpr (THINK) {                 // the first C chains are ready at t = 0
+                pq = ((uint32_t)li < k.conc && (uint32_t)li < N) ? 0ull : INF64;
+                pid = (uint32_t)li;
+              }
+              active = true;
             }
-            setup_replica<G>(R, W, k, k0, k1, gamma, gp, li, gmask);
-            rowoff = (r - p.r_base) * N;           // < 2^32: a chunk's rows are capped by the scratch budget
-            h = 0;
-            gen = 0;
-            t_idle = 0;
-            my_slo = 0;
-            my_sum = 0;
-            if constexpr (THINK) {                 // the first C chains are ready at t = 0
-              pq = ((uint32_t)li < k.conc && (uint32_t)li < N) ? 0ull : INF64;
-              pid = (uint32_t)li;
-            }
-            active = true;
           }
         }
+        want = !active && !exhausted;
       }
-      want = !active && !exhausted;
+      if (!__any_sync(FULL, active)) break;
+      acq = false;
     }
-    if (!__any_sync(FULL, active)) break;
     __syncwarp();   // orders this iteration's ring reads/writes after the previous iteration's (ring reuse)
 
     // ---- (a2, a3) keep [h, h + G) generated (groups with room generate ahead to share the pass)
@@ -771,6 +775,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
         }
       }
       if (fin) active = false;
+      acq = true;                                       // (the only way a group goes idle)
     }
     if (ct.steps >= 0x40000000u || ct.dsteps >= 0x40000000u) flush_counters(p, ct);  // rare
   }
