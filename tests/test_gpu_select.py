@@ -93,7 +93,7 @@ def test_select_rows_many_rows_one_wave(S):
     np.testing.assert_array_equal(got, expected(rows, nm, 99))
 
 
-@pytest.mark.parametrize("n", [700, 3000, 5001])
+@pytest.mark.parametrize("n", [1, 5, 700, 3000, 5001])
 def test_select_rows_block_sizes(S, n):
     """More rows than SMs, so K1b takes its row-length block size (64 / 128 / 256 threads for these lengths);
     every adversarial family repeated over 300 rows."""
