@@ -248,6 +248,62 @@ __host__ __device__ uint32_t neighbors_of(const slo_space& sp, const slo_knobs& 
   return n;
 }
 
+// the i-th raw move of neighbors_of's stencil order (i < raw_moves(sp)); a raw move equal to K or to an earlier
+// raw move is dropped there
+__device__ static inline uint32_t raw_moves(const slo_space& sp) { return sp.stencil == 0 ? 7u : (sp.stencil == 1 ? 8u : 31u); }
+__device__ static inline slo_knobs raw_move(const slo_space& sp, const slo_knobs& K, uint32_t i) {
+  if (sp.stencil == 0) {                 // conc -, +, max_num_seqs -, +, draft_len -, +, toggle
+    if (i == 6) {
+      slo_knobs t = K;
+      t.spec_on = K.spec_on ? 0 : 1;
+      return t;
+    }
+    return moved(sp, K, (int)(i >> 1), (i & 1) ? +1 : -1);
+  }
+  if (sp.stencil == 1) {                 // W, k, B, max_wait
+    const int order[4] = {3, 2, 1, 4};
+    return moved(sp, K, order[i >> 1], (i & 1) ? +1 : -1);
+  }
+  if (i < 26) {                          // (dc, db, dg) in {-1, 0, 1}^3 \ 0, lexicographic
+    const uint32_t v = i < 13 ? i : i + 1;
+    const int dc = (int)(v / 9) - 1, db = (int)((v / 3) % 3) - 1, dg = (int)(v % 3) - 1;
+    slo_knobs c = K;
+    dim_set(c, 0, clampi(dim_get(K, 0) + dc * sp.step[0], sp.lo[0], sp.hi[0]));
+    dim_set(c, 1, clampi(dim_get(K, 1) + db * sp.step[1], sp.lo[1], sp.hi[1]));
+    dim_set(c, 2, clampi(dim_get(K, 2) + dg * sp.step[2], sp.lo[2], sp.hi[2]));
+    return c;
+  }
+  if (i < 30) return moved(sp, K, i < 28 ? 3 : 4, (i & 1) ? +1 : -1);   // W -, +, max_wait -, +
+  slo_knobs t = K;
+  t.spec_on = K.spec_on ? 0 : 1;
+  return t;
+}
+
+// neighbors_of on one warp (every lane calls it; out in shared memory): lane i builds raw move i, keeps it when
+// it differs from K and from every raw move before it, and the kept moves are compacted in order (the first cap)
+__device__ static uint32_t neighbors_warp(const slo_space& sp, const slo_knobs& K, slo_knobs* out, uint32_t cap) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nraw = raw_moves(sp);
+  const bool have = lane < nraw;
+  const slo_knobs c = have ? raw_move(sp, K, lane) : K;
+  // raw moves differ from K only in words 0 (C, B, gamma, spec_on), 1 (W) and 3 (max_wait)
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(&c);
+  const uint32_t* kw = reinterpret_cast<const uint32_t*>(&K);
+  bool keep = have && !(cw[0] == kw[0] && cw[1] == kw[1] && cw[3] == kw[3]);
+  for (uint32_t j = 0; j + 1 < nraw; ++j) {
+    const uint32_t w0 = __shfl_sync(FULL, cw[0], (int)j), w1 = __shfl_sync(FULL, cw[1], (int)j),
+                   w3 = __shfl_sync(FULL, cw[3], (int)j);
+    if (j < lane && w0 == cw[0] && w1 == cw[1] && w3 == cw[3]) keep = false;
+  }
+  const uint32_t km = __ballot_sync(FULL, keep);
+  const uint32_t pos = __popc(km & ((1u << lane) - 1u));
+  __syncwarp();
+  if (keep && pos < cap) out[pos] = c;
+  __syncwarp();
+  const uint32_t n = __popc(km);
+  return n < cap ? n : cap;
+}
+
 // ------------------------------------------------------------------------------------------------
 // K3: one warp; lane k scores candidate k (Eq. 3), warp argmax, Alg. 1 move + best, next stencil.
 // ------------------------------------------------------------------------------------------------
@@ -347,11 +403,13 @@ __device__ static void climb_core(const slo_space& space, const slo_score_params
     st.moved = moved_;
     st.argmax = idx;
     next[0] = K;
-    uint32_t nn = 1 + neighbors_of(space, K, next + 1, n_cand > 0 ? n_cand - 1 : 0);
-    st.n_next = nn;
-    for (uint32_t i = nn; i < n_cand; ++i) next[i] = slo_knobs{};   // conc = 0: invalid, no simulation work
     *state = st;
   }
+  __syncwarp();
+  const slo_knobs K = next[0];                          // [K', neighbours(K'), padding] on the whole warp
+  const uint32_t nn = 1 + neighbors_warp(space, K, next + 1, n_cand > 0 ? n_cand - 1 : 0);
+  for (uint32_t i = nn + (uint32_t)lane; i < n_cand; i += 32) next[i] = slo_knobs{};   // conc = 0: invalid
+  if (lane == 0) state->n_next = nn;
   __syncwarp();
 }
 
@@ -423,13 +481,19 @@ __global__ void __launch_bounds__(1024) slo_lookahead_prepare_kernel(slo_space s
   __shared__ uint32_t warp_tot[32];
   __shared__ uint32_t s_tot;
   const uint32_t t = threadIdx.x;
-  if (t == 0) {
-    raw[0] = state->K;
-    cnt[0] = neighbors_of(space, raw[0], raw + 1, 31);
+  const uint32_t wid = t >> 5;
+  if (wid == 0) {
+    if (t == 0) raw[0] = state->K;
+    __syncwarp();
+    const uint32_t n1 = neighbors_warp(space, raw[0], raw + 1, 31);
+    if (t == 0) cnt[0] = n1;
   }
   __syncthreads();
   const uint32_t nb = cnt[0];
-  if (t >= 1 && t <= nb) cnt[t] = neighbors_of(space, raw[t], raw + 32 + (t - 1) * 31, 31);
+  if (wid >= 1 && wid <= nb) {                           // warp w: the neighbours of raw[w]
+    const uint32_t nw = neighbors_warp(space, raw[wid], raw + 32 + (wid - 1) * 31, 31);
+    if ((t & 31) == 0) cnt[wid] = nw;
+  }
   __syncthreads();
   // slot t holds a candidate: 0 = K, 1..nb = N(K), 32 + 31 (i - 1) + j = the j-th neighbour of raw[i]
   bool valid = t <= nb;
@@ -509,10 +573,11 @@ __global__ void slo_lookahead_step_kernel(slo_space space, slo_score_params sp, 
     }
     tab[i] = a;
   }
-  if (lane == 0) {                                       // [K, neighbours(K), padding]: the plain climb's list
-    cands[0] = state->K;
-    const uint32_t nn = 1 + neighbors_of(space, cands[0], cands + 1, n_cand - 1);
-    for (uint32_t i = nn; i < n_cand; ++i) cands[i] = slo_knobs{};
+  if (lane == 0) cands[0] = state->K;                   // [K, neighbours(K), padding]: the plain climb's list
+  __syncwarp();
+  {
+    const uint32_t nn = 1 + neighbors_warp(space, cands[0], cands + 1, n_cand - 1);
+    for (uint32_t i = nn + (uint32_t)lane; i < n_cand; i += 32) cands[i] = slo_knobs{};
   }
   __syncwarp();
   for (int st = 0; st < 2; ++st) {

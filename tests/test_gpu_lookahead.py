@@ -4,6 +4,8 @@ Its trajectory must equal the plain device climb's (dist.ClimbGraph, itself chec
 oracle/climb.py in test_gpu_parity.py) bit for bit: every field of the climb state after every step."""
 import dataclasses
 
+import numpy as np
+
 import pytest
 import torch
 
@@ -135,4 +137,31 @@ def test_lookahead_seed_sharded_two_ranks(tmp_path):
     ref = la.states(rounds)
     assert [ref[i].numpy().tobytes().hex() for i in range(ref.shape[0])] == got
     la.close()
+    s.close()
+
+
+def test_device_neighbour_lists_equal_host_rule():
+    """K3's warp-parallel neighbour generation (neighbors_warp) writes the same [K, neighbours(K), padding] list as
+    the host rule (slo_neighbors, and oracle/climb.py's neighbours: P:142, R21) for random and boundary K
+    on every stencil: a step whose aggregates are all invalid does not move, so it rewrites the list around K."""
+    import random
+    from oracle import climb
+    rng = random.Random(17)
+    s = sim.Simulator([inputs.preset_ll()], device=0)
+    dev = torch.device("cuda", 0)
+    for space in (inputs.SPACE_LIVE, inputs.SPACE_SIM, inputs.SPACE_WIDE32):
+        for trial in range(40):
+            lo, hi = space["lo"], space["hi"]
+            pick = (lambda d: rng.choice([lo[d], hi[d], rng.randrange(lo[d], hi[d] + 1)]))
+            K = inputs.knobs(conc=pick(0), max_num_seqs=pick(1), draft_len=pick(2), spec_on=rng.randrange(2),
+                             draft_width=pick(3), max_wait_us=pick(4))
+            cands = sim.knobs_tensor([K] + [inputs.PAD_KNOBS] * 31, device=dev)
+            aggs = torch.zeros((32, 32), dtype=torch.uint8, device=dev)           # n_seeds = 0: invalid
+            st = s.climb_state(K)
+            s.hillclimb_step(space, dict(inputs.SCORE_DEFAULTS), cands, aggs, 1, st)
+            torch.cuda.synchronize()
+            got = sim.unpack_knobs(cands.cpu().numpy().view(np.uint8).view(sim._lib.KNOB_DTYPE))
+            exp = [K] + climb.neighbours(space, K)
+            assert got[:len(exp)] == exp, (space["stencil"], K)
+            assert all(k["conc"] == 0 for k in got[len(exp):])          # padding: invalid records
     s.close()
