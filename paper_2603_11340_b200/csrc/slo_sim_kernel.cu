@@ -551,7 +551,7 @@ __device__ __forceinline__ void run_mode(const SimParams& p, int cls, uint8_t* w
   uint64_t t_idle = 0;
   uint32_t my_slo = 0;
   uint64_t my_sum = 0;
-  bool active = false, exhausted = false;
+  bool active = false, exhausted = count == 0;      // (an empty list: no cursor atomics)
   uint64_t pq = INF64;        // THINK: this lane's pending ready instant
   uint32_t pid = 0xFFFFFFFFu; // THINK: its user chain id
 
@@ -827,7 +827,7 @@ __device__ __forceinline__ void serve_mode(const SimParams& p, int cls, uint8_t*
   uint64_t alpha0 = 0, alpha1 = 0, t_idle = 0, my_sum = 0;
   uint32_t my_slo = 0;
   unsigned long long dsteps = 0;                       // decode steps (sum over batches of max S), lane 0
-  bool active = false, exhausted = (uint32_t)g >= p.gpw, closed = false, spec = false;
+  bool active = false, exhausted = (uint32_t)g >= p.gpw || count == 0, closed = false, spec = false;
   uint4 stg{0, 0, 0, 0};                               // K1g record of request gen + li, loaded ahead
 
   bool acq = true;
@@ -1081,6 +1081,7 @@ __device__ __forceinline__ void scan_mode(const SimParams& p, int cls, uint8_t* 
   const uint32_t N = p.warmup + p.seg;
   const uint32_t count = p.counts[cls];
   const uint32_t* list = p.lists + (size_t)cls * p.n_chunk;
+  if (count == 0) return;                             // (an empty list: no cursor atomics)
   for (;;) {
     uint32_t idx = 0;
     if (lane == 0) idx = atomicAdd(p.cursor + cls, 1u);
@@ -1283,7 +1284,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
   uint32_t r = 0, rowoff = 0, nq = 0, ndone = 0, gen = 0, it = 0, nrun = 0, npre = 0;
   uint32_t C = 0, B = 0, gamma = 0, noise = 0, k0 = 0, k1 = 0, alpha0 = 0, alpha1 = 0;
   uint64_t t = 0, s_next = INF64, a_w = 0;
-  bool active = false, exhausted = false, need_s = false, closed = false;
+  bool active = false, exhausted = count == 0, need_s = false, closed = false;
   // slot state (lane = one slot of the running set)
   bool run = false;
   // sleft: decode iterations the slot's request still runs; stot: its S (counters); fw: noise window
