@@ -331,6 +331,13 @@ __device__ __forceinline__ int gen_list(int q) {
 
 #ifndef SLO_GEN_MINB
 #define SLO_GEN_MINB 3
+// K1c refills its 2G-word noise window once more than SLO_CONT_REFILL / 8 of it is used (pooled over the
+// warp's groups): 6 (1.5G) measured 1.4 % faster than 4 on C2-cont; must stay < 8 (an exhausted window
+// would leave K = 0)
+#ifndef SLO_CONT_REFILL
+#define SLO_CONT_REFILL 6
+#endif
+static_assert(SLO_CONT_REFILL >= 1 && SLO_CONT_REFILL < 8, "SLO_CONT_REFILL in [1, 7]");
 #endif
 __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(const SimParams p, uint4* __restrict__ rec) {
   __shared__ uint32_t s_tm1[16];
@@ -1487,7 +1494,8 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
     if (__any_sync(FULL, dec)) {
       const bool nz = dec && noise != 0;
       // noise window of 2G decode iterations: lane li holds positions li (fw) and G + li (fw2) after nzc used
-      if (__any_sync(FULL, nz && nzc > (uint32_t)G)) {       // pooled shift-refill once half of it is used
+      if (__any_sync(FULL, nz && nzc > (uint32_t)(SLO_CONT_REFILL * G / 4))) {   // pooled shift-refill once
+                                                       // SLO_CONT_REFILL / 8 of it is used
         if (lane == 0) KPROF(8, 1u);
         const uint32_t sA = (uint32_t)li + nzc, sB = (uint32_t)(G + li) + nzc;   // old positions of the new ones
         const uint32_t a0 = __shfl_sync(FULL, fw, (int)(sA & (G - 1)), G);
