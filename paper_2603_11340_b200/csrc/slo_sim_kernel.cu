@@ -332,12 +332,15 @@ __device__ __forceinline__ int gen_list(int q) {
 #ifndef SLO_GEN_MINB
 #define SLO_GEN_MINB 3
 // K1c refills its 2G-word noise window once more than SLO_CONT_REFILL / 8 of it is used (pooled over the
-// warp's groups): 6 (1.5G) measured 1.4 % faster than 4 on C2-cont; must stay < 8 (an exhausted window
-// would leave K = 0)
+// warp's groups); with both ITER blocks of a lane drawn together (SLO_CONT_PAIRDRAW) 5 (1.25G) measured best
+// on C2-cont (4: +0.8 %, 6: +0.3 %, 7: +1 %); must stay < 8 (an exhausted window would leave K = 0)
 #ifndef SLO_CONT_REFILL
-#define SLO_CONT_REFILL 6
+#define SLO_CONT_REFILL 5
 #endif
 static_assert(SLO_CONT_REFILL >= 1 && SLO_CONT_REFILL < 8, "SLO_CONT_REFILL in [1, 7]");
+#ifndef SLO_CONT_PAIRDRAW
+#define SLO_CONT_PAIRDRAW 1
+#endif
 #endif
 __global__ void __launch_bounds__(kGenThreads, SLO_GEN_MINB) slo_gen_kernel(const SimParams p, uint4* __restrict__ rec) {
   __shared__ uint32_t s_tm1[16];
@@ -1502,6 +1505,13 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
         const uint32_t b0 = __shfl_sync(FULL, fw2, (int)(sA & (G - 1)), G);
         const uint32_t b1 = __shfl_sync(FULL, fw2, (int)(sB & (G - 1)), G);
         if (nz && nzc > 0) {
+#if SLO_CONT_PAIRDRAW
+          // both ITER blocks drawn together (two independent Philox chains interleave); kept only where new
+          const uint32_t na = noise_factor(philox(it + (uint32_t)li, 3, 0, 0, k0, k1).x, noise);
+          const uint32_t nb = noise_factor(philox(it + (uint32_t)(G + li), 3, 0, 0, k0, k1).x, noise);
+          fw = sA < (uint32_t)(2 * G) ? (sA < (uint32_t)G ? a0 : b0) : na;
+          fw2 = sB < (uint32_t)(2 * G) ? b1 : nb;
+#else
           if (sA < (uint32_t)(2 * G)) {
             fw = sA < (uint32_t)G ? a0 : b0;
           } else {                                       // ITER block it + li, word 0 (§2.12)
@@ -1512,6 +1522,7 @@ __device__ __forceinline__ void run_cont(const SimParams& p, int cls, uint8_t* w
           } else {                                       // ITER block it + G + li
             fw2 = noise_factor(philox(it + (uint32_t)(G + li), 3, 0, 0, k0, k1).x, noise);
           }
+#endif
           nzc = 0;
         }
       }
